@@ -1,0 +1,174 @@
+/*
+ * mxfft_b200.h -- C-ABI of the B200-native MX-FFT hot path (sm_100a).
+ *
+ * The reference (arxiv/paper_2512_04317, package `mxfft`, pure Python/NumPy)
+ * has no FFI: its boundary for this path is the Python API re-exported in
+ * pkg/src/mxfft/__init__.py:3-65.  Each entry point below replaces one
+ * reference function (cited as pkg/src/mxfft/<file>:<line>); the Python
+ * package paper_2512_04317_b200 binds them with ctypes and keeps the
+ * reference's names, argument meanings and exceptions.
+ *
+ * Conventions
+ *  - Every function returns an mxfft_status; mxfft_last_error() holds the
+ *    message of the most recent failure on the calling thread.
+ *  - Data pointers are DEVICE pointers unless a parameter says "host".
+ *    The caller allocates all memory (including workspace); the library only
+ *    owns plan tables.  No allocation happens on the transform path.
+ *  - `stream` is a cudaStream_t passed as uintptr_t (0 = legacy default).
+ *    All calls are stream-ordered and asynchronous unless stated otherwise.
+ *  - Complex data is interleaved (re, im): complex64 = 2 x float,
+ *    complex128 = 2 x double.
+ */
+#ifndef MXFFT_B200_H
+#define MXFFT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MXFFT_OK = 0,
+    MXFFT_ERR_INVALID_VALUE = 1,     /* errors.InvalidValue   (errors.py:8)  */
+    MXFFT_ERR_SHAPE = 2,             /* errors.ShapeError     (errors.py:12) */
+    MXFFT_ERR_UNSUPPORTED_SIZE = 3,  /* errors.UnsupportedSize(errors.py:16) */
+    MXFFT_ERR_VALUE = 4,             /* ValueError (bad direction / block size / argument) */
+    MXFFT_ERR_CUDA = 5,              /* RuntimeError (CUDA failure) */
+    MXFFT_ERR_MANTISSA_OVERFLOW = 6  /* errors.MantissaOverflow (errors.py:20) */
+} mxfft_status;
+
+/* Element format (minifloat.py:28-46).  policy: 0 = "ieee", 1 = "extended",
+ * 2 = "finite"; bias is the resolved bias (2^(E-1)-1 by default). */
+typedef struct {
+    int32_t exponent_bits;
+    int32_t mantissa_bits;
+    int32_t policy;
+    int32_t bias;
+} mxfft_format;
+
+/* Prescale configuration (PrescaleConfig, prescale.py:21-37). */
+typedef struct {
+    double target;
+    double tau;
+    double tau_min;
+    int32_t k_min;
+    int32_t k_max;
+} mxfft_prescale_cfg;
+
+/* One segment's prescale result (PrescaleResult, prescale.py:40-46).
+ * flags bit 0: a non-finite value was seen (InvalidValue);
+ * flags bit 1: log2 landed within a few ulps of a rounding boundary, so the
+ *              host must confirm k with its own log2 (measure-zero case). */
+typedef struct {
+    double a_max;
+    double p_tau;
+    int32_t k1;
+    int32_t k2;
+    int32_t k;
+    int32_t flags;
+    int64_t nnz;
+} mxfft_prescale_result;
+
+typedef struct mxfft_plan_s* mxfft_plan;
+
+int32_t mxfft_version(void);
+const char* mxfft_last_error(void);
+
+/* quantize_array (minifloat.py:105-120): RNE onto the format grid with
+ * saturation, FP64 in/out (n values).  *d_nonfinite (device int32) is set
+ * to 1 when a non-finite input is seen (the host raises InvalidValue). */
+int32_t mxfft_quantize_f64(const double* x, double* out, int64_t n, const mxfft_format* fmt,
+                           int32_t* d_nonfinite, uintptr_t stream);
+
+/* block_scales + encode (mxblock.py:27-51 / fftcore.py:131-147), batched:
+ * v: FP64 (nblocks, block_len) -> codes FP64 (nblocks, block_len), scales FP64 (nblocks). */
+int32_t mxfft_mx_encode_f64(const double* v, int64_t nblocks, int32_t block_len,
+                            const mxfft_format* fmt, double* codes, double* scales,
+                            int32_t* d_nonfinite, uintptr_t stream);
+
+/* decode_block_mx (mxblock.py:86-90), batched: codes (nblocks, block_len) with
+ * block_len even, scales (nblocks) -> complex128 (nblocks, block_len/2). */
+int32_t mxfft_mx_decode_f64(const double* codes, const double* scales, int64_t nblocks,
+                            int32_t block_len, double* out, uintptr_t stream);
+
+/* FftPlan(n, ModeSpec.mx(fmt, block_size)) (fftcore.py:84-121).
+ * h_twiddles: HOST complex128 (stages, n/2) twiddles in butterfly order, built by
+ * the caller with the reference's own NumPy expression (fftcore.py:101-105); the
+ * library encodes them on the device (fftcore.py:108-113).  Synchronous. */
+int32_t mxfft_plan_create(mxfft_plan* plan, int32_t n, const mxfft_format* fmt,
+                          int32_t block_size, const double* h_twiddles, uintptr_t stream);
+int32_t mxfft_plan_destroy(mxfft_plan plan);
+
+/* Read the encoded twiddles back to HOST arrays: codes (stages, n/2) x2 and
+ * scales (stages, n/2/cpb) -- plan.mx_twiddles of the reference.  Synchronous. */
+int32_t mxfft_plan_twiddles(mxfft_plan plan, double* h_codes_re, double* h_codes_im,
+                            double* h_scales);
+
+/* Batched 1-D MX transform along contiguous rows (_fft_batch_mx,
+ * fftcore.py:259-282): x, y complex64 (batch, n); x may alias y. */
+int32_t mxfft_fft_rows(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t inverse,
+                       uintptr_t stream);
+
+/* Batched 1-D MX transform along the COLUMNS of `batch` n x n complex64 images
+ * (the second pass of fft_2d, fftcore.py:352, without materialising rows.T);
+ * x may alias y.  With mxfft_fft_rows this gives either pass of fft_2d alone. */
+int32_t mxfft_fft_cols(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t inverse,
+                       uintptr_t stream);
+
+/* Batched 2-D MX transform (fft_2d, fftcore.py:344-353 = rows then columns) of
+ * `batch` n x n complex64 images; x may alias y.
+ *   mode 0: forward; 1: inverse; 2: round trip = forward, inverse, x 1/n^2
+ *           (roundtrip_pipeline's per-coil body, mri.py:100-105).
+ *   d_k:    optional per-image int32 prescale exponents (device).  Image i is
+ *           multiplied by 2^k[i / k_group] on load (apply_prescale,
+ *           prescale.py:76-86) and the result by 2^-k on store (undo_prescale,
+ *           prescale.py:89-91).  NULL = no prescale.
+ * Exact in FP32 (power-of-two scalings) while results stay in FP32 range. */
+int32_t mxfft_fft2(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t mode,
+                   const int32_t* d_k, int32_t k_group, uintptr_t stream);
+
+/* compute_prescale (prescale.py:61-73) over `nseg` segments of `seg_points`
+ * complex values each (complex64 when is_c128 == 0, else complex128),
+ * contiguous.  Writes one mxfft_prescale_result per segment to d_out and, when
+ * d_k is not NULL, the applied exponent k to d_k[seg].  workspace: device
+ * buffer of at least mxfft_prescale_workspace_bytes(nseg, seg_points) bytes. */
+int32_t mxfft_prescale_stats(const void* x, int32_t is_c128, int64_t nseg, int64_t seg_points,
+                             const mxfft_prescale_cfg* cfg, mxfft_prescale_result* d_out,
+                             int32_t* d_k, void* workspace, int64_t workspace_bytes,
+                             uintptr_t stream);
+int64_t mxfft_prescale_workspace_bytes(int64_t nseg, int64_t seg_points);
+
+/* Root-sum-square coil combine (rss, mri.py:70-81) of per-coil complex images
+ * (complex64 when is_c128 == 0, else complex128): x (groups, coils, npix) ->
+ * FP64 (groups, npix).  |z| is computed exactly as numpy's np.abs(complex128). */
+int32_t mxfft_rss(const void* x, int32_t is_c128, int64_t groups, int32_t coils, int64_t npix,
+                  double* out, uintptr_t stream);
+
+/* Test instrumentation: run the 1-D row transform stage by stage through the
+ * same device code as mxfft_fft_rows and record, per stage s (arrays laid out
+ * [stage][batch][...]): v-block scale exponents v_exp (int32, n/2/cpb per row),
+ * v codes (float, n/2 x 2), product exponents p_exp and shifts p_shift (int32),
+ * product codes p_codes (float, n/2 x 2) and the stage output (complex64, n).
+ * Any output pointer may be NULL.  y receives the final output. */
+int32_t mxfft_fft_rows_debug(mxfft_plan plan, const void* x, void* y, int64_t batch,
+                             int32_t inverse, int32_t* v_exp, float* v_codes, int32_t* p_exp,
+                             int32_t* p_shift, float* p_codes, void* stage_out, uintptr_t stream);
+
+/* Test instrumentation: compare the hardware quantizer used inside the
+ * transform (F2FP.SATFINITE pack + unpack) with the reference-literal FP64
+ * quantizer over all 2^32 FP32 bit patterns (non-finite skipped).  Adds the
+ * mismatch count to *d_mismatches and atomicMin's the first bad pattern into
+ * *d_first_bad (device pointers; initialise to 0 / 0xffffffff). */
+int32_t mxfft_selftest_hw_quantizer(const mxfft_format* fmt, uint64_t* d_mismatches,
+                                    uint32_t* d_first_bad, uintptr_t stream);
+
+/* Total number of kernels this library has launched in the process
+ * (bookkeeping for the benchmark's gpu_launches count). */
+int64_t mxfft_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MXFFT_B200_H */

@@ -1,0 +1,115 @@
+"""ctypes binding of the C-ABI library (include/mxfft_b200.h).
+
+The product has no CPU fallback: importing a compute entry point without the
+built ``_lib/libmxfft_b200.so`` or without a CUDA device raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import errors
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libmxfft_b200.so")
+
+_lib = None
+
+
+class FormatC(ctypes.Structure):
+    _fields_ = [("exponent_bits", ctypes.c_int32), ("mantissa_bits", ctypes.c_int32),
+                ("policy", ctypes.c_int32), ("bias", ctypes.c_int32)]
+
+
+class PrescaleCfgC(ctypes.Structure):
+    _fields_ = [("target", ctypes.c_double), ("tau", ctypes.c_double),
+                ("tau_min", ctypes.c_double), ("k_min", ctypes.c_int32),
+                ("k_max", ctypes.c_int32)]
+
+
+# mxfft_prescale_result, as a numpy structured dtype (40 bytes, C layout)
+PRESCALE_RESULT_DTYPE = np.dtype([("a_max", "<f8"), ("p_tau", "<f8"), ("k1", "<i4"),
+                                  ("k2", "<i4"), ("k", "<i4"), ("flags", "<i4"),
+                                  ("nnz", "<i8")])
+
+# exported symbols and their signatures (argtypes, restype)
+_vp, _i32, _i64, _u = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+_fp = ctypes.POINTER(FormatC)
+SIGNATURES = {
+    "mxfft_version": ([], _i32),
+    "mxfft_last_error": ([], ctypes.c_char_p),
+    "mxfft_launch_count": ([], _i64),
+    "mxfft_quantize_f64": ([_vp, _vp, _i64, _fp, _vp, _u], _i32),
+    "mxfft_mx_encode_f64": ([_vp, _i64, _i32, _fp, _vp, _vp, _vp, _u], _i32),
+    "mxfft_mx_decode_f64": ([_vp, _vp, _i64, _i32, _vp, _u], _i32),
+    "mxfft_plan_create": ([ctypes.POINTER(_vp), _i32, _fp, _i32, _vp, _u], _i32),
+    "mxfft_plan_destroy": ([_vp], _i32),
+    "mxfft_plan_twiddles": ([_vp, _vp, _vp, _vp], _i32),
+    "mxfft_fft_rows": ([_vp, _vp, _vp, _i64, _i32, _u], _i32),
+    "mxfft_fft_cols": ([_vp, _vp, _vp, _i64, _i32, _u], _i32),
+    "mxfft_fft2": ([_vp, _vp, _vp, _i64, _i32, _vp, _i32, _u], _i32),
+    "mxfft_prescale_stats": ([_vp, _i32, _i64, _i64, ctypes.POINTER(PrescaleCfgC), _vp, _vp,
+                              _vp, _i64, _u], _i32),
+    "mxfft_prescale_workspace_bytes": ([_i64, _i64], _i64),
+    "mxfft_rss": ([_vp, _i32, _i64, _i32, _i64, _vp, _u], _i32),
+    "mxfft_selftest_hw_quantizer": ([_fp, _vp, _vp, _u], _i32),
+    "mxfft_fft_rows_debug": ([_vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _u], _i32),
+}
+
+
+def load():
+    """Load the shared library (no CUDA needed just to load)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"CUDA extension not built: {LIB_PATH} is missing "
+                "(run __graft_entry__.build() or `make -C paper_2512_04317_b200/csrc`)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (argt, rest) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.argtypes = argt
+            fn.restype = rest
+        _lib = L
+    return _lib
+
+
+def lib():
+    """The library, for compute calls: also requires a CUDA device."""
+    L = load()
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2512_04317_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    return L
+
+
+_STATUS = {
+    1: errors.InvalidValue,
+    2: errors.ShapeError,
+    3: errors.UnsupportedSize,
+    4: ValueError,
+    5: RuntimeError,
+    6: errors.MantissaOverflow,
+}
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = load().mxfft_last_error().decode(errors="replace")
+        raise _STATUS.get(rc, RuntimeError)(msg)
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def launch_count() -> int:
+    return int(load().mxfft_launch_count())

@@ -1,0 +1,349 @@
+// mxfft_capi.cu -- extern "C" entry points declared in include/mxfft_b200.h.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/mxfft_b200.h"
+#include "mxfft_common.cuh"
+#include "mxfft_internal.h"
+
+namespace mxfft {
+static std::atomic<long long> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+cudaError_t plan_encode(Plan& p, const double* d_tw, cudaStream_t st);
+cudaError_t launch_prescale(const void* x, int is_c128, int64_t nseg, int64_t npts,
+                            const mxfft_prescale_cfg& c, mxfft_prescale_result* out, int32_t* kvec,
+                            cudaStream_t st);
+}  // namespace mxfft
+
+using namespace mxfft;
+
+struct mxfft_plan_s {
+    Plan p;
+};
+
+static thread_local std::string g_err;
+
+static int32_t fail(int32_t code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+static int32_t cuda_fail(cudaError_t e, const char* where) {
+    return fail(MXFFT_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call, where)                                   \
+    do {                                                  \
+        cudaError_t _e = (call);                          \
+        if (_e != cudaSuccess) return cuda_fail(_e, where); \
+    } while (0)
+
+static bool check_fmt(const mxfft_format* f, std::string& why) {
+    if (!f) {
+        why = "null format";
+        return false;
+    }
+    if (f->exponent_bits < 2) {
+        why = "exponent_bits must be >= 2";
+        return false;
+    }
+    if (f->mantissa_bits < 1) {
+        why = "mantissa_bits must be >= 1";
+        return false;
+    }
+    if (f->policy < 0 || f->policy > 2) {
+        why = "unknown policy";
+        return false;
+    }
+    if (f->exponent_bits > 11 || f->mantissa_bits > 52) {
+        why = "format wider than FP64 is not supported";
+        return false;
+    }
+    return true;
+}
+
+static FmtDesc desc_of(const mxfft_format* f) {
+    return make_fmt(f->exponent_bits, f->mantissa_bits, f->policy, f->bias);
+}
+
+static int ilog2(int64_t n) {
+    int s = 0;
+    while ((int64_t(1) << s) < n) ++s;
+    return s;
+}
+
+extern "C" {
+
+int32_t mxfft_version(void) { return 1; }
+
+const char* mxfft_last_error(void) { return g_err.c_str(); }
+
+int64_t mxfft_launch_count(void) { return g_launches.load(); }
+
+int32_t mxfft_quantize_f64(const double* x, double* out, int64_t n, const mxfft_format* fmt,
+                           int32_t* d_nonfinite, uintptr_t stream) {
+    std::string why;
+    if (!check_fmt(fmt, why)) return fail(MXFFT_ERR_VALUE, why);
+    if (n < 0) return fail(MXFFT_ERR_SHAPE, "negative length");
+    CK(launch_quantize_f64(x, out, n, desc_of(fmt), d_nonfinite, (cudaStream_t)stream),
+       "quantize_f64");
+    return MXFFT_OK;
+}
+
+int32_t mxfft_mx_encode_f64(const double* v, int64_t nblocks, int32_t block_len,
+                            const mxfft_format* fmt, double* codes, double* scales,
+                            int32_t* d_nonfinite, uintptr_t stream) {
+    std::string why;
+    if (!check_fmt(fmt, why)) return fail(MXFFT_ERR_VALUE, why);
+    if (block_len < 1 || nblocks < 0) return fail(MXFFT_ERR_SHAPE, "block must be non-empty");
+    CK(launch_encode_f64(v, nblocks, block_len, desc_of(fmt), codes, scales, nullptr, d_nonfinite,
+                         (cudaStream_t)stream),
+       "mx_encode_f64");
+    return MXFFT_OK;
+}
+
+int32_t mxfft_mx_decode_f64(const double* codes, const double* scales, int64_t nblocks,
+                            int32_t block_len, double* out, uintptr_t stream) {
+    if (block_len % 2 != 0) return fail(MXFFT_ERR_SHAPE, "complex block length must be even");
+    CK(launch_decode_f64(codes, scales, nblocks, block_len, out, (cudaStream_t)stream),
+       "mx_decode_f64");
+    return MXFFT_OK;
+}
+
+int32_t mxfft_plan_create(mxfft_plan* plan, int32_t n, const mxfft_format* fmt,
+                          int32_t block_size, const double* h_twiddles, uintptr_t stream) {
+    if (!plan) return fail(MXFFT_ERR_VALUE, "null plan pointer");
+    *plan = nullptr;
+    if (n < 2 || (n & (n - 1)))
+        return fail(MXFFT_ERR_UNSUPPORTED_SIZE,
+                    "transform length must be a power of two >= 2, got " + std::to_string(n));
+    if (block_size < 2 || block_size % 2)
+        return fail(MXFFT_ERR_VALUE, "block_size must be an even integer >= 2");
+    std::string why;
+    if (!check_fmt(fmt, why)) return fail(MXFFT_ERR_VALUE, why);
+    const int m = n / 2;
+    const int cpb = std::min(block_size / 2, m);  // fftcore.py:109
+    if (m % cpb != 0)
+        return fail(MXFFT_ERR_VALUE, "block_size/2 must divide n/2 (fftcore.py:139-141 reshape)");
+    auto* h = new mxfft_plan_s;
+    Plan& p = h->p;
+    p.n = n;
+    p.log2n = ilog2(n);
+    p.block_size = block_size;
+    p.cpb = cpb;
+    p.fmt = desc_of(fmt);
+    const int st = p.log2n;
+    const int nb = m / cpb;
+    cudaStream_t s = (cudaStream_t)stream;
+    double* d_tw = nullptr;
+    cudaError_t e;
+    if ((e = cudaMalloc(&p.d_wcr, sizeof(double) * st * m)) != cudaSuccess ||
+        (e = cudaMalloc(&p.d_wci, sizeof(double) * st * m)) != cudaSuccess ||
+        (e = cudaMalloc(&p.d_wsexp, sizeof(int) * st * nb)) != cudaSuccess ||
+        (e = cudaMalloc(&p.d_tw_fwd, sizeof(float2) * n)) != cudaSuccess ||
+        (e = cudaMalloc(&p.d_tw_inv, sizeof(float2) * n)) != cudaSuccess ||
+        (e = cudaMalloc(&p.d_tw_exp, sizeof(int) * n)) != cudaSuccess ||
+        (e = cudaMalloc(&d_tw, sizeof(double) * 2 * st * m)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(d_tw, h_twiddles, sizeof(double) * 2 * st * m,
+                             cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+        (e = plan_encode(p, d_tw, s)) != cudaSuccess || (e = cudaStreamSynchronize(s)) != cudaSuccess) {
+        cudaFree(d_tw);
+        mxfft_plan_destroy(h);
+        return cuda_fail(e, "plan_create");
+    }
+    cudaFree(d_tw);
+    *plan = h;
+    return MXFFT_OK;
+}
+
+int32_t mxfft_plan_destroy(mxfft_plan plan) {
+    if (!plan) return MXFFT_OK;
+    Plan& p = plan->p;
+    cudaFree(p.d_wcr);
+    cudaFree(p.d_wci);
+    cudaFree(p.d_wsexp);
+    cudaFree(p.d_tw_fwd);
+    cudaFree(p.d_tw_inv);
+    cudaFree(p.d_tw_exp);
+    delete plan;
+    return MXFFT_OK;
+}
+
+int32_t mxfft_plan_twiddles(mxfft_plan plan, double* h_codes_re, double* h_codes_im,
+                            double* h_scales) {
+    if (!plan) return fail(MXFFT_ERR_VALUE, "null plan");
+    const Plan& p = plan->p;
+    const int m = p.n / 2, nb = m / p.cpb, st = p.log2n;
+    CK(cudaMemcpy(h_codes_re, p.d_wcr, sizeof(double) * st * m, cudaMemcpyDeviceToHost), "plan_twiddles");
+    CK(cudaMemcpy(h_codes_im, p.d_wci, sizeof(double) * st * m, cudaMemcpyDeviceToHost), "plan_twiddles");
+    int* tmp = new int[st * nb];
+    cudaError_t e = cudaMemcpy(tmp, p.d_wsexp, sizeof(int) * st * nb, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess)
+        for (int i = 0; i < st * nb; ++i) h_scales[i] = std::ldexp(1.0, tmp[i]);
+    delete[] tmp;
+    if (e != cudaSuccess) return cuda_fail(e, "plan_twiddles");
+    return MXFFT_OK;
+}
+
+int32_t mxfft_fft_rows(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t inverse,
+                       uintptr_t stream) {
+    if (!plan) return fail(MXFFT_ERR_VALUE, "null plan");
+    if (batch < 0) return fail(MXFFT_ERR_SHAPE, "negative batch");
+    if (batch == 0) return MXFFT_OK;
+    LinePass lp;
+    lp.in = x;
+    lp.out = y;
+    lp.col_mode = 0;
+    lp.lines_per_image = 1;
+    lp.total_lines = batch;
+    lp.img_elems = plan->p.n;
+    lp.inverse = inverse ? 1 : 0;
+    CK(run_lines(plan->p, lp, (cudaStream_t)stream), "fft_rows");
+    return MXFFT_OK;
+}
+
+int32_t mxfft_fft_cols(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t inverse,
+                       uintptr_t stream) {
+    if (!plan) return fail(MXFFT_ERR_VALUE, "null plan");
+    if (batch < 0) return fail(MXFFT_ERR_SHAPE, "negative batch");
+    if (batch == 0) return MXFFT_OK;
+    LinePass lp;
+    lp.in = x;
+    lp.out = y;
+    lp.col_mode = 1;
+    lp.img_elems = (int64_t)plan->p.n * plan->p.n;
+    lp.lines_per_image = plan->p.n;
+    lp.total_lines = batch * plan->p.n;
+    lp.batch = batch;
+    lp.inverse = inverse ? 1 : 0;
+    CK(run_lines(plan->p, lp, (cudaStream_t)stream), "fft_cols");
+    return MXFFT_OK;
+}
+
+int32_t mxfft_fft2(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t mode,
+                   const int32_t* d_k, int32_t k_group, uintptr_t stream) {
+    if (!plan) return fail(MXFFT_ERR_VALUE, "null plan");
+    if (mode < 0 || mode > 2) return fail(MXFFT_ERR_VALUE, "mode must be 0 (forward), 1 (inverse) or 2 (round trip)");
+    if (batch < 0) return fail(MXFFT_ERR_SHAPE, "negative batch");
+    if (batch == 0) return MXFFT_OK;
+    const Plan& p = plan->p;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nn = (int64_t)p.n * p.n;
+    const int npass = mode == 2 ? 4 : 2;
+    for (int pass = 0; pass < npass; ++pass) {
+        LinePass lp;
+        lp.in = pass == 0 ? x : y;
+        lp.out = y;
+        lp.col_mode = pass & 1;
+        lp.img_elems = nn;
+        lp.lines_per_image = p.n;
+        lp.total_lines = batch * p.n;
+        lp.batch = batch;
+        lp.inverse = mode == 1 || (mode == 2 && pass >= 2);
+        lp.kvec = d_k;
+        lp.k_group = k_group > 0 ? k_group : 1;
+        if (pass == 0 && d_k) lp.kin_sign = 1;
+        if (pass == npass - 1) {
+            if (d_k) lp.kout_sign = -1;
+            if (mode == 2) lp.kout_const = -2 * p.log2n;  // x 1/n^2 (mri.py:100)
+        }
+        CK(run_lines(p, lp, s), "fft2");
+    }
+    return MXFFT_OK;
+}
+
+int64_t mxfft_prescale_workspace_bytes(int64_t nseg, int64_t seg_points) {
+    (void)nseg;
+    (void)seg_points;
+    return 0;
+}
+
+int32_t mxfft_prescale_stats(const void* x, int32_t is_c128, int64_t nseg, int64_t seg_points,
+                             const mxfft_prescale_cfg* cfg, mxfft_prescale_result* d_out,
+                             int32_t* d_k, void* workspace, int64_t workspace_bytes,
+                             uintptr_t stream) {
+    (void)workspace;
+    (void)workspace_bytes;
+    if (!cfg) return fail(MXFFT_ERR_VALUE, "null config");
+    if (nseg < 0 || seg_points < 0) return fail(MXFFT_ERR_SHAPE, "negative size");
+    if (nseg == 0) return MXFFT_OK;
+    if (seg_points > (int64_t)0x7fffffff) return fail(MXFFT_ERR_UNSUPPORTED_SIZE, "segment too large");
+    CK(launch_prescale(x, is_c128, nseg, seg_points, *cfg, d_out, d_k, (cudaStream_t)stream),
+       "prescale_stats");
+    return MXFFT_OK;
+}
+
+int32_t mxfft_rss(const void* x, int32_t is_c128, int64_t groups, int32_t coils, int64_t npix,
+                  double* out, uintptr_t stream) {
+    if (coils < 1) return fail(MXFFT_ERR_SHAPE, "need at least one coil");
+    CK(launch_rss(x, is_c128, groups, coils, npix, out, (cudaStream_t)stream), "rss");
+    return MXFFT_OK;
+}
+
+int32_t mxfft_fft_rows_debug(mxfft_plan plan, const void* x, void* y, int64_t batch,
+                             int32_t inverse, int32_t* v_exp, float* v_codes, int32_t* p_exp,
+                             int32_t* p_shift, float* p_codes, void* stage_out, uintptr_t stream) {
+    if (!plan) return fail(MXFFT_ERR_VALUE, "null plan");
+    const Plan& p = plan->p;
+    if (!fast_path_ok(p)) return fail(MXFFT_ERR_VALUE, "debug capture needs a fast-path plan");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t m = p.n / 2, nb = m / p.cpb, st = p.log2n;
+    // scratch for any dump array the caller did not ask for
+    int32_t *ve = v_exp, *pe = p_exp, *ps = p_shift;
+    float *vc = v_codes, *pc = p_codes;
+    void* scratch[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    const size_t nbx = sizeof(int32_t) * st * batch * nb, ncx = sizeof(float) * 2 * st * batch * m;
+    if (!ve) { CK(cudaMalloc(&scratch[0], nbx), "debug"); ve = (int32_t*)scratch[0]; }
+    if (!pe) { CK(cudaMalloc(&scratch[1], nbx), "debug"); pe = (int32_t*)scratch[1]; }
+    if (!ps) { CK(cudaMalloc(&scratch[2], nbx), "debug"); ps = (int32_t*)scratch[2]; }
+    if (!vc) { CK(cudaMalloc(&scratch[3], ncx), "debug"); vc = (float*)scratch[3]; }
+    if (!pc) { CK(cudaMalloc(&scratch[4], ncx), "debug"); pc = (float*)scratch[4]; }
+    LinePass lp;
+    lp.in = x;
+    lp.out = y;
+    lp.col_mode = 0;
+    lp.lines_per_image = 1;
+    lp.total_lines = batch;
+    lp.img_elems = p.n;
+    lp.inverse = inverse ? 1 : 0;
+    lp.d_vexp = ve;
+    lp.d_vcodes = vc;
+    lp.d_pexp = pe;
+    lp.d_pshift = ps;
+    lp.d_pcodes = pc;
+    cudaError_t e = run_lines(p, lp, s);
+    if (e == cudaSuccess && stage_out) {
+        for (int k = 0; k < st && e == cudaSuccess; ++k) {
+            LinePass l2 = lp;
+            l2.d_vexp = nullptr;
+            l2.d_vcodes = nullptr;
+            l2.d_pexp = nullptr;
+            l2.d_pshift = nullptr;
+            l2.d_pcodes = nullptr;
+            l2.stage_limit = k + 1;
+            l2.out = reinterpret_cast<float2*>(stage_out) + (int64_t)k * batch * p.n;
+            e = run_lines(p, l2, s);
+        }
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    for (void* q : scratch) cudaFree(q);
+    if (e != cudaSuccess) return cuda_fail(e, "fft_rows_debug");
+    return MXFFT_OK;
+}
+
+}  // extern "C"
+
+extern "C" int32_t mxfft_selftest_hw_quantizer(const mxfft_format* fmt, uint64_t* d_mismatches,
+                                               uint32_t* d_first_bad, uintptr_t stream) {
+    std::string why;
+    if (!check_fmt(fmt, why)) return fail(MXFFT_ERR_VALUE, why);
+    FmtDesc f = desc_of(fmt);
+    if (f.id == F_GENERIC) return fail(MXFFT_ERR_VALUE, "format has no hardware quantizer");
+    CK(launch_selftest_hwq(f, reinterpret_cast<unsigned long long*>(d_mismatches), d_first_bad,
+                           (cudaStream_t)stream),
+       "selftest_hw_quantizer");
+    return MXFFT_OK;
+}

@@ -1,0 +1,251 @@
+// mxfft_codec.cu -- element/MX block codec kernels, plan-table construction, RSS.
+//
+// These serve the public codec API (quantize_array, encode_block_mx,
+// decode_block_mx) and plan creation.  They use the reference-literal FP64
+// quantizer (quantize_ref == minifloat.py:114-120) because the API takes FP64
+// inputs: rounding FP64 -> FP32 before a hardware cvt would double-round.
+#include "mxfft_common.cuh"
+#include "mxfft_internal.h"
+
+namespace mxfft {
+
+__global__ void k_quantize_f64(const double* __restrict__ x, double* __restrict__ out, int64_t n,
+                               FmtDesc f, int32_t* nonfinite) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = x[i];
+        if (!isfinite(v)) {
+            if (nonfinite) *nonfinite = 1;
+            out[i] = 0.0;
+            continue;
+        }
+        out[i] = quantize_ref(v, f);
+    }
+}
+
+static int grid_for(int64_t n, int threads) {
+    int64_t g = (n + threads - 1) / threads;
+    if (g > 148 * 32) g = 148 * 32;
+    return (int)(g < 1 ? 1 : g);
+}
+
+cudaError_t launch_quantize_f64(const double* x, double* out, int64_t n, const FmtDesc& f,
+                                int32_t* d_nonfinite, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_quantize_f64<<<grid_for(n, 256), 256, 0, st>>>(x, out, n, f, d_nonfinite);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// encode_block_mx (mxblock.py:41-51), one warp per block.
+__global__ void k_encode_f64(const double* __restrict__ v, int64_t nblocks, int len, FmtDesc f,
+                             double* __restrict__ codes, double* __restrict__ scales,
+                             int* __restrict__ scale_exp, int32_t* nonfinite) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t b = warp; b < nblocks; b += nwarps) {
+        const double* x = v + b * len;
+        double amax = 0.0;
+        int bad = 0;
+        for (int i = lane; i < len; i += 32) {
+            const double a = x[i];
+            bad |= !isfinite(a);
+            amax = fmax(amax, fabs(a));
+        }
+        for (int o = 16; o; o >>= 1) {
+            amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+            bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+        }
+        if (bad) {
+            if (lane == 0 && nonfinite) *nonfinite = 1;
+            continue;
+        }
+        const int se = block_scale_exp(amax, f);
+        const double inv = ldexp(1.0, -se);
+        for (int i = lane; i < len; i += 32) codes[b * len + i] = quantize_ref(x[i] * inv, f);
+        if (lane == 0) {
+            if (scales) scales[b] = ldexp(1.0, se);
+            if (scale_exp) scale_exp[b] = se;
+        }
+    }
+}
+
+cudaError_t launch_encode_f64(const double* v, int64_t nblocks, int block_len, const FmtDesc& f,
+                              double* codes, double* scales, int* scale_exp, int32_t* d_nonfinite,
+                              cudaStream_t st) {
+    if (nblocks <= 0) return cudaSuccess;
+    k_encode_f64<<<grid_for(nblocks * 32, 256), 256, 0, st>>>(v, nblocks, block_len, f, codes,
+                                                               scales, scale_exp, d_nonfinite);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// decode_block_mx (mxblock.py:86-90): (codes[0::2] + i codes[1::2]) * scale
+__global__ void k_decode_f64(const double* __restrict__ codes, const double* __restrict__ scales,
+                             int64_t nblocks, int len, double* __restrict__ out) {
+    const int64_t half = len / 2;
+    const int64_t total = nblocks * half;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / half, j = i - b * half;
+        const double s = scales[b];
+        out[2 * i] = codes[b * len + 2 * j] * s;
+        out[2 * i + 1] = codes[b * len + 2 * j + 1] * s;
+    }
+}
+
+cudaError_t launch_decode_f64(const double* codes, const double* scales, int64_t nblocks,
+                              int block_len, double* out, cudaStream_t st) {
+    if (nblocks <= 0) return cudaSuccess;
+    k_decode_f64<<<grid_for(nblocks * (block_len / 2), 256), 256, 0, st>>>(codes, scales, nblocks,
+                                                                          block_len, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// Twiddle encoding (fftcore.py:108-113 -> _encode_blocks_batch): one thread per
+// (stage, block); tw: complex128 (stages, m) in butterfly order.
+__global__ void k_plan_encode(const double* __restrict__ tw, int stages, int m, int cpb, FmtDesc f,
+                              double* wcr, double* wci, int* wsexp) {
+    const int nb = m / cpb;
+    const int64_t total = (int64_t)stages * nb;
+    for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+         id += (int64_t)gridDim.x * blockDim.x) {
+        const int s = (int)(id / nb), k = (int)(id % nb);
+        const double* w = tw + 2 * ((int64_t)s * m + (int64_t)k * cpb);
+        double amax = 0.0;
+        for (int j = 0; j < cpb; ++j) amax = fmax(amax, fmax(fabs(w[2 * j]), fabs(w[2 * j + 1])));
+        const int se = block_scale_exp(amax, f);
+        const double inv = ldexp(1.0, -se);
+        for (int j = 0; j < cpb; ++j) {
+            const int64_t o = (int64_t)s * m + (int64_t)k * cpb + j;
+            wcr[o] = quantize_ref(w[2 * j] * inv, f);
+            wci[o] = quantize_ref(w[2 * j + 1] * inv, f);
+        }
+        wsexp[id] = se;
+    }
+}
+
+// Compressed kernel tables: stage s, j < 2^s at offset 2^s - 1.  Butterfly t = j
+// of group 0 carries twiddle j; its block is j / cpb (fftcore.py:101-113).
+__global__ void k_plan_compress(const double* wcr, const double* wci, const int* wsexp, int stages,
+                                int m, int cpb, float2* tw_fwd, float2* tw_inv, int* tw_exp) {
+    const int nb = m / cpb;
+    const int total = (1 << stages) - 1;
+    for (int id = blockIdx.x * blockDim.x + threadIdx.x; id < total; id += gridDim.x * blockDim.x) {
+        const int s = 31 - __clz(id + 1);
+        const int j = id - ((1 << s) - 1);
+        const float r = (float)wcr[(int64_t)s * m + j], im = (float)wci[(int64_t)s * m + j];
+        tw_fwd[id] = make_float2(r, im);
+        tw_inv[id] = make_float2(r, -im);
+        tw_exp[id] = wsexp[(int64_t)s * nb + j / cpb];
+    }
+}
+
+cudaError_t plan_encode(Plan& p, const double* d_tw, cudaStream_t st) {
+    const int m = p.n / 2;
+    const int nb = m / p.cpb;
+    const int64_t total = (int64_t)p.log2n * nb;
+    k_plan_encode<<<grid_for(total, 128), 128, 0, st>>>(d_tw, p.log2n, m, p.cpb, p.fmt, p.d_wcr,
+                                                        p.d_wci, p.d_wsexp);
+    note_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int tot = p.n - 1;
+    k_plan_compress<<<grid_for(tot, 256), 256, 0, st>>>(p.d_wcr, p.d_wci, p.d_wsexp, p.log2n, m,
+                                                         p.cpb, p.d_tw_fwd, p.d_tw_inv, p.d_tw_exp);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// |z| exactly as numpy 2.3.5 computes np.abs(complex128) on FMA hosts:
+// larger * sqrt(fma(r, r, 1)), r = smaller / larger (IEEE-rounded ops only).
+__device__ __forceinline__ double np_cabs(double re, double im) {
+    const double a = fabs(re), b = fabs(im);
+    const double larger = fmax(a, b), smaller = fmin(a, b);
+    if (larger == 0.0) return 0.0;
+    const double r = __ddiv_rn(smaller, larger);
+    return __dmul_rn(__dsqrt_rn(__fma_rn(r, r, 1.0)), larger);
+}
+
+// rss (mri.py:70-81): sqrt(sum_c |T_c|^2), coils accumulated in order.
+template <typename T>
+__global__ void k_rss(const T* __restrict__ x, int64_t groups, int coils, int64_t npix,
+                      double* __restrict__ out) {
+    const int64_t total = groups * npix;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = i / npix, p = i - g * npix;
+        double acc = 0.0;
+        for (int c = 0; c < coils; ++c) {
+            const T v = x[(g * coils + c) * npix + p];
+            const double m = np_cabs((double)v.x, (double)v.y);
+            const double sq = __dmul_rn(m, m);
+            acc = c == 0 ? sq : __dadd_rn(acc, sq);
+        }
+        out[i] = __dsqrt_rn(acc);
+    }
+}
+
+cudaError_t launch_rss(const void* x, int is_c128, int64_t groups, int coils, int64_t npix,
+                       double* out, cudaStream_t st) {
+    if (groups * npix <= 0) return cudaSuccess;
+    if (is_c128)
+        k_rss<double2><<<grid_for(groups * npix, 256), 256, 0, st>>>(
+            reinterpret_cast<const double2*>(x), groups, coils, npix, out);
+    else
+        k_rss<float2><<<grid_for(groups * npix, 256), 256, 0, st>>>(
+            reinterpret_cast<const float2*>(x), groups, coils, npix, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace mxfft
+
+namespace mxfft {
+
+// Self-test (test instrumentation): for every finite FP32 bit pattern x, compare
+// the hardware quantizer used inside the transform (HwFmt<ID>::q2) with the
+// reference-literal FP64 quantizer (quantize_ref); count mismatches.
+template <int ID>
+__global__ void k_selftest_hwq(FmtDesc f, unsigned long long* mismatches, unsigned* first_bad) {
+    const uint64_t total = 1ull << 32;
+    unsigned long long bad = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total / 2;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned b0 = (unsigned)(2 * i), b1 = b0 + 1;
+        float a = __uint_as_float(b0), b = __uint_as_float(b1);
+        const bool fa = isfinite(a), fb = isfinite(b);
+        if (!fa) a = 0.f;
+        if (!fb) b = 0.f;
+        float qa, qb;
+        HwFmt<ID>::q2(a, b, qa, qb);
+        if (fa && (double)qa != quantize_ref((double)a, f)) {
+            ++bad;
+            atomicMin(first_bad, b0);
+        }
+        if (fb && (double)qb != quantize_ref((double)b, f)) {
+            ++bad;
+            atomicMin(first_bad, b1);
+        }
+    }
+    if (bad) atomicAdd(mismatches, bad);
+}
+
+cudaError_t launch_selftest_hwq(const FmtDesc& f, unsigned long long* mism, unsigned* first_bad,
+                                cudaStream_t st) {
+    const int grid = 148 * 16, thr = 256;
+    switch (f.id) {
+        case F_E4M3: k_selftest_hwq<F_E4M3><<<grid, thr, 0, st>>>(f, mism, first_bad); break;
+        case F_E5M2: k_selftest_hwq<F_E5M2><<<grid, thr, 0, st>>>(f, mism, first_bad); break;
+        case F_E2M3: k_selftest_hwq<F_E2M3><<<grid, thr, 0, st>>>(f, mism, first_bad); break;
+        case F_E3M2: k_selftest_hwq<F_E3M2><<<grid, thr, 0, st>>>(f, mism, first_bad); break;
+        case F_E2M1: k_selftest_hwq<F_E2M1><<<grid, thr, 0, st>>>(f, mism, first_bad); break;
+        default: return cudaErrorInvalidValue;
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace mxfft

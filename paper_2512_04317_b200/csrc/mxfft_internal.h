@@ -1,0 +1,99 @@
+// mxfft_internal.h -- library-internal types shared by the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mxfft_common.cuh"
+
+namespace mxfft {
+
+// Encoded plan (FftPlan, fftcore.py:84-117), resident on the device.
+struct Plan {
+    int n, log2n, block_size, cpb;
+    FmtDesc fmt;
+    // full tables, reference layout: codes (stages, n/2), scale exponents (stages, n/2/cpb)
+    double* d_wcr = nullptr;
+    double* d_wci = nullptr;
+    int* d_wsexp = nullptr;
+    // compressed kernel tables: per stage s, entries j < 2^s at offset 2^s - 1
+    float2* d_tw_fwd = nullptr;  // (wr, wi) codes
+    float2* d_tw_inv = nullptr;  // (wr, -wi): conjugated twiddles (fftcore.py:267-268)
+    int* d_tw_exp = nullptr;     // exponent of the block containing j
+};
+
+// One pass of 1-D transforms over a set of lines.
+struct LinePass {
+    const void* in = nullptr;
+    void* out = nullptr;
+    int col_mode = 0;            // 0: lines are contiguous rows; 1: columns of n x n images
+    int64_t img_elems = 0;       // complex elements per image
+    int lines_per_image = 1;     // rows mode: lines per image (for k lookup)
+    int64_t total_lines = 0;     // rows mode: number of lines
+    int64_t batch = 0;           // cols mode: number of images
+    int inverse = 0;
+    const int32_t* kvec = nullptr;
+    int k_group = 1;
+    int kin_sign = 0, kout_sign = 0, kout_const = 0;
+    int stage_limit = -1;
+    int32_t* d_vexp = nullptr;
+    float* d_vcodes = nullptr;
+    int32_t* d_pexp = nullptr;
+    int32_t* d_pshift = nullptr;
+    float* d_pcodes = nullptr;
+};
+
+struct LinesArgs {
+    const float2* in;
+    float2* out;
+    int n, log2n, T, log2T, LT, LS, col_mode;
+    int64_t img_elems;
+    int lines_per_image, tiles_per_image;
+    int64_t total_lines, batch;
+    const float2* tw;
+    const int* tw_exp;
+    const int32_t* kvec;
+    int k_group, kin_sign, kout_sign, kout_const, stage_limit;
+    int32_t* d_vexp;
+    float* d_vcodes;
+    int32_t* d_pexp;
+    int32_t* d_pshift;
+    float* d_pcodes;
+};
+
+struct GenericArgs {
+    const float2* in;
+    float2* out;
+    int n, log2n, cpb;
+    FmtDesc fmt;
+    const double* wcr;
+    const double* wci;
+    const int* wsexp;
+    int inverse, col_mode;
+    int64_t img_elems;
+    int lines_per_image;
+    const int32_t* kvec;
+    int k_group, kin_sign, kout_sign, kout_const;
+};
+
+bool fast_path_ok(const Plan& p);
+cudaError_t run_lines(const Plan& p, const LinePass& lp, cudaStream_t st);
+
+// codec kernels (mxfft_codec.cu)
+cudaError_t launch_quantize_f64(const double* x, double* out, int64_t n, const FmtDesc& f,
+                                int32_t* d_nonfinite, cudaStream_t st);
+cudaError_t launch_encode_f64(const double* v, int64_t nblocks, int block_len, const FmtDesc& f,
+                              double* codes, double* scales, int* scale_exp, int32_t* d_nonfinite,
+                              cudaStream_t st);
+cudaError_t launch_decode_f64(const double* codes, const double* scales, int64_t nblocks,
+                              int block_len, double* out, cudaStream_t st);
+cudaError_t plan_encode(Plan& p, const double* d_tw, cudaStream_t st);
+cudaError_t launch_rss(const void* x, int is_c128, int64_t groups, int coils, int64_t npix,
+                       double* out, cudaStream_t st);
+
+}  // namespace mxfft
+
+namespace mxfft {
+cudaError_t launch_selftest_hwq(const FmtDesc& f, unsigned long long* mism, unsigned* first_bad,
+                                cudaStream_t st);
+}  // namespace mxfft

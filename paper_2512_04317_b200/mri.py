@@ -1,0 +1,143 @@
+"""MRI-style pipelines on the GPU: prescale -> MX-FFT2 (-> inverse) -> undo -> RSS.
+
+Public surface of pkg/src/mxfft/mri.py:35-107 (ComplexGrid, RssImage, rss,
+forward_pipeline, roundtrip_pipeline).  One coil stack shares one global
+prescale exponent (mri.py:88, mri.py:98); every coil is transformed
+independently.  On the device the whole pipeline is:
+
+  mxfft_prescale_stats (k on device, no host sync)
+  mxfft_fft2 (x*2^k fused into the first load, 2^-k [and 1/N^2] into the last store)
+  mxfft_rss (|T_c| summed over coils, numpy-exact magnitude)
+
+The batched entry points (*_device) take (B, N, N) complex64 CUDA tensors and
+give each image its own prescale (C = 1 stacks) -- the BASELINE workloads.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+
+from . import _native
+from .errors import InvalidValue, ShapeError
+from .fftcore import FftPlan, fft2_device
+from .prescale import (PrescaleConfig, decode_results, k_from_stats, prescale_stats_device)
+
+KSPACE = "kspace"
+IMAGE = "image"
+
+
+@dataclasses.dataclass(frozen=True)
+class ComplexGrid:
+    """(coils, n, n) complex128 samples tagged "kspace" or "image"."""
+
+    data: np.ndarray
+    domain: str
+
+    def __post_init__(self):
+        d = np.asarray(self.data, dtype=np.complex128)
+        if d.ndim != 3 or d.shape[1] != d.shape[2]:
+            raise ShapeError("grid data must be (coils, n, n)")
+        if self.domain not in (KSPACE, IMAGE):
+            raise InvalidValue(f"unknown domain tag {self.domain!r}")
+        if not np.isfinite(d).all():
+            raise InvalidValue("non-finite grid data")
+        object.__setattr__(self, "data", d)
+
+    @property
+    def coils(self) -> int:
+        return self.data.shape[0]
+
+    @property
+    def n(self) -> int:
+        return self.data.shape[1]
+
+
+@dataclasses.dataclass(frozen=True)
+class RssImage:
+    pixels: np.ndarray  # (n, n) nonnegative FP64
+
+    @property
+    def n(self) -> int:
+        return self.pixels.shape[0]
+
+
+def rss_device(x, coils: int = 1):
+    """RSS of a CUDA complex tensor (groups*coils, ...) -> CUDA float64 (groups, ...)."""
+    import torch
+
+    x = x.contiguous()
+    npix = x[0].numel()
+    groups = x.shape[0] // coils
+    out = torch.empty((groups,) + tuple(x.shape[1:]), dtype=torch.float64, device=x.device)
+    _native.check(_native.lib().mxfft_rss(x.data_ptr(), int(x.dtype == torch.complex128), groups,
+                                          coils, npix, out.data_ptr(), _native.stream_handle()))
+    return out
+
+
+def rss(images) -> RssImage:
+    """sqrt(sum_c |T_c|^2) per pixel (coil combine)."""
+    import torch
+
+    if isinstance(images, ComplexGrid):
+        stack = images.data
+    else:
+        arrs = [np.asarray(a, dtype=np.complex128) for a in images]
+        if not arrs:
+            raise ShapeError("need at least one coil")
+        if any(a.shape != arrs[0].shape for a in arrs):
+            raise ShapeError("coil images must share one shape")
+        stack = np.stack(arrs)
+    t = torch.from_numpy(np.ascontiguousarray(stack)).cuda()
+    return RssImage(rss_device(t, coils=stack.shape[0])[0].cpu().numpy())
+
+
+# ---------------------------------------------------------------------------
+# batched, device-resident pipelines (one prescale per image)
+# ---------------------------------------------------------------------------
+def pipeline_device(x, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, coils: int = 1,
+                    out=None, k=None, res=None):
+    """x: CUDA complex64 (B*coils, N, N).  Stacks of `coils` consecutive images
+    share one prescale (C = 1: per image).  Returns (out complex64, k int32 (B,),
+    stats uint8 (B, 40)) without synchronizing."""
+    n = plan.n
+    nstack = x.shape[0] // coils
+    res, k = prescale_stats_device(x, nstack, coils * n * n, cfg, k_out=k, res_out=res)
+    y = fft2_device(x, plan, "roundtrip" if roundtrip else "forward", k=k, k_group=coils, out=out)
+    return y, k, res
+
+
+def _run_grid(grid: ComplexGrid, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool) -> RssImage:
+    import torch
+
+    x128 = torch.from_numpy(np.ascontiguousarray(grid.data)).cuda()
+    # statistics on the caller's FP64 values (prescale.py:66-69), transform in complex64
+    res, k = prescale_stats_device(x128, 1, x128.numel(), cfg)
+    x = x128.to(torch.complex64)
+    y = fft2_device(x, plan, "roundtrip" if roundtrip else "forward", k=k, k_group=grid.coils)
+    r = decode_results(res)[0]
+    if int(r["flags"]) & 1:
+        raise InvalidValue("non-finite input to prescale")
+    if int(r["flags"]) & 2:  # k near a log2 rounding boundary: decide on the host
+        kh, _, _ = k_from_stats(float(r["a_max"]), float(r["p_tau"]), cfg)
+        if kh != int(r["k"]):
+            k = torch.tensor([kh], dtype=torch.int32, device=x.device)
+            y = fft2_device(x, plan, "roundtrip" if roundtrip else "forward", k=k,
+                            k_group=grid.coils)
+    return RssImage(rss_device(y, coils=grid.coils)[0].cpu().numpy())
+
+
+def forward_pipeline(kspace: ComplexGrid, plan: FftPlan, cfg: PrescaleConfig) -> RssImage:
+    """Prescale -> per-coil forward 2-D FFT -> exact undo -> RSS (mri.py:84-91)."""
+    if kspace.domain != KSPACE:
+        raise InvalidValue("forward_pipeline expects a k-space grid")
+    return _run_grid(kspace, plan, cfg, roundtrip=False)
+
+
+def roundtrip_pipeline(image: ComplexGrid, plan: FftPlan, cfg: PrescaleConfig) -> RssImage:
+    """Prescale -> per-coil forward then inverse 2-D FFT x 1/N^2 -> undo -> RSS
+    (mri.py:94-107)."""
+    if image.domain != IMAGE:
+        raise InvalidValue("roundtrip_pipeline expects an image grid")
+    return _run_grid(image, plan, cfg, roundtrip=True)

@@ -1,0 +1,134 @@
+"""Global power-of-two prescale (Alg. 1 of the paper) and its exact inverse.
+
+Same API as pkg/src/mxfft/prescale.py:21-91.  The statistics (peak magnitude,
+tau-percentile of the nonzero magnitudes, k) are computed on the GPU by
+mxfft_prescale_stats: a fused amax + histogram radix-select kernel.  The one
+scalar decision the host keeps is re-deriving k when the device flags a log2
+that landed within a few ulps of a rounding boundary (never for real data).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import math
+
+import numpy as np
+
+from . import _native
+from .errors import ConfigError, InvalidValue
+
+EPS = 1e-30  # log2 guard for an all-zero peak or tail (prescale.py:18)
+
+
+@dataclasses.dataclass(frozen=True)
+class PrescaleConfig:
+    target: float = 1.0
+    tau: float = 1.0  # percentile (in percent) of the nonzero magnitudes
+    tau_min: float = 2.0**-20
+    k_min: int = -40
+    k_max: int = 40
+
+    def __post_init__(self):
+        if not self.target > 0:
+            raise ConfigError("target", "must be > 0")
+        if not 0 < self.tau < 100:
+            raise ConfigError("tau", "must be in (0, 100)")
+        if not self.tau_min > 0:
+            raise ConfigError("tau_min", "must be > 0")
+        if self.k_min > self.k_max:
+            raise ConfigError("k_min", "must be <= k_max")
+
+    def as_c(self) -> _native.PrescaleCfgC:
+        return _native.PrescaleCfgC(float(self.target), float(self.tau), float(self.tau_min),
+                                    int(self.k_min), int(self.k_max))
+
+
+@dataclasses.dataclass(frozen=True)
+class PrescaleResult:
+    k: int
+    a_max: float
+    p_tau: float
+    k1: int
+    k2: int
+
+
+def k_from_stats(a_max: float, p_tau: float, cfg: PrescaleConfig):
+    """The scalar k rule (prescale.py:70-72) evaluated with the host's log2."""
+    v = math.log2(cfg.target / max(a_max, EPS))
+    k1 = math.floor(v + 0.5) if v >= 0 else math.ceil(v - 0.5)
+    k2 = math.ceil(math.log2(cfg.tau_min / max(p_tau, EPS)))
+    return min(max(max(k1, k2), cfg.k_min), cfg.k_max), k1, k2
+
+
+def prescale_stats_device(x, nseg: int, seg_points: int, cfg: PrescaleConfig, k_out=None,
+                          res_out=None):
+    """Launch the statistics kernel on a CUDA tensor (complex64 or complex128,
+    nseg contiguous segments of seg_points values) without synchronizing.
+    Returns (results uint8 tensor (nseg, 40), k int32 tensor (nseg,))."""
+    import torch
+
+    L = _native.lib()
+    if x.dtype not in (torch.complex64, torch.complex128):
+        raise TypeError("prescale statistics take complex64 or complex128 data")
+    res = res_out if res_out is not None else torch.empty(
+        (nseg, _native.PRESCALE_RESULT_DTYPE.itemsize), dtype=torch.uint8, device=x.device)
+    k = k_out if k_out is not None else torch.empty(nseg, dtype=torch.int32, device=x.device)
+    c = cfg.as_c()
+    _native.check(L.mxfft_prescale_stats(x.data_ptr(), int(x.dtype == torch.complex128), nseg,
+                                         seg_points, ctypes.byref(c), res.data_ptr(), k.data_ptr(),
+                                         None, 0, _native.stream_handle()))
+    return res, k
+
+
+def decode_results(res) -> np.ndarray:
+    """Device result rows -> numpy structured array (a_max, p_tau, k1, k2, k, flags, nnz)."""
+    return np.frombuffer(res.cpu().numpy().tobytes(), dtype=_native.PRESCALE_RESULT_DTYPE)
+
+
+def _is_grid(x) -> bool:
+    return not isinstance(x, np.ndarray) and hasattr(x, "data")
+
+
+def _data_of(x) -> np.ndarray:
+    return np.asarray(x.data if _is_grid(x) else x)
+
+
+def compute_prescale(x, cfg: PrescaleConfig) -> PrescaleResult:
+    """Choose k for input x (array or grid) over all of its values."""
+    import torch
+
+    data = np.asarray(_data_of(x))
+    c = np.ascontiguousarray(data, dtype=np.complex128).reshape(-1)
+    if c.size == 0:
+        raise ValueError("zero-size array")
+    t = torch.from_numpy(c).cuda()
+    res, _ = prescale_stats_device(t, 1, c.size, cfg)
+    r = decode_results(res)[0]
+    if int(r["flags"]) & 1:
+        raise InvalidValue("non-finite input to prescale")
+    a_max, p_tau = float(r["a_max"]), float(r["p_tau"])
+    k, k1, k2 = int(r["k"]), int(r["k1"]), int(r["k2"])
+    if int(r["flags"]) & 2:
+        k, k1, k2 = k_from_stats(a_max, p_tau, cfg)
+    return PrescaleResult(k=k, a_max=a_max, p_tau=p_tau, k1=k1, k2=k2)
+
+
+def apply_prescale(x, k: int):
+    """x * 2^k, exact; returns the same kind of object (array or grid)."""
+    import torch
+
+    data = _data_of(x)
+    arr = np.asarray(data)
+    if arr.dtype.kind not in "fc":
+        arr = arr.astype(np.float64)
+    t = torch.from_numpy(np.ascontiguousarray(arr)).cuda()
+    scaled = (t * math.ldexp(1.0, k)).cpu().numpy().reshape(arr.shape)
+    if _is_grid(x):
+        return dataclasses.replace(x, data=scaled)
+    return scaled
+
+
+def undo_prescale(x, k: int):
+    """Exact inverse of apply_prescale."""
+    return apply_prescale(x, -k)

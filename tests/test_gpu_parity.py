@@ -1,0 +1,365 @@
+"""GPU parity: the CUDA product (through its C-ABI) against the CPU oracle and
+the reference's golden vectors.  Integer/exponent/code outputs must be
+bit-exact; transform outputs are compared for exact value equality (the
+oracle and kernel do the same FP32 operations in the same order), which is
+stronger than the north-star tolerance (relative L2 <= 1e-5, asserted too)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+FMTS = ["e4m3", "e5m2", "e2m3", "e3m2", "e2m1"]
+
+
+@pytest.fixture(scope="module")
+def mx():
+    import paper_2512_04317_b200 as m
+
+    return m
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+
+    return t
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def assert_same(got, want, what=""):
+    got = np.asarray(got)
+    want = np.asarray(want)
+    assert got.shape == want.shape, (what, got.shape, want.shape)
+    if not np.array_equal(got, want):
+        bad = np.argwhere(got != want)
+        raise AssertionError(f"{what}: {len(bad)} mismatches, first at {bad[0]}: "
+                             f"{got[tuple(bad[0])]} vs {want[tuple(bad[0])]}; "
+                             f"rel_l2={rel_l2(got.astype(complex), want.astype(complex)):.3e}")
+
+
+# ---------------------------------------------------------------------------
+# element quantizers
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name", FMTS)
+def test_hw_quantizer_exhaustive(mx, torch, name):
+    """Hardware F2FP pack/unpack == reference FP64 quantizer on all 2^32 floats."""
+    from paper_2512_04317_b200 import _native
+
+    f = mx.get_mx_format(name)
+    mism = torch.zeros(1, dtype=torch.int64, device="cuda")
+    first = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    c = f.as_c()
+    _native.check(_native.lib().mxfft_selftest_hw_quantizer(ctypes.byref(c), mism.data_ptr(),
+                                                            first.data_ptr(), 0))
+    torch.cuda.synchronize()
+    assert int(mism.item()) == 0, f"first bad pattern 0x{int(first.item()) & 0xffffffff:08x}"
+
+
+def test_quantize_array_golden(mx):
+    g = golden("quantize")
+    for name in FMTS + ["fp16"]:
+        f = mx.get_mx_format(name)
+        assert_same(mx.quantize_array(g[f"{name}_x"], f), g[f"{name}_q"], name)
+
+
+def test_quantize_kats(mx):
+    # reference tests/test_minifloat.py:74-92
+    assert mx.quantize_scalar(1e6, mx.E4M3) == 448.0
+    assert mx.quantize_scalar(-1e6, mx.E4M3) == -448.0
+    assert mx.quantize_scalar(1e9, mx.E5M2) == 57344.0
+    assert mx.quantize_scalar(0.3, mx.E4M3) == 0.3125
+    assert mx.quantize_scalar(mx.E4M3.min_subnormal / 2, mx.E4M3) == 0.0
+    with pytest.raises(mx.InvalidValue):
+        mx.quantize_array([1.0, float("inf")], mx.E4M3)
+
+
+def test_mx_block_codec(mx, rng):
+    b = mx.encode_block_mx([1.0, 0.5, -0.25, 0.0], mx.E4M3)
+    assert b.scale == 2.0**-8 and np.array_equal(b.codes, [256.0, 128.0, -64.0, 0.0])
+    assert np.array_equal(mx.decode_block_mx(b), [1.0 + 0.5j, -0.25 + 0.0j])
+    z = mx.encode_block_mx([0.0] * 4, mx.E4M3)
+    assert z.scale == 1.0 and not z.codes.any()
+    with pytest.raises(mx.InvalidValue):
+        mx.encode_block_mx([1.0, float("nan")], mx.E4M3)
+    with pytest.raises(mx.MantissaOverflow):
+        mx.encode_from_mant_block([mx.E4M3.max_finite * 2], [0.0], 1.0, mx.E4M3)
+    amax = np.abs(rng.standard_normal(200)) * 10.0 ** rng.uniform(-8, 8, 200)
+    assert_same(mx.mxblock.block_scales(amax, mx.E4M3), O.block_scales(amax, O.E4M3), "scales")
+    for name in FMTS:
+        v = rng.standard_normal((50, 32)) * 10.0 ** rng.uniform(-6, 6, (50, 1))
+        cr, ci, s = mx.fftcore._encode_blocks_batch(v[:, :16], v[:, 16:], 8,
+                                                     mx.get_mx_format(name))
+        ocr, oci, os_ = O.encode_blocks(v[:, :16], v[:, 16:], 8, O.ALL_MX[name])
+        assert_same(cr, ocr, name)
+        assert_same(ci, oci, name)
+        assert_same(s, os_, name)
+
+
+# ---------------------------------------------------------------------------
+# plans and 1-D transforms
+# ---------------------------------------------------------------------------
+def test_plan_twiddles_golden(mx):
+    g = golden("twiddles")
+    for name in FMTS:
+        for bsz in (2, 32):
+            for n in (8, 256):
+                p = mx.make_plan(n, mx.ModeSpec.mx(mx.get_mx_format(name), bsz))
+                key = f"{name}_{bsz}_{n}"
+                cr = np.stack([t[0][0] for t in p.mx_twiddles])
+                ci = np.stack([t[1][0] for t in p.mx_twiddles])
+                sc = np.stack([t[2][0] for t in p.mx_twiddles])
+                assert_same(cr, g[key + "_cr"], key)
+                assert_same(ci, g[key + "_ci"], key)
+                assert_same(sc, g[key + "_s"], key)
+
+
+def test_rows_golden(mx):
+    g = golden("batch")
+    for ci, case in enumerate(g["cases"]):
+        name, bsz, n = str(case).split(":")
+        p = mx.make_plan(int(n), mx.ModeSpec.mx(mx.get_mx_format(name), int(bsz)))
+        x = g[f"c{ci}_x"]
+        assert_same(mx.fftcore._fft_batch(x, p, "forward"), g[f"c{ci}_fwd"], f"{case} fwd")
+        assert_same(mx.fftcore._fft_batch(x, p, "inverse"), g[f"c{ci}_inv"], f"{case} inv")
+
+
+def test_stage_capture_golden(mx, torch):
+    """Per-stage v-block exponents and codes, product exponents/shifts/codes and
+    stage outputs of the kernel == those captured from the reference."""
+    g = golden("stages")
+    checked = 0
+    for ci, case in enumerate(g["cases"]):
+        name, bsz, n = str(case).split(":")
+        p = mx.make_plan(int(n), mx.ModeSpec.mx(mx.get_mx_format(name), int(bsz)))
+        if not mx.fftcore.fast_path_supported(p):
+            continue
+        x = torch.from_numpy(g[f"c{ci}_x"]).cuda().to(torch.complex64)
+        for direction in ("forward", "inverse"):
+            y, cap = mx.fftcore.fft_rows_debug(x, p, direction == "inverse")
+            pre = f"c{ci}_{direction}_"
+            assert_same(y, g[pre + "y"], case)
+            assert_same(cap["v_exp"], g[pre + "v_exp"], f"{case} v_exp")
+            assert_same(cap["v_codes"].astype(np.float64), g[pre + "v_codes"], f"{case} v_codes")
+            assert_same(cap["p_exp"], g[pre + "p_exp"], f"{case} p_exp")
+            assert_same(cap["p_shift"], g[pre + "p_shift"], f"{case} p_shift")
+            assert_same(cap["p_codes"].astype(np.float64), g[pre + "p_codes"], f"{case} p_codes")
+            assert_same(cap["stage_out"], g[pre + "out"], f"{case} stage_out")
+            checked += 1
+    assert checked >= 8
+
+
+def test_rows_vs_oracle_all_formats_blocks(mx, torch, rng):
+    for name in FMTS:
+        for bsz in (2, 4, 8, 16, 32, 64):
+            for n in (32, 128, 512, 2048):
+                x = (rng.standard_normal((6, n)) + 1j * rng.standard_normal((6, n))) \
+                    * 10.0 ** rng.uniform(-4, 4, (6, 1))
+                x = x.astype(np.complex64)
+                p = mx.make_plan(n, mx.ModeSpec.mx(mx.get_mx_format(name), bsz))
+                op = O.make_plan(n, O.ALL_MX[name], bsz)
+                for inv in (False, True):
+                    got = mx.fftcore.fft_rows_device(torch.from_numpy(x).cuda(), p, inv)
+                    assert_same(got.cpu().numpy(), O.fft_batch(x, op, inv), f"{name}:{bsz}:{n}:{inv}")
+
+
+def test_rows_16384(mx, torch):
+    """One 16384-point row per C5 (E4M3, B=32), a few rows."""
+    from paper_2512_04317_b200.workloads import ellipse_kspace
+
+    n = 16384
+    x = np.stack([ellipse_kspace(128, s).reshape(-1) for s in range(3)]) * np.float32(2.0**-12)
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.E4M3, 32))
+    op = O.make_plan(n, O.E4M3, 32)
+    for inv in (False, True):
+        got = mx.fftcore.fft_rows_device(torch.from_numpy(x).cuda(), p, inv).cpu().numpy()
+        assert_same(got, O.fft_batch(x, op, inv), f"16384 inv={inv}")
+
+
+# ---------------------------------------------------------------------------
+# 2-D transforms and pipelines
+# ---------------------------------------------------------------------------
+def test_fft2_golden(mx):
+    g = golden("fft2")
+    for ci, case in enumerate(g["cases"]):
+        name, bsz, n = str(case).split(":")
+        p = mx.make_plan(int(n), mx.ModeSpec.mx(mx.get_mx_format(name), int(bsz)))
+        x = g[f"c{ci}_x"]
+        assert_same(mx.fft_2d(x, p, "forward"), g[f"c{ci}_fwd"], f"{case} fwd")
+        assert_same(mx.fft_2d(x, p, "inverse"), g[f"c{ci}_inv"], f"{case} inv")
+
+
+def test_pipelines_golden(mx):
+    g = golden("pipelines")
+    cfg = mx.PrescaleConfig()
+    for ci, case in enumerate(g["cases"]):
+        name, bsz, n = str(case).split(":")
+        p = mx.make_plan(int(n), mx.ModeSpec.mx(mx.get_mx_format(name), int(bsz)))
+        x = g[f"c{ci}_x"][None]
+        fwd = mx.forward_pipeline(mx.ComplexGrid(x, "kspace"), p, cfg)
+        rt = mx.roundtrip_pipeline(mx.ComplexGrid(x, "image"), p, cfg)
+        assert_same(fwd.pixels, g[f"c{ci}_fwd_rss"], f"{case} forward rss")
+        assert_same(rt.pixels, g[f"c{ci}_rt_rss"], f"{case} round-trip rss")
+        assert mx.compute_prescale(x, cfg).k == int(g[f"c{ci}_k"])
+
+
+def test_prescale_golden(mx):
+    g = golden("prescale")
+    cfg = mx.PrescaleConfig()
+    for i in range(int(g["count"])):
+        r = mx.compute_prescale(g[f"x{i}"], cfg)
+        assert [r.k, r.k1, r.k2] == list(g["k"][i]), i
+        assert r.a_max == g[f"am{i}"][0] and r.p_tau == g[f"am{i}"][1], i
+    with pytest.raises(mx.InvalidValue):
+        mx.compute_prescale(np.array([np.inf]), cfg)
+
+
+def test_prescale_device_batch_vs_oracle(mx, torch, rng):
+    """Per-image statistics of the batched complex64 path (the bench path),
+    including constant images (window overflow -> radix-select fallback),
+    all-zero images and sparse images."""
+    from paper_2512_04317_b200.prescale import decode_results
+    from paper_2512_04317_b200.workloads import ellipse_kspace_batch
+
+    cfg = mx.PrescaleConfig()
+    n = 128
+    x = ellipse_kspace_batch(6, n, seed=11)
+    x[1] = 3.0
+    x[2] = 0.0
+    x[3][rng.random((n, n)) < 0.9] = 0
+    x[4] *= np.float32(1e-30)
+    x[5] *= np.float32(1e20)
+    res, k = mx.prescale_stats_device(torch.from_numpy(x).cuda(), 6, n * n, cfg)
+    r = decode_results(res)
+    for i in range(6):
+        o = O.compute_prescale(x[i])
+        assert (int(r["k"][i]), int(r["k1"][i]), int(r["k2"][i])) == (o.k, o.k1, o.k2), i
+        assert float(r["a_max"][i]) == o.a_max and float(r["p_tau"][i]) == o.p_tau, i
+        assert int(k[i]) == o.k
+
+
+@pytest.mark.parametrize("name,bsz,n,batch,noise", [
+    ("e4m3", 32, 256, 3, 0.01), ("e5m2", 32, 256, 2, 0.01),      # C1/C2
+    ("e3m2", 16, 512, 1, 0.01), ("e2m3", 32, 512, 1, 0.01), ("e2m1", 64, 512, 1, 0.01),  # C3
+    ("e4m3", 32, 128, 4, 0.05),                                  # C4
+])
+def test_pipeline_device_vs_oracle(mx, torch, name, bsz, n, batch, noise):
+    """Per-image forward and round-trip pipelines (the benchmark path), bit-exact
+    complex outputs, equal k, and PSNR/NRMSE parity against the FP64 reference."""
+    from paper_2512_04317_b200.workloads import ellipse_kspace_batch
+
+    x = ellipse_kspace_batch(batch, n, seed=1000 + n + bsz, noise=noise)
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.get_mx_format(name), bsz))
+    op = O.make_plan(n, O.ALL_MX[name], bsz)
+    cfg = mx.PrescaleConfig()
+    xd = torch.from_numpy(x).cuda()
+    yf, kf, _ = mx.pipeline_device(xd, p, cfg, roundtrip=False)
+    yr, kr, _ = mx.pipeline_device(xd, p, cfg, roundtrip=True)
+    yf, yr = yf.cpu().numpy(), yr.cpu().numpy()
+    for i in range(batch):
+        of, _, k1 = O.pipeline(x[i], op, False)
+        orr, rss_o, k2 = O.pipeline(x[i], op, True)
+        assert int(kf[i]) == k1 and int(kr[i]) == k2
+        assert_same(yf[i].astype(np.complex128), of[0], f"fwd img{i}")
+        assert_same(yr[i].astype(np.complex128), orr[0], f"rt img{i}")
+        assert rel_l2(yr[i].astype(complex), orr[0]) <= 1e-5
+        ref = np.abs(x[i].astype(np.complex128))  # round trip recovers the input
+        gpu_rss = np.abs(yr[i].astype(np.complex128))
+        assert abs(O.psnr(ref, gpu_rss) - O.psnr(ref, rss_o)) <= 0.01
+        assert abs(np.sqrt(O.nmse(ref, gpu_rss)) - np.sqrt(O.nmse(ref, rss_o))) <= 1e-4
+
+
+# ---------------------------------------------------------------------------
+# properties and edge cases (reference tests/test_fftcore.py:165-226)
+# ---------------------------------------------------------------------------
+def test_delta_and_dc(mx):
+    p = mx.make_plan(8, mx.ModeSpec.mx(mx.E4M3, 32))
+    x = np.zeros(8, complex)
+    x[0] = 1.0
+    assert np.array_equal(mx.fft_1d(x, p), np.ones(8, np.complex64))
+    X = mx.fft_1d(np.ones(8, complex), p)
+    assert X[0] == 8.0 and np.max(np.abs(X[1:])) <= 8 * 2.0**-4
+    p = mx.make_plan(64, mx.ModeSpec.mx(mx.E4M3, 32))
+    d = np.zeros((64, 64), complex)
+    d[0, 0] = 1.0
+    assert np.array_equal(mx.fft_2d(d, p), np.ones((64, 64)))
+
+
+def test_pow2_equivariance_and_determinism(mx, torch, rng):
+    n = 256
+    x = (rng.standard_normal((4, n, n)) + 1j * rng.standard_normal((4, n, n))).astype(np.complex64)
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.E4M3, 32))
+    xd = torch.from_numpy(x).cuda()
+    a = mx.fft2_device(xd, p).cpu().numpy()
+    b = mx.fft2_device(xd, p).cpu().numpy()
+    assert np.array_equal(a, b)
+    c = mx.fft2_device(xd * 32, p).cpu().numpy()
+    assert np.array_equal(c, a * np.float32(32))
+
+
+def test_inverse_is_conjugate_forward(mx, rng):
+    for block in (2, 8, 32):
+        x = rng.standard_normal(32) + 1j * rng.standard_normal(32)
+        p = mx.make_plan(32, mx.ModeSpec.mx(mx.E4M3, block))
+        assert rel_l2(mx.fft_1d(x, p, "inverse"), np.conj(mx.fft_1d(np.conj(x), p))) <= 1e-6
+
+
+def test_extreme_magnitudes_slow_path(mx, torch, rng):
+    """Values whose block exponents leave FP32's normal range exercise the
+    FP64-assisted fallback inside the kernel; still bit-exact."""
+    n = 256
+    op = O.make_plan(n, O.E4M3, 32)
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.E4M3, 32))
+    for scale in (1e-38, 1e-30, 1e25, 1e30):
+        x = ((rng.standard_normal((2, n)) + 1j * rng.standard_normal((2, n))) * scale).astype(np.complex64)
+        x[1, ::3] = 0
+        got = mx.fftcore.fft_rows_device(torch.from_numpy(x).cuda(), p).cpu().numpy()
+        assert_same(got, O.fft_batch(x, op), f"scale {scale}")
+
+
+def test_zero_and_errors(mx, torch):
+    p = mx.make_plan(64, mx.ModeSpec.mx(mx.E4M3, 32))
+    z = torch.zeros((2, 64, 64), dtype=torch.complex64, device="cuda")
+    y, k, _ = mx.pipeline_device(z, p, mx.PrescaleConfig(), roundtrip=True)
+    assert not y.abs().sum().item() and int(k[0]) == 40
+    with pytest.raises(mx.UnsupportedSize):
+        mx.fft_2d(np.zeros((64, 32), complex), p)
+    with pytest.raises(mx.UnsupportedSize):
+        mx.fft_2d(np.zeros((32, 32), complex), p)
+    with pytest.raises(mx.ShapeError):
+        mx.fft_1d(np.zeros(32, complex), p)
+    with pytest.raises(ValueError):
+        mx.fft_1d(np.zeros(64, complex), p, "sideways")
+
+
+def test_butterfly_api(mx, rng):
+    # reference tests/test_fftcore.py:109-162 semantics, via the oracle
+    v = rng.standard_normal(4) + 1j * rng.standard_normal(4)
+    y0, y1 = mx.butterfly_mx(np.zeros(4, complex), v, np.ones(4, complex), mx.E4M3)
+    inter = np.empty(8)
+    inter[0::2], inter[1::2] = v.real, v.imag
+    want = mx.decode_block_mx(mx.encode_block_mx(inter, mx.E4M3)).astype(np.complex64)
+    assert np.array_equal(y0, want) and np.array_equal(y1, -y0)
+    m = mx.E4M3.max_finite
+    y0, _ = mx.butterfly_mx(np.zeros(2, complex), np.array([m, m], complex),
+                            np.array([m, -m], complex), mx.E4M3)
+    assert np.all(np.isfinite(y0))
+    for _ in range(10):
+        cpb = int(rng.choice([1, 4, 16]))
+        u = rng.standard_normal(cpb) + 1j * rng.standard_normal(cpb)
+        v = rng.standard_normal(cpb) + 1j * rng.standard_normal(cpb)
+        w = np.exp(-2j * np.pi * rng.uniform(0, 1, cpb))
+        y0, y1 = mx.butterfly_mx(u, v, w, mx.E4M3)
+        w_enc = mx.fftcore._encode_blocks_batch(w.real[None], w.imag[None], cpb, mx.E4M3)
+        wv = mx.fftcore._mx_multiply_batch(v.real[None], v.imag[None], w_enc, mx.E4M3, cpb)[0]
+        u32 = u.astype(np.complex64)
+        assert np.array_equal(y0, u32 + wv.astype(np.complex64))
+        assert np.array_equal(y1, u32 - wv.astype(np.complex64))
