@@ -143,9 +143,9 @@ int32_t mxfft_plan_create(mxfft_plan* plan, int32_t n, const mxfft_format* fmt,
     if ((e = cudaMalloc(&p.d_wcr, sizeof(double) * st * m)) != cudaSuccess ||
         (e = cudaMalloc(&p.d_wci, sizeof(double) * st * m)) != cudaSuccess ||
         (e = cudaMalloc(&p.d_wsexp, sizeof(int) * st * nb)) != cudaSuccess ||
-        (e = cudaMalloc(&p.d_tw_fwd, sizeof(float2) * n)) != cudaSuccess ||
-        (e = cudaMalloc(&p.d_tw_inv, sizeof(float2) * n)) != cudaSuccess ||
-        (e = cudaMalloc(&p.d_tw_exp, sizeof(int) * n)) != cudaSuccess ||
+        (e = cudaMalloc(&p.d_tw16_fwd, sizeof(unsigned) * n)) != cudaSuccess ||
+        (e = cudaMalloc(&p.d_tw16_inv, sizeof(unsigned) * n)) != cudaSuccess ||
+        (e = cudaMalloc(&p.d_twe8, n)) != cudaSuccess ||
         (e = cudaMalloc(&d_tw, sizeof(double) * 2 * st * m)) != cudaSuccess ||
         (e = cudaMemcpyAsync(d_tw, h_twiddles, sizeof(double) * 2 * st * m,
                              cudaMemcpyHostToDevice, s)) != cudaSuccess ||
@@ -165,9 +165,9 @@ int32_t mxfft_plan_destroy(mxfft_plan plan) {
     cudaFree(p.d_wcr);
     cudaFree(p.d_wci);
     cudaFree(p.d_wsexp);
-    cudaFree(p.d_tw_fwd);
-    cudaFree(p.d_tw_inv);
-    cudaFree(p.d_tw_exp);
+    cudaFree(p.d_tw16_fwd);
+    cudaFree(p.d_tw16_inv);
+    cudaFree(p.d_twe8);
     delete plan;
     return MXFFT_OK;
 }
@@ -288,7 +288,7 @@ int32_t mxfft_fft_rows_debug(mxfft_plan plan, const void* x, void* y, int64_t ba
                              int32_t* p_shift, float* p_codes, void* stage_out, uintptr_t stream) {
     if (!plan) return fail(MXFFT_ERR_VALUE, "null plan");
     const Plan& p = plan->p;
-    if (!fast_path_ok(p)) return fail(MXFFT_ERR_VALUE, "debug capture needs a fast-path plan");
+    if (!mx_lines_ok(p)) return fail(MXFFT_ERR_VALUE, "debug capture needs a line-kernel plan");
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t m = p.n / 2, nb = m / p.cpb, st = p.log2n;
     // scratch for any dump array the caller did not ask for

@@ -127,19 +127,30 @@ __global__ void k_plan_encode(const double* __restrict__ tw, int stages, int m, 
     }
 }
 
-// Compressed kernel tables: stage s, j < 2^s at offset 2^s - 1.  Butterfly t = j
-// of group 0 carries twiddle j; its block is j / cpb (fftcore.py:101-113).
-__global__ void k_plan_compress(const double* wcr, const double* wci, const int* wsexp, int stages,
-                                int m, int cpb, float2* tw_fwd, float2* tw_inv, int* tw_exp) {
+// Kernel tables: stage s, j < 2^s at entry 2^s + j (entry 0 unused).
+// Butterfly t = j of group 0 carries twiddle j, and its block is j / cpb
+// (fftcore.py:101-113), so one entry per (s, j) describes every block.
+// Codes are packed f16x2 (exact for every MX element format).
+__global__ void k_plan_tables(const double* wcr, const double* wci, const int* wsexp, int stages,
+                              int m, int cpb, unsigned* tw_fwd, unsigned* tw_inv,
+                              signed char* tw_exp) {
     const int nb = m / cpb;
-    const int total = (1 << stages) - 1;
+    const int total = 1 << stages;
     for (int id = blockIdx.x * blockDim.x + threadIdx.x; id < total; id += gridDim.x * blockDim.x) {
-        const int s = 31 - __clz(id + 1);
-        const int j = id - ((1 << s) - 1);
-        const float r = (float)wcr[(int64_t)s * m + j], im = (float)wci[(int64_t)s * m + j];
-        tw_fwd[id] = make_float2(r, im);
-        tw_inv[id] = make_float2(r, -im);
-        tw_exp[id] = wsexp[(int64_t)s * nb + j / cpb];
+        if (id == 0) {
+            tw_fwd[0] = tw_inv[0] = 0u;
+            tw_exp[0] = 0;
+            continue;
+        }
+        const int s = 31 - __clz(id);
+        const int j = id - (1 << s);
+        const double r = wcr[(int64_t)s * m + j], im = wci[(int64_t)s * m + j];
+        const __half2 f = __halves2half2(__double2half(r), __double2half(im));
+        const __half2 c = __halves2half2(__double2half(r), __double2half(-im));
+        tw_fwd[id] = *reinterpret_cast<const unsigned*>(&f);
+        tw_inv[id] = *reinterpret_cast<const unsigned*>(&c);
+        const int e = wsexp[(int64_t)s * nb + j / cpb];
+        tw_exp[id] = (signed char)(e < -128 ? -128 : (e > 127 ? 127 : e));
     }
 }
 
@@ -152,11 +163,33 @@ cudaError_t plan_encode(Plan& p, const double* d_tw, cudaStream_t st) {
     note_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const int tot = p.n - 1;
-    k_plan_compress<<<grid_for(tot, 256), 256, 0, st>>>(p.d_wcr, p.d_wci, p.d_wsexp, p.log2n, m,
-                                                         p.cpb, p.d_tw_fwd, p.d_tw_inv, p.d_tw_exp);
+    k_plan_tables<<<grid_for(p.n, 256), 256, 0, st>>>(p.d_wcr, p.d_wci, p.d_wsexp, p.log2n, m,
+                                                       p.cpb, p.d_tw16_fwd, p.d_tw16_inv, p.d_twe8);
     note_launch();
-    return cudaGetLastError();
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // stage 0/1 shortcut is valid only if the encoded twiddles are exactly
+    // w = 1 (j = 0) and w = -i (stage 1, j = 1) at block scale 2^-emax
+    p.trivial01 = 0;
+    if (p.log2n >= 2 && p.fmt.id != F_GENERIC) {
+        double cr[3], ci[3];
+        int ex0 = 0, ex1 = 0, ex1b = 0;
+        const int nb = m / p.cpb;
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+        cudaMemcpy(&cr[0], p.d_wcr, sizeof(double), cudaMemcpyDeviceToHost);
+        cudaMemcpy(&ci[0], p.d_wci, sizeof(double), cudaMemcpyDeviceToHost);
+        cudaMemcpy(&cr[1], p.d_wcr + m, 2 * sizeof(double), cudaMemcpyDeviceToHost);
+        cudaMemcpy(&ci[1], p.d_wci + m, 2 * sizeof(double), cudaMemcpyDeviceToHost);
+        cudaMemcpy(&ex0, p.d_wsexp, sizeof(int), cudaMemcpyDeviceToHost);
+        cudaMemcpy(&ex1, p.d_wsexp + nb, sizeof(int), cudaMemcpyDeviceToHost);
+        cudaMemcpy(&ex1b, p.d_wsexp + nb + (1 / p.cpb), sizeof(int), cudaMemcpyDeviceToHost);
+        const double one = ldexp(1.0, p.fmt.emax);
+        p.trivial01 = cr[0] == one && ci[0] == 0.0 && cr[1] == one && ci[1] == 0.0 &&
+                      cr[2] == 0.0 && ci[2] == -one && ex0 == -p.fmt.emax && ex1 == -p.fmt.emax &&
+                      ex1b == -p.fmt.emax;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 // |z| exactly as numpy 2.3.5 computes np.abs(complex128) on FMA hosts:

@@ -16,10 +16,11 @@ struct Plan {
     double* d_wcr = nullptr;
     double* d_wci = nullptr;
     int* d_wsexp = nullptr;
-    // compressed kernel tables: per stage s, entries j < 2^s at offset 2^s - 1
-    float2* d_tw_fwd = nullptr;  // (wr, wi) codes
-    float2* d_tw_inv = nullptr;  // (wr, -wi): conjugated twiddles (fftcore.py:267-268)
-    int* d_tw_exp = nullptr;     // exponent of the block containing j
+    // kernel tables, entry half + j (j < half = 2^s) for stage s; entry 0 unused:
+    unsigned* d_tw16_fwd = nullptr;  // packed f16x2 codes (lo = re, hi = im)
+    unsigned* d_tw16_inv = nullptr;  // conjugated twiddles (fftcore.py:267-268)
+    signed char* d_twe8 = nullptr;   // log2 scale of the block holding butterfly j
+    int trivial01 = 0;  // stage 0/1 twiddles are exactly 1 and -i at scale 2^-emax
 };
 
 // One pass of 1-D transforms over a set of lines.
@@ -43,17 +44,19 @@ struct LinePass {
     float* d_pcodes = nullptr;
 };
 
-struct LinesArgs {
+// arguments of the fast line kernel (mxfft_lines.cu)
+struct MxLinesArgs {
     const float2* in;
     float2* out;
-    int n, log2n, T, log2T, LT, LS, col_mode;
-    int64_t img_elems;
-    int lines_per_image, tiles_per_image;
-    int64_t total_lines, batch;
-    const float2* tw;
-    const int* tw_exp;
+    int n, log2n, log2T, col_mode;
+    int lines_per_image;
+    int64_t total_lines;
+    const unsigned* tw16;
+    const signed char* twe;
+    int trivial01, inverse;
     const int32_t* kvec;
     int k_group, kin_sign, kout_sign, kout_const, stage_limit;
+    int tw_chunks;
     int32_t* d_vexp;
     float* d_vcodes;
     int32_t* d_pexp;
@@ -61,6 +64,7 @@ struct LinesArgs {
     float* d_pcodes;
 };
 
+// arguments of the generic reference-literal kernel (mxfft_fft.cu)
 struct GenericArgs {
     const float2* in;
     float2* out;
@@ -76,7 +80,8 @@ struct GenericArgs {
     int k_group, kin_sign, kout_sign, kout_const;
 };
 
-bool fast_path_ok(const Plan& p);
+bool mx_lines_ok(const Plan& p);
+cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st);
 cudaError_t run_lines(const Plan& p, const LinePass& lp, cudaStream_t st);
 
 // codec kernels (mxfft_codec.cu)
@@ -90,10 +95,7 @@ cudaError_t launch_decode_f64(const double* codes, const double* scales, int64_t
 cudaError_t plan_encode(Plan& p, const double* d_tw, cudaStream_t st);
 cudaError_t launch_rss(const void* x, int is_c128, int64_t groups, int coils, int64_t npix,
                        double* out, cudaStream_t st);
-
-}  // namespace mxfft
-
-namespace mxfft {
 cudaError_t launch_selftest_hwq(const FmtDesc& f, unsigned long long* mism, unsigned* first_bad,
                                 cudaStream_t st);
+
 }  // namespace mxfft

@@ -1,0 +1,68 @@
+// mxfft_lines.cu -- dispatch of the line kernel (kernels in mxfft_lines.cuh,
+// instantiated per element format in lines_<fmt>.cu).
+#include "mxfft_common.cuh"
+#include "mxfft_internal.h"
+
+namespace mxfft {
+
+cudaError_t run_mx_lines_e4m3(const MxLinesArgs&, int, int, size_t, bool, cudaStream_t);
+cudaError_t run_mx_lines_e5m2(const MxLinesArgs&, int, int, size_t, bool, cudaStream_t);
+cudaError_t run_mx_lines_e2m3(const MxLinesArgs&, int, int, size_t, bool, cudaStream_t);
+cudaError_t run_mx_lines_e3m2(const MxLinesArgs&, int, int, size_t, bool, cudaStream_t);
+cudaError_t run_mx_lines_e2m1(const MxLinesArgs&, int, int, size_t, bool, cudaStream_t);
+
+static cudaError_t disp_fmt(const MxLinesArgs& a, int id, int cpb, int nt, size_t smem, bool dbg,
+                            cudaStream_t st) {
+    switch (id) {
+        case F_E4M3: return run_mx_lines_e4m3(a, cpb, nt, smem, dbg, st);
+        case F_E5M2: return run_mx_lines_e5m2(a, cpb, nt, smem, dbg, st);
+        case F_E2M3: return run_mx_lines_e2m3(a, cpb, nt, smem, dbg, st);
+        case F_E3M2: return run_mx_lines_e3m2(a, cpb, nt, smem, dbg, st);
+        case F_E2M1: return run_mx_lines_e2m1(a, cpb, nt, smem, dbg, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+bool mx_lines_ok(const Plan& p) {
+    if (p.fmt.id == F_GENERIC) return false;
+    if (p.cpb > 32 || (p.cpb & (p.cpb - 1))) return false;
+    if (p.log2n < 5 || p.log2n > 14) return false;
+    const int T = p.n >> 5;
+    if (p.cpb == 32 && T > 32) return false;  // lane-pair blocks need both halves in one warp
+    return true;
+}
+
+cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
+    MxLinesArgs a{};
+    a.in = reinterpret_cast<const float2*>(lp.in);
+    a.out = reinterpret_cast<float2*>(lp.out);
+    a.n = p.n;
+    a.log2n = p.log2n;
+    a.log2T = p.log2n - 5;
+    a.col_mode = lp.col_mode;
+    a.lines_per_image = lp.col_mode ? p.n : lp.lines_per_image;
+    a.total_lines = lp.col_mode ? lp.batch * p.n : lp.total_lines;
+    a.tw16 = lp.inverse ? p.d_tw16_inv : p.d_tw16_fwd;
+    a.twe = p.d_twe8;
+    a.trivial01 = p.trivial01;
+    a.inverse = lp.inverse;
+    a.kvec = lp.kvec;
+    a.k_group = lp.k_group > 0 ? lp.k_group : 1;
+    a.kin_sign = lp.kin_sign;
+    a.kout_sign = lp.kout_sign;
+    a.kout_const = lp.kout_const;
+    a.stage_limit = lp.stage_limit >= 0 ? lp.stage_limit : p.log2n;
+    a.d_vexp = lp.d_vexp;
+    a.d_vcodes = lp.d_vcodes;
+    a.d_pexp = lp.d_pexp;
+    a.d_pshift = lp.d_pshift;
+    a.d_pcodes = lp.d_pcodes;
+    const int T = p.n >> 5;
+    const int nt = T <= 128 ? 128 : T;
+    a.tw_chunks = (p.n * 5 + 15) / 16;
+    const size_t smem = (size_t)a.tw_chunks * 16 + (size_t)nt * 32 * sizeof(float2);
+    const bool dbg = lp.d_vexp != nullptr;
+    return disp_fmt(a, p.fmt.id, p.cpb, nt, smem, dbg, st);
+}
+
+}  // namespace mxfft

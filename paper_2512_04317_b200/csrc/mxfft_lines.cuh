@@ -1,0 +1,561 @@
+// mxfft_lines.cuh -- the MX-FFT line kernel for sm_100a (the hot path).
+//
+// One "line" = one 1-D transform of length n (a row, or a column of an n x n
+// image).  A line is owned by T = n/32 threads; each thread holds 32 complex
+// FP32 values in registers.
+//
+//   load   : thread c reads its 32 elements straight from HBM in bit-reversed
+//            order (fftcore.py:262): position 32c+i <- natural index
+//            rev5(i)*T + rev_T(c); a warp's loads cover whole 32B sectors.
+//   stages 0..4 run in registers (blocks of cpb butterflies are in-thread, or
+//            split over a lane pair for cpb = 32).  Stages 0 and 1 have the
+//            twiddles 1 and -i (+i inverse); when the plan's encoded twiddles
+//            are exactly those, the MX product reduces to the v-block codes
+//            (proved in DESIGN.md) and the multiply/renormalize is skipped.
+//   stages >= 5 exchange through shared memory once per stage; thread t takes
+//            butterflies [16t, 16t+16) = whole MX blocks.  The layout is an XOR
+//            swizzle on 16-byte chunks chosen so that every access pattern
+//            (the layout-A write and the u/v runs of every stage) is free of
+//            bank conflicts.
+//   store  : the last stage writes its u/v runs straight to HBM.
+//
+// Per butterfly (general stage): FMNMX3 (v amax), 2 FMUL + 2 F2FP (v codes),
+// 4 FHFMA (exact mantissa-space products from packed f16 codes), FMNMX3
+// (product amax), 2 FMUL + 2 F2FP + 2 HADD2 (requantize), 4 FFMA (decode
+// folded into u +- t).  Twiddles live in shared memory as packed f16 codes.
+#pragma once
+#include "mxfft_common.cuh"
+#include "mxfft_internal.h"
+
+namespace mxfft {
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+// 16-byte-chunk swizzle of the line data: bit b >= 3 of the chunk index is
+// folded into bit (b mod 3) of the bank group, except bit 6 which is folded
+// into all three.  Any three consecutive chunk bits (layout-A writes) and the
+// bit sets {3,5,6}, {3,4,6}, {3,4,5} (stage-5/6/>=7 runs) map bijectively onto
+// the 8 bank groups -> conflict-free 128-bit accesses.
+__device__ __forceinline__ int dsw(int C) {
+    const int x = C >> 3;
+    int f = (x ^ (x >> 3) ^ (x >> 6) ^ (x >> 9)) & 7;
+    f ^= ((C >> 6) & 1) * 6;
+    return C ^ f;
+}
+
+// twiddle table swizzle (4-byte entries, 16-byte chunks): stage-s lanes read
+// chunks (half + 16t)/4 + k; folding chunk bits 3,4 into bits 0,1 spreads them.
+__device__ __forceinline__ int tws(int idx) {
+    const int c = idx >> 2;
+    return ((c ^ ((c >> 3) & 3)) << 2) | (idx & 3);
+}
+
+template <int BITS>
+__host__ __device__ constexpr int rev_c(int i) {
+    int r = 0;
+    for (int b = 0; b < BITS; ++b) r |= ((i >> b) & 1) << (BITS - 1 - b);
+    return r;
+}
+
+// packed quantize: returns f16x2 codes with lo = q(re), hi = q(im)
+template <int ID>
+__device__ __forceinline__ unsigned q2h(float re, float im);
+template <>
+__device__ __forceinline__ unsigned q2h<F_E4M3>(float re, float im) {
+    unsigned short p;
+    unsigned h;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(p) : "f"(im), "f"(re));
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h) : "h"(p));
+    return h;
+}
+template <>
+__device__ __forceinline__ unsigned q2h<F_E5M2>(float re, float im) {
+    unsigned short p;
+    unsigned h;
+    asm("cvt.rn.satfinite.e5m2x2.f32 %0, %1, %2;" : "=h"(p) : "f"(im), "f"(re));
+    asm("cvt.rn.f16x2.e5m2x2 %0, %1;" : "=r"(h) : "h"(p));
+    return h;
+}
+template <>
+__device__ __forceinline__ unsigned q2h<F_E2M3>(float re, float im) {
+    unsigned short p;
+    unsigned h;
+    asm("cvt.rn.satfinite.e2m3x2.f32 %0, %1, %2;" : "=h"(p) : "f"(im), "f"(re));
+    asm("cvt.rn.f16x2.e2m3x2 %0, %1;" : "=r"(h) : "h"(p));
+    return h;
+}
+template <>
+__device__ __forceinline__ unsigned q2h<F_E3M2>(float re, float im) {
+    unsigned short p;
+    unsigned h;
+    asm("cvt.rn.satfinite.e3m2x2.f32 %0, %1, %2;" : "=h"(p) : "f"(im), "f"(re));
+    asm("cvt.rn.f16x2.e3m2x2 %0, %1;" : "=r"(h) : "h"(p));
+    return h;
+}
+template <>
+__device__ __forceinline__ unsigned q2h<F_E2M1>(float re, float im) {
+    unsigned h;
+    asm("{\n\t.reg .b8 t;\n\tcvt.rn.satfinite.e2m1x2.f32 t, %1, %2;\n\t"
+        "cvt.rn.f16x2.e2m1x2 %0, t;\n\t}"
+        : "=r"(h)
+        : "f"(im), "f"(re));
+    return h;
+}
+
+__device__ __forceinline__ float h_lo(unsigned h) {
+    return __low2float(*reinterpret_cast<const __half2*>(&h));
+}
+__device__ __forceinline__ float h_hi(unsigned h) {
+    return __high2float(*reinterpret_cast<const __half2*>(&h));
+}
+
+// exact mantissa-space complex product of packed f16 codes W = (wr, wi) and
+// C = (cr, ci): pr = fl(wr*cr - wi*ci), pi = fl(wr*ci + wi*cr) (fftcore.py:168-169);
+// each f16 x f16 product is exact in FP32, one rounding per sum.
+__device__ __forceinline__ void cprod(unsigned W, unsigned C, float& pr, float& pi) {
+    asm("{\n\t.reg .f16 wl, wh, cl, ch;\n\t.reg .f32 t1, t2;\n\t"
+        "mov.b32 {wl, wh}, %2;\n\tmov.b32 {cl, ch}, %3;\n\t"
+        "fma.rn.f32.f16 t1, wh, ch, 0f80000000;\n\t"
+        "neg.f32 t1, t1;\n\t"
+        "fma.rn.f32.f16 %0, wl, cl, t1;\n\t"
+        "fma.rn.f32.f16 t2, wh, cl, 0f80000000;\n\t"
+        "fma.rn.f32.f16 %1, wl, ch, t2;\n\t}"
+        : "=f"(pr), "=f"(pi)
+        : "r"(W), "r"(C));
+}
+
+// max over the lane pair sharing a 32-butterfly block (pairs always take the
+// same branches, so the 2-lane mask is valid even in divergent code)
+template <bool PAIR>
+__device__ __forceinline__ float pair_max(float a) {
+    if (PAIR) {
+        const unsigned lane = threadIdx.x & 31;
+        a = fmaxf(a, __shfl_xor_sync(3u << (lane & ~1u), a, 1));
+    }
+    return a;
+}
+
+struct LDbg {
+    int32_t* vexp;
+    float* vcodes;
+    int32_t* pexp;
+    int32_t* pshift;
+    float* pcodes;
+    int64_t row, rows;
+    int m, cpb, stage;
+};
+
+__device__ __forceinline__ void dbg_codes(const LDbg& d, int bfly, float a, float b, float c,
+                                          float e) {
+    if (d.row >= d.rows) return;
+    const int64_t o = ((int64_t)d.stage * d.rows + d.row) * d.m + bfly;
+    d.vcodes[2 * o] = a;
+    d.vcodes[2 * o + 1] = b;
+    d.pcodes[2 * o] = c;
+    d.pcodes[2 * o + 1] = e;
+}
+__device__ __forceinline__ void dbg_exps(const LDbg& d, int bfly, int ev, int E, int sh) {
+    if (d.row >= d.rows) return;
+    const int64_t o = ((int64_t)d.stage * d.rows + d.row) * (d.m / d.cpb) + bfly / d.cpb;
+    d.vexp[o] = ev;
+    d.pexp[o] = E;
+    d.pshift[o] = sh;
+}
+
+// ---------------------------------------------------------------------------
+// rare path: extreme magnitudes (scale or decode exponent outside FP32's
+// normal range).  FP64-assisted, exact; works on a local copy.
+// ---------------------------------------------------------------------------
+template <int ID, int NB, bool PAIR, bool DBG>
+__device__ __noinline__ void mxb_slow(float2* u, float2* v, const unsigned* w, int ew, int ev,
+                                      const LDbg* d, int bfly0) {
+    using F = HwFmt<ID>;
+    const double inv = ldexp(1.0, -ev);
+    float pr[NB], pi[NB];
+    unsigned cv[NB];
+    float ap = 0.f;
+    for (int i = 0; i < NB; ++i) {
+        cv[i] = q2h<ID>((float)((double)v[i].x * inv), (float)((double)v[i].y * inv));
+        cprod(w[i], cv[i], pr[i], pi[i]);
+        ap = fmax3(ap, fabsf(pr[i]), fabsf(pi[i]));
+    }
+    if (PAIR) {
+        const unsigned lane = threadIdx.x & 31;
+        ap = fmaxf(ap, __shfl_xor_sync(3u << (lane & ~1u), ap, 1));
+    }
+    const int sh = ap > F::MAXF ? shift_for<F>(ap) : 0;
+    const float fac = exp2i(-sh);
+    const int E = ew + ev + sh;
+    const double sc = ldexp(1.0, E);
+    for (int i = 0; i < NB; ++i) {
+        const unsigned qp = q2h<ID>(__fmul_rn(pr[i], fac), __fmul_rn(pi[i], fac));
+        const float qr = h_lo(qp), qi = h_hi(qp);
+        const float tr = (float)((double)qr * sc), ti = (float)((double)qi * sc);
+        const float2 uu = u[i];
+        u[i] = make_float2(__fadd_rn(uu.x, tr), __fadd_rn(uu.y, ti));
+        v[i] = make_float2(__fsub_rn(uu.x, tr), __fsub_rn(uu.y, ti));
+        if (DBG) dbg_codes(*d, bfly0 + i, h_lo(cv[i]), h_hi(cv[i]), qr, qi);
+    }
+    if (DBG && ((bfly0 % d->cpb) == 0)) dbg_exps(*d, bfly0, ev, E, sh);
+}
+
+// ---------------------------------------------------------------------------
+// general MX block: NB butterflies held by this thread (NB = cpb, or 16 of a
+// 32-butterfly block split over a lane pair)
+// ---------------------------------------------------------------------------
+template <int ID, int NB, bool PAIR, bool DBG>
+__device__ __forceinline__ void mxb(float2 (&u)[NB], float2 (&v)[NB], const unsigned (&w)[NB],
+                                    int ew, const LDbg* d, int bfly0) {
+    using F = HwFmt<ID>;
+    using Rg = DecodeRange<F>;
+    float am = 0.f;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) am = fmax3(am, fabsf(v[i].x), fabsf(v[i].y));
+    am = pair_max<PAIR>(am);
+    const int ev = am > 0.f ? floor_log2f(am) - F::EMAX : 0;
+    const float inv = exp2i(-ev);
+    unsigned cv[NB];
+    float pr[NB], pi[NB];
+    float ap = 0.f;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        cv[i] = q2h<ID>(v[i].x * inv, v[i].y * inv);
+        cprod(w[i], cv[i], pr[i], pi[i]);
+        ap = fmax3(ap, fabsf(pr[i]), fabsf(pi[i]));
+    }
+    ap = pair_max<PAIR>(ap);
+    const int sh = ap > F::MAXF ? shift_for<F>(ap) : 0;
+    const int E = ew + ev + sh;
+    const bool fast = (ev >= -127) & (ev <= 126) & (E >= Rg::ELO) & (E <= Rg::EHI);
+    if (__builtin_expect(!fast, 0)) {
+        float2 tu[NB], tv[NB];
+        unsigned tw[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            tu[i] = u[i];
+            tv[i] = v[i];
+            tw[i] = w[i];
+        }
+        mxb_slow<ID, NB, PAIR, DBG>(tu, tv, tw, ew, ev, d, bfly0);
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            u[i] = tu[i];
+            v[i] = tv[i];
+        }
+        return;
+    }
+    const float fac = exp2i(-sh);
+    const float sc = exp2i(E);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const unsigned qp = q2h<ID>(pr[i] * fac, pi[i] * fac);
+        const float qr = h_lo(qp), qi = h_hi(qp);
+        const float2 uu = u[i];
+        u[i] = make_float2(__fmaf_rn(qr, sc, uu.x), __fmaf_rn(qi, sc, uu.y));
+        v[i] = make_float2(__fmaf_rn(-qr, sc, uu.x), __fmaf_rn(-qi, sc, uu.y));
+        if (DBG) dbg_codes(*d, bfly0 + i, h_lo(cv[i]), h_hi(cv[i]), qr, qi);
+    }
+    if (DBG && ((bfly0 % d->cpb) == 0)) dbg_exps(*d, bfly0, ev, E, sh);
+}
+
+// Stages 0/1 with twiddles exactly (2^emax, 0) / (0, -+2^emax) at scale 2^-emax:
+// the product block equals the v block shifted by emax, so its codes are the
+// v codes (j = 0) or (ci, -cr) * sigma (j = 1) and E = ev.  Returns false when
+// the exponents leave the fast range (the caller then runs the general path).
+template <int ID, int NB, bool PAIR, int S, bool DBG>
+__device__ __forceinline__ bool trivial_block(float2 (&u)[NB], float2 (&v)[NB], int j0,
+                                              float sigma, const LDbg* d, int bfly0) {
+    using F = HwFmt<ID>;
+    using Rg = DecodeRange<F>;
+    float am = 0.f;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) am = fmax3(am, fabsf(v[i].x), fabsf(v[i].y));
+    am = pair_max<PAIR>(am);
+    const int ev = am > 0.f ? floor_log2f(am) - F::EMAX : 0;
+    if (!((ev >= -127) & (ev <= 126) & (ev >= Rg::ELO) & (ev <= Rg::EHI))) return false;
+    const float inv = exp2i(-ev), sc = exp2i(ev);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const unsigned cv = q2h<ID>(v[i].x * inv, v[i].y * inv);
+        const float cr = h_lo(cv), ci = h_hi(cv);
+        const bool rot = S == 1 && ((j0 + i) & 1);
+        const float tr = rot ? sigma * ci : cr;
+        const float ti = rot ? -sigma * cr : ci;
+        const float2 uu = u[i];
+        u[i] = make_float2(__fmaf_rn(tr, sc, uu.x), __fmaf_rn(ti, sc, uu.y));
+        v[i] = make_float2(__fmaf_rn(-tr, sc, uu.x), __fmaf_rn(-ti, sc, uu.y));
+        if (DBG) dbg_codes(*d, bfly0 + i, cr, ci, tr, ti);
+    }
+    if (DBG && ((bfly0 % d->cpb) == 0))
+        dbg_exps(*d, bfly0, ev, am > 0.f ? ev : -F::EMAX, am > 0.f ? F::EMAX : 0);
+    return true;
+}
+
+// One register-resident stage S (half = 2^S <= 16) over the thread's 32 values.
+template <int ID, int CPB, int S, bool DBG>
+__device__ __forceinline__ void local_stage(float2 (&x)[32], const unsigned* tw, const signed char* twe,
+                                            int c, bool trivial, float sigma, LDbg* d) {
+    constexpr int half = 1 << S;
+    constexpr int NB = CPB < 16 ? CPB : 16;
+    constexpr bool PAIR = CPB == 32;
+    if (DBG) d->stage = S;
+#pragma unroll
+    for (int k = 0; k < 16 / NB; ++k) {
+        float2 ub[NB], vb[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            const int b = k * NB + i, g = b >> S, j = b & (half - 1);
+            ub[i] = x[g * 2 * half + j];
+            vb[i] = x[g * 2 * half + half + j];
+        }
+        const int j0 = (k * NB) & (half - 1);
+        const int bfly0 = c * 16 + k * NB;
+        bool done = false;
+        if (S <= 1 && trivial) done = trivial_block<ID, NB, PAIR, S, DBG>(ub, vb, j0, sigma, d, bfly0);
+        if (!done) {
+            unsigned w[NB];
+#pragma unroll
+            for (int i = 0; i < NB; ++i) w[i] = tw[tws(half + ((k * NB + i) & (half - 1)))];
+            mxb<ID, NB, PAIR, DBG>(ub, vb, w, twe[half + j0], d, bfly0);
+        }
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            const int b = k * NB + i, g = b >> S, j = b & (half - 1);
+            x[g * 2 * half + j] = ub[i];
+            x[g * 2 * half + half + j] = vb[i];
+        }
+    }
+}
+
+__device__ __forceinline__ float2 scl(float2 a, float f) { return make_float2(a.x * f, a.y * f); }
+
+__device__ __forceinline__ float2 pscale(float2 a, int e) {
+    if (e >= -126 && e <= 127) return scl(a, exp2i(e));
+    const double f = ldexp(1.0, e);
+    return make_float2((float)((double)a.x * f), (float)((double)a.y * f));
+}
+
+// ---------------------------------------------------------------------------
+// kernel body
+// ---------------------------------------------------------------------------
+template <int ID, int CPB, bool DBG>
+__device__ __forceinline__ void lines_body(const MxLinesArgs& a) {
+    constexpr int NB = CPB < 16 ? CPB : 16;
+    constexpr bool PAIR = CPB == 32;
+    extern __shared__ float4 smem4[];
+    const int n = a.n, lt = a.log2T, T = 1 << lt;
+    unsigned* tw = reinterpret_cast<unsigned*>(smem4);
+    signed char* twe = reinterpret_cast<signed char*>(tw + n);
+    float2* data = reinterpret_cast<float2*>(smem4 + a.tw_chunks);
+    const int tid = threadIdx.x, NT = blockDim.x;
+
+    // twiddle tables -> shared memory (swizzled codes, plain exponents)
+    for (int i = tid; i < n; i += NT) {
+        tw[tws(i)] = a.tw16[i];
+        twe[i] = a.twe[i];
+    }
+
+    const int W = T > 32 ? T : 32;  // threads sharing one smem region
+    const bool big = T > 32;
+    float2* R = data + (tid / W) * (W * 32);
+    const int lane_r = tid % W;
+    const int ebase = (lane_r >> lt) * n;  // line offset inside the region
+    const int tl = lane_r & (T - 1);
+    const int c = big ? (int)(__brev((unsigned)tl) >> (32 - lt)) : tl;  // owned chunk
+    const int lines_per_cta = NT >> lt;
+    const int64_t ngroups = (a.total_lines + lines_per_cta - 1) / lines_per_cta;
+    const float sigma = a.inverse ? -1.f : 1.f;
+    const int stages = a.log2n;
+    const int slim = a.stage_limit;
+    LDbg dbg;
+    if (DBG) {
+        dbg.vexp = a.d_vexp;
+        dbg.vcodes = a.d_vcodes;
+        dbg.pexp = a.d_pexp;
+        dbg.pshift = a.d_pshift;
+        dbg.pcodes = a.d_pcodes;
+        dbg.rows = a.total_lines;
+        dbg.m = n / 2;
+        dbg.cpb = CPB;
+    }
+    __syncthreads();
+
+    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        const int64_t line = grp * lines_per_cta + (tid >> lt);
+        const bool active = line < a.total_lines;
+        const int64_t img = line / a.lines_per_image;
+        int64_t base;
+        int64_t es;
+        if (a.col_mode) {
+            base = img * (int64_t)n * n + (line - img * n);
+            es = n;
+        } else {
+            base = line * n;
+            es = 1;
+        }
+        const int kk = (a.kvec && active) ? a.kvec[img / a.k_group] : 0;
+        const int kin = a.kin_sign * kk;
+        const int kout = a.kout_sign * kk + a.kout_const;
+        if (DBG) dbg.row = line;
+
+        // ---- load: position 32c+i <- natural index rev5(i)*T + rev_T(c) ----
+        float2 x[32];
+        const int rcol = big ? tl : (lt ? (int)(__brev((unsigned)c) >> (32 - lt)) : 0);
+        if (active) {
+            const float2* src = a.in + base;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = __ldg(src + (int64_t)((rev_c<5>(i) << lt) | rcol) * es);
+            if (kin) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) x[i] = pscale(x[i], kin);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = make_float2(0.f, 0.f);
+        }
+
+        // ---- register stages ----
+        const int nloc = stages < 5 ? stages : 5;
+        const int lim_loc = slim < nloc ? slim : nloc;
+        if (lim_loc > 0) local_stage<ID, CPB, 0, DBG>(x, tw, twe, c, a.trivial01, sigma, &dbg);
+        if (lim_loc > 1) local_stage<ID, CPB, 1, DBG>(x, tw, twe, c, a.trivial01, sigma, &dbg);
+        if (lim_loc > 2) local_stage<ID, CPB, 2, DBG>(x, tw, twe, c, false, sigma, &dbg);
+        if (lim_loc > 3) local_stage<ID, CPB, 3, DBG>(x, tw, twe, c, false, sigma, &dbg);
+        if (lim_loc > 4) local_stage<ID, CPB, 4, DBG>(x, tw, twe, c, false, sigma, &dbg);
+
+        // ---- shared-memory stages ----
+        int U = 32 * c, V = 32 * c + 16;  // current positions of x[0..15], x[16..31]
+        const int last = slim < stages ? slim : stages;
+        for (int s = 5; s < last; ++s) {
+            // publish current values at their positions
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) {
+                *reinterpret_cast<float4*>(R + 2 * dsw((ebase + U + i) >> 1)) =
+                    make_float4(x[i].x, x[i].y, x[i + 1].x, x[i + 1].y);
+                *reinterpret_cast<float4*>(R + 2 * dsw((ebase + V + i) >> 1)) =
+                    make_float4(x[16 + i].x, x[16 + i].y, x[17 + i].x, x[17 + i].y);
+            }
+            if (big) __syncthreads(); else __syncwarp();
+            const int half = 1 << s;
+            const int b0 = 16 * tl;
+            const int j0 = b0 & (half - 1);
+            U = ((b0 >> s) << (s + 1)) + j0;
+            V = U + half;
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) {
+                const float4 qu = *reinterpret_cast<const float4*>(R + 2 * dsw((ebase + U + i) >> 1));
+                const float4 qv = *reinterpret_cast<const float4*>(R + 2 * dsw((ebase + V + i) >> 1));
+                x[i] = make_float2(qu.x, qu.y);
+                x[i + 1] = make_float2(qu.z, qu.w);
+                x[16 + i] = make_float2(qv.x, qv.y);
+                x[17 + i] = make_float2(qv.z, qv.w);
+            }
+            unsigned w16[16];
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) {
+                const uint4 q = *reinterpret_cast<const uint4*>(tw + tws(half + j0 + i));
+                w16[i] = q.x;
+                w16[i + 1] = q.y;
+                w16[i + 2] = q.z;
+                w16[i + 3] = q.w;
+            }
+            if (DBG) dbg.stage = s;
+#pragma unroll
+            for (int k = 0; k < 16 / NB; ++k) {
+                float2 ub[NB], vb[NB];
+                unsigned wb[NB];
+#pragma unroll
+                for (int i = 0; i < NB; ++i) {
+                    ub[i] = x[k * NB + i];
+                    vb[i] = x[16 + k * NB + i];
+                    wb[i] = w16[k * NB + i];
+                }
+                mxb<ID, NB, PAIR, DBG>(ub, vb, wb, twe[half + j0 + k * NB], &dbg, b0 + k * NB);
+#pragma unroll
+                for (int i = 0; i < NB; ++i) {
+                    x[k * NB + i] = ub[i];
+                    x[16 + k * NB + i] = vb[i];
+                }
+            }
+        }
+
+        // ---- store (undo_prescale / 1/n^2 fused) ----
+        if (active) {
+            float2* dst = a.out + base;
+            if (kout) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) x[i] = pscale(x[i], kout);
+            }
+            if (es == 1) {
+#pragma unroll
+                for (int i = 0; i < 16; i += 2) {
+                    *reinterpret_cast<float4*>(dst + U + i) = make_float4(x[i].x, x[i].y, x[i + 1].x, x[i + 1].y);
+                    *reinterpret_cast<float4*>(dst + V + i) =
+                        make_float4(x[16 + i].x, x[16 + i].y, x[17 + i].x, x[17 + i].y);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    dst[(int64_t)(U + i) * es] = x[i];
+                    dst[(int64_t)(V + i) * es] = x[16 + i];
+                }
+            }
+        }
+        // the next group rewrites shared memory: wait for this group's readers
+        if (big) __syncthreads(); else __syncwarp();
+    }
+}
+
+template <int ID, int CPB, bool DBG>
+__global__ void __launch_bounds__(128, 3) k_mx_lines(MxLinesArgs a) {
+    lines_body<ID, CPB, DBG>(a);
+}
+
+template <int ID, int CPB, bool DBG>
+__global__ void __launch_bounds__(512, 1) k_mx_lines_big(MxLinesArgs a) {
+    lines_body<ID, CPB, DBG>(a);
+}
+
+// ---------------------------------------------------------------------------
+// launch
+// ---------------------------------------------------------------------------
+template <int ID, int CPB, bool DBG>
+static cudaError_t launch_t(const MxLinesArgs& a, int nt, size_t smem, cudaStream_t st) {
+    static int occ[2] = {0, 0};
+    static int sms = 0;
+    const bool bigk = nt > 128;
+    auto k = bigk ? k_mx_lines_big<ID, CPB, DBG> : k_mx_lines<ID, CPB, DBG>;
+    if (!occ[bigk]) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        int dev;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[bigk], k, nt, smem);
+        if (e != cudaSuccess) return e;
+        if (occ[bigk] < 1) occ[bigk] = 1;
+    }
+    const int lines_per_cta = nt >> a.log2T;
+    const int64_t groups = (a.total_lines + lines_per_cta - 1) / lines_per_cta;
+    const int64_t cap = (int64_t)sms * occ[bigk];
+    const int grid = (int)(groups < cap ? groups : cap);
+    k<<<grid, nt, smem, st>>>(a);
+    note_launch();
+    return cudaGetLastError();
+}
+
+template <int ID, bool DBG>
+static cudaError_t disp_cpb(const MxLinesArgs& a, int cpb, int nt, size_t smem, cudaStream_t st) {
+    switch (cpb) {
+        case 1: return launch_t<ID, 1, DBG>(a, nt, smem, st);
+        case 2: return launch_t<ID, 2, DBG>(a, nt, smem, st);
+        case 4: return launch_t<ID, 4, DBG>(a, nt, smem, st);
+        case 8: return launch_t<ID, 8, DBG>(a, nt, smem, st);
+        case 16: return launch_t<ID, 16, DBG>(a, nt, smem, st);
+        case 32: return launch_t<ID, 32, DBG>(a, nt, smem, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace mxfft
