@@ -59,7 +59,9 @@ cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
     a.d_pcodes = lp.d_pcodes;
     const int T = p.n >> 5;
     const int nt = T <= 128 ? 128 : T;
-    a.tw_chunks = (p.n * 5 + 15) / 16;
+    // twiddle prefix rounded up to 1 KB: the data regions must stay 128-byte
+    // aligned (run addresses are formed with OR, see radr())
+    a.tw_chunks = ((p.n * 5 + 1023) / 1024) * 64;
     const size_t smem = (size_t)a.tw_chunks * 16 + (size_t)nt * 32 * sizeof(float2);
     const bool dbg = lp.d_vexp != nullptr;
     return disp_fmt(a, p.fmt.id, p.cpb, nt, smem, dbg, st);

@@ -293,6 +293,9 @@ __device__ __forceinline__ bool trivial_block(float2 (&u)[NB], float2 (&v)[NB], 
 }
 
 // One register-resident stage S (half = 2^S <= 16) over the thread's 32 values.
+// Stages 0/1 take the trivial-twiddle shortcut (plans always qualify; any
+// block outside the fast exponent range goes through the out-of-line exact
+// path).  Stages 2..4 run the general block inline.
 template <int ID, int CPB, int S, bool DBG>
 __device__ __forceinline__ void local_stage(float2 (&x)[32], const unsigned* tw, const signed char* twe,
                                             int c, bool trivial, float sigma, LDbg* d) {
@@ -311,9 +314,31 @@ __device__ __forceinline__ void local_stage(float2 (&x)[32], const unsigned* tw,
         }
         const int j0 = (k * NB) & (half - 1);
         const int bfly0 = c * 16 + k * NB;
-        bool done = false;
-        if (S <= 1 && trivial) done = trivial_block<ID, NB, PAIR, S, DBG>(ub, vb, j0, sigma, d, bfly0);
-        if (!done) {
+        if (S <= 1) {
+            bool done = trivial && trivial_block<ID, NB, PAIR, S, DBG>(ub, vb, j0, sigma, d, bfly0);
+            if (!done) {
+                // exact out-of-line path (also covers plans whose stage-0/1
+                // twiddles are not exactly 1 / -i)
+                float2 tu[NB], tv[NB];
+                unsigned tww[NB];
+                float am = 0.f;
+#pragma unroll
+                for (int i = 0; i < NB; ++i) {
+                    tu[i] = ub[i];
+                    tv[i] = vb[i];
+                    tww[i] = tw[tws(half + ((k * NB + i) & (half - 1)))];
+                    am = fmax3(am, fabsf(vb[i].x), fabsf(vb[i].y));
+                }
+                am = pair_max<PAIR>(am);
+                const int ev = am > 0.f ? floor_log2f(am) - HwFmt<ID>::EMAX : 0;
+                mxb_slow<ID, NB, PAIR, DBG>(tu, tv, tww, twe[half + j0], ev, d, bfly0);
+#pragma unroll
+                for (int i = 0; i < NB; ++i) {
+                    ub[i] = tu[i];
+                    vb[i] = tv[i];
+                }
+            }
+        } else {
             unsigned w[NB];
 #pragma unroll
             for (int i = 0; i < NB; ++i) w[i] = tw[tws(half + ((k * NB + i) & (half - 1)))];
@@ -328,13 +353,60 @@ __device__ __forceinline__ void local_stage(float2 (&x)[32], const unsigned* tw,
     }
 }
 
-__device__ __forceinline__ float2 scl(float2 a, float f) { return make_float2(a.x * f, a.y * f); }
-
-__device__ __forceinline__ float2 pscale(float2 a, int e) {
-    if (e >= -126 && e <= 127) return scl(a, exp2i(e));
+// power-of-two scaling of the thread's 32 values (apply/undo prescale, 1/n^2):
+// one FP32 multiply when 2^e is a normal float, else an exact FP64 product
+// rounded once (out of line: never taken for real data).
+static __device__ __noinline__ void scale32_slow(float2* x, int e) {
     const double f = ldexp(1.0, e);
-    return make_float2((float)((double)a.x * f), (float)((double)a.y * f));
+    for (int i = 0; i < 32; ++i) x[i] = make_float2((float)((double)x[i].x * f), (float)((double)x[i].y * f));
 }
+
+__device__ __forceinline__ void scale32(float2 (&x)[32], int e) {
+    if (e >= -126 && e <= 127) {
+        const float f = exp2i(e);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = make_float2(x[i].x * f, x[i].y * f);
+    } else {
+        float2 t[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) t[i] = x[i];
+        scale32_slow(t, e);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = t[i];
+    }
+}
+
+// shared memory accesses by 32-bit shared-window address
+__device__ __forceinline__ void sts128(unsigned addr, float2 a, float2 b) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a.x), "f"(a.y), "f"(b.x),
+                 "f"(b.y)
+                 : "memory");
+}
+__device__ __forceinline__ void lds128(unsigned addr, float2& a, float2& b) {
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(a.x), "=f"(a.y), "=f"(b.x), "=f"(b.y)
+                 : "r"(addr)
+                 : "memory");
+}
+__device__ __forceinline__ uint4 lds128u(unsigned addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+
+// A run of 16 complex (8 chunks) starting at element e (multiple of 16) of the
+// region at shared address rb: chunk k lives at a0 | (f ^ 16k).
+struct Run {
+    unsigned a0, f;
+};
+__device__ __forceinline__ Run mkrun(unsigned rb, int e) {
+    const int C0 = e >> 1;
+    return {rb + (unsigned)C0 * 16u, (unsigned)(dsw(C0) ^ C0) << 4};
+}
+__device__ __forceinline__ unsigned radr(const Run& r, int k) { return r.a0 | (r.f ^ (unsigned)(k << 4)); }
 
 // ---------------------------------------------------------------------------
 // kernel body
@@ -347,7 +419,6 @@ __device__ __forceinline__ void lines_body(const MxLinesArgs& a) {
     const int n = a.n, lt = a.log2T, T = 1 << lt;
     unsigned* tw = reinterpret_cast<unsigned*>(smem4);
     signed char* twe = reinterpret_cast<signed char*>(tw + n);
-    float2* data = reinterpret_cast<float2*>(smem4 + a.tw_chunks);
     const int tid = threadIdx.x, NT = blockDim.x;
 
     // twiddle tables -> shared memory (swizzled codes, plain exponents)
@@ -358,11 +429,15 @@ __device__ __forceinline__ void lines_body(const MxLinesArgs& a) {
 
     const int W = T > 32 ? T : 32;  // threads sharing one smem region
     const bool big = T > 32;
-    float2* R = data + (tid / W) * (W * 32);
+    const unsigned tw_sh = (unsigned)__cvta_generic_to_shared(tw);
+    const unsigned rbase = (unsigned)__cvta_generic_to_shared(smem4 + a.tw_chunks) +
+                           (unsigned)((tid / W) * (W * 32)) * 8u;
+    if (rbase & 127u) __trap();  // radr() ORs chunk offsets into 128-byte-aligned run bases
     const int lane_r = tid % W;
     const int ebase = (lane_r >> lt) * n;  // line offset inside the region
     const int tl = lane_r & (T - 1);
     const int c = big ? (int)(__brev((unsigned)tl) >> (32 - lt)) : tl;  // owned chunk
+    const int rcol = big ? tl : (lt ? (int)(__brev((unsigned)c) >> (32 - lt)) : 0);
     const int lines_per_cta = NT >> lt;
     const int64_t ngroups = (a.total_lines + lines_per_cta - 1) / lines_per_cta;
     const float sigma = a.inverse ? -1.f : 1.f;
@@ -399,25 +474,21 @@ __device__ __forceinline__ void lines_body(const MxLinesArgs& a) {
         const int kout = a.kout_sign * kk + a.kout_const;
         if (DBG) dbg.row = line;
 
-        // ---- load: position 32c+i <- natural index rev5(i)*T + rev_T(c) ----
+        // ---- load: x[rev5(m)] <- natural index m*T + rev_T(c) (fftcore.py:262) ----
         float2 x[32];
-        const int rcol = big ? tl : (lt ? (int)(__brev((unsigned)c) >> (32 - lt)) : 0);
         if (active) {
-            const float2* src = a.in + base;
+            const float2* src = a.in + base + (int64_t)rcol * es;
+            const int64_t stride = (int64_t)T * es;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) x[i] = __ldg(src + (int64_t)((rev_c<5>(i) << lt) | rcol) * es);
-            if (kin) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) x[i] = pscale(x[i], kin);
-            }
+            for (int m = 0; m < 32; ++m) x[rev_c<5>(m)] = __ldg(src + m * stride);
+            if (kin) scale32(x, kin);
         } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i) x[i] = make_float2(0.f, 0.f);
         }
 
         // ---- register stages ----
-        const int nloc = stages < 5 ? stages : 5;
-        const int lim_loc = slim < nloc ? slim : nloc;
+        const int lim_loc = slim < 5 ? slim : 5;
         if (lim_loc > 0) local_stage<ID, CPB, 0, DBG>(x, tw, twe, c, a.trivial01, sigma, &dbg);
         if (lim_loc > 1) local_stage<ID, CPB, 1, DBG>(x, tw, twe, c, a.trivial01, sigma, &dbg);
         if (lim_loc > 2) local_stage<ID, CPB, 2, DBG>(x, tw, twe, c, false, sigma, &dbg);
@@ -428,13 +499,13 @@ __device__ __forceinline__ void lines_body(const MxLinesArgs& a) {
         int U = 32 * c, V = 32 * c + 16;  // current positions of x[0..15], x[16..31]
         const int last = slim < stages ? slim : stages;
         for (int s = 5; s < last; ++s) {
-            // publish current values at their positions
+            {  // publish current values at their positions
+                const Run ru = mkrun(rbase, ebase + U), rv = mkrun(rbase, ebase + V);
 #pragma unroll
-            for (int i = 0; i < 16; i += 2) {
-                *reinterpret_cast<float4*>(R + 2 * dsw((ebase + U + i) >> 1)) =
-                    make_float4(x[i].x, x[i].y, x[i + 1].x, x[i + 1].y);
-                *reinterpret_cast<float4*>(R + 2 * dsw((ebase + V + i) >> 1)) =
-                    make_float4(x[16 + i].x, x[16 + i].y, x[17 + i].x, x[17 + i].y);
+                for (int k = 0; k < 8; ++k) {
+                    sts128(radr(ru, k), x[2 * k], x[2 * k + 1]);
+                    sts128(radr(rv, k), x[16 + 2 * k], x[17 + 2 * k]);
+                }
             }
             if (big) __syncthreads(); else __syncwarp();
             const int half = 1 << s;
@@ -442,19 +513,18 @@ __device__ __forceinline__ void lines_body(const MxLinesArgs& a) {
             const int j0 = b0 & (half - 1);
             U = ((b0 >> s) << (s + 1)) + j0;
             V = U + half;
+            {
+                const Run ru = mkrun(rbase, ebase + U), rv = mkrun(rbase, ebase + V);
 #pragma unroll
-            for (int i = 0; i < 16; i += 2) {
-                const float4 qu = *reinterpret_cast<const float4*>(R + 2 * dsw((ebase + U + i) >> 1));
-                const float4 qv = *reinterpret_cast<const float4*>(R + 2 * dsw((ebase + V + i) >> 1));
-                x[i] = make_float2(qu.x, qu.y);
-                x[i + 1] = make_float2(qu.z, qu.w);
-                x[16 + i] = make_float2(qv.x, qv.y);
-                x[17 + i] = make_float2(qv.z, qv.w);
+                for (int k = 0; k < 8; ++k) {
+                    lds128(radr(ru, k), x[2 * k], x[2 * k + 1]);
+                    lds128(radr(rv, k), x[16 + 2 * k], x[17 + 2 * k]);
+                }
             }
             unsigned w16[16];
 #pragma unroll
             for (int i = 0; i < 16; i += 4) {
-                const uint4 q = *reinterpret_cast<const uint4*>(tw + tws(half + j0 + i));
+                const uint4 q = lds128u(tw_sh + 4u * (unsigned)tws(half + j0 + i));
                 w16[i] = q.x;
                 w16[i + 1] = q.y;
                 w16[i + 2] = q.z;
@@ -482,11 +552,8 @@ __device__ __forceinline__ void lines_body(const MxLinesArgs& a) {
 
         // ---- store (undo_prescale / 1/n^2 fused) ----
         if (active) {
+            if (kout) scale32(x, kout);
             float2* dst = a.out + base;
-            if (kout) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) x[i] = pscale(x[i], kout);
-            }
             if (es == 1) {
 #pragma unroll
                 for (int i = 0; i < 16; i += 2) {
@@ -495,10 +562,12 @@ __device__ __forceinline__ void lines_body(const MxLinesArgs& a) {
                         make_float4(x[16 + i].x, x[16 + i].y, x[17 + i].x, x[17 + i].y);
                 }
             } else {
+                float2* du = dst + (int64_t)U * es;
+                float2* dv = dst + (int64_t)V * es;
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                    dst[(int64_t)(U + i) * es] = x[i];
-                    dst[(int64_t)(V + i) * es] = x[16 + i];
+                    du[i * es] = x[i];
+                    dv[i * es] = x[16 + i];
                 }
             }
         }
