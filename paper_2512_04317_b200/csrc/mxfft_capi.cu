@@ -15,7 +15,9 @@ void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 cudaError_t plan_encode(Plan& p, const double* d_tw, cudaStream_t st);
 cudaError_t launch_prescale(const void* x, int is_c128, int64_t nseg, int64_t npts,
                             const mxfft_prescale_cfg& c, mxfft_prescale_result* out, int32_t* kvec,
-                            cudaStream_t st);
+                            void* ws, int64_t ws_bytes, cudaStream_t st);
+int64_t prescale_fast_ws_bytes(int64_t nseg, int64_t npts);
+bool prescale_fast_ok(int64_t npts);
 }  // namespace mxfft
 
 using namespace mxfft;
@@ -256,22 +258,22 @@ int32_t mxfft_fft2(mxfft_plan plan, const void* x, void* y, int64_t batch, int32
 }
 
 int64_t mxfft_prescale_workspace_bytes(int64_t nseg, int64_t seg_points) {
-    (void)nseg;
-    (void)seg_points;
-    return 0;
+    // sampled fast path for complex64 segments; 0 means "exact kernel only"
+    if (nseg <= 0 || !prescale_fast_ok(seg_points) || (seg_points & 1)) return 0;
+    return prescale_fast_ws_bytes(nseg, seg_points);
 }
 
 int32_t mxfft_prescale_stats(const void* x, int32_t is_c128, int64_t nseg, int64_t seg_points,
                              const mxfft_prescale_cfg* cfg, mxfft_prescale_result* d_out,
                              int32_t* d_k, void* workspace, int64_t workspace_bytes,
                              uintptr_t stream) {
-    (void)workspace;
-    (void)workspace_bytes;
     if (!cfg) return fail(MXFFT_ERR_VALUE, "null config");
     if (nseg < 0 || seg_points < 0) return fail(MXFFT_ERR_SHAPE, "negative size");
     if (nseg == 0) return MXFFT_OK;
     if (seg_points > (int64_t)0x7fffffff) return fail(MXFFT_ERR_UNSUPPORTED_SIZE, "segment too large");
-    CK(launch_prescale(x, is_c128, nseg, seg_points, *cfg, d_out, d_k, (cudaStream_t)stream),
+    if (seg_points & 1) workspace = nullptr;  // fast path reads complex pairs
+    CK(launch_prescale(x, is_c128, nseg, seg_points, *cfg, d_out, d_k, workspace, workspace_bytes,
+                       (cudaStream_t)stream),
        "prescale_stats");
     return MXFFT_OK;
 }

@@ -204,27 +204,49 @@ __device__ __noinline__ void mxb_slow(float2* u, float2* v, const unsigned* w, i
 // general MX block: NB butterflies held by this thread (NB = cpb, or 16 of a
 // 32-butterfly block split over a lane pair)
 // ---------------------------------------------------------------------------
+// block maximum of |re|, |im| over NB complex values as four interleaved
+// FMNMX3 chains (dependency depth ~NB/4 + 2 instead of NB)
+template <int NB>
+__device__ __forceinline__ float amax_c(const float2 (&v)[NB]) {
+    constexpr int L = NB < 4 ? NB : 4;
+    float m[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) m[l] = fmaxf(fabsf(v[l].x), fabsf(v[l].y));
+#pragma unroll
+    for (int i = L; i < NB; ++i) m[i % L] = fmax3(m[i % L], fabsf(v[i].x), fabsf(v[i].y));
+    if (L == 1) return m[0];
+    if (L == 2) return fmaxf(m[0], m[1]);
+    return fmaxf(fmax3(m[0], m[1], m[2 % L]), m[3 % L]);
+}
+template <int NB>
+__device__ __forceinline__ float amax_2(const float (&a)[NB], const float (&b)[NB]) {
+    constexpr int L = NB < 4 ? NB : 4;
+    float m[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) m[l] = fmaxf(fabsf(a[l]), fabsf(b[l]));
+#pragma unroll
+    for (int i = L; i < NB; ++i) m[i % L] = fmax3(m[i % L], fabsf(a[i]), fabsf(b[i]));
+    if (L == 1) return m[0];
+    if (L == 2) return fmaxf(m[0], m[1]);
+    return fmaxf(fmax3(m[0], m[1], m[2 % L]), m[3 % L]);
+}
+
 template <int ID, int NB, bool PAIR, bool DBG>
 __device__ __forceinline__ void mxb(float2 (&u)[NB], float2 (&v)[NB], const unsigned (&w)[NB],
                                     int ew, const LDbg* d, int bfly0) {
     using F = HwFmt<ID>;
     using Rg = DecodeRange<F>;
-    float am = 0.f;
-#pragma unroll
-    for (int i = 0; i < NB; ++i) am = fmax3(am, fabsf(v[i].x), fabsf(v[i].y));
-    am = pair_max<PAIR>(am);
+    const float am = pair_max<PAIR>(amax_c<NB>(v));
     const int ev = am > 0.f ? floor_log2f(am) - F::EMAX : 0;
     const float inv = exp2i(-ev);
     unsigned cv[NB];
     float pr[NB], pi[NB];
-    float ap = 0.f;
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
         cv[i] = q2h<ID>(v[i].x * inv, v[i].y * inv);
         cprod(w[i], cv[i], pr[i], pi[i]);
-        ap = fmax3(ap, fabsf(pr[i]), fabsf(pi[i]));
     }
-    ap = pair_max<PAIR>(ap);
+    const float ap = pair_max<PAIR>(amax_2<NB>(pr, pi));
     const int sh = ap > F::MAXF ? shift_for<F>(ap) : 0;
     const int E = ew + ev + sh;
     const bool fast = (ev >= -127) & (ev <= 126) & (E >= Rg::ELO) & (E <= Rg::EHI);
@@ -268,10 +290,7 @@ __device__ __forceinline__ bool trivial_block(float2 (&u)[NB], float2 (&v)[NB], 
                                               float sigma, const LDbg* d, int bfly0) {
     using F = HwFmt<ID>;
     using Rg = DecodeRange<F>;
-    float am = 0.f;
-#pragma unroll
-    for (int i = 0; i < NB; ++i) am = fmax3(am, fabsf(v[i].x), fabsf(v[i].y));
-    am = pair_max<PAIR>(am);
+    const float am = pair_max<PAIR>(amax_c<NB>(v));
     const int ev = am > 0.f ? floor_log2f(am) - F::EMAX : 0;
     if (!((ev >= -127) & (ev <= 126) & (ev >= Rg::ELO) & (ev <= Rg::EHI))) return false;
     const float inv = exp2i(-ev), sc = exp2i(ev);
@@ -577,7 +596,7 @@ __device__ __forceinline__ void lines_body(const MxLinesArgs& a) {
 }
 
 template <int ID, int CPB, bool DBG>
-__global__ void __launch_bounds__(128, 3) k_mx_lines(MxLinesArgs a) {
+__global__ void __launch_bounds__(128, MXFFT_LINES_MINB) k_mx_lines(MxLinesArgs a) {
     lines_body<ID, CPB, DBG>(a);
 }
 

@@ -187,7 +187,9 @@ __device__ double radix_select(const T* x, int64_t npts, int wlo, int whi, unsig
 template <typename T>
 __global__ void __launch_bounds__(PS_THREADS) k_prescale(const T* __restrict__ xall, int64_t npts,
                                                          PsCfg cfg, mxfft_prescale_result* out,
-                                                         int32_t* kvec) {
+                                                         int32_t* kvec, const int* only_if) {
+    // exact fallback for segments the sampled fast path flagged (or all)
+    if (only_if && !only_if[blockIdx.x]) return;
     extern __shared__ unsigned long long ps_smem[];
     PsShared& S = *reinterpret_cast<PsShared*>(ps_smem);
     const T* x = xall + (int64_t)blockIdx.x * npts;
@@ -346,9 +348,15 @@ __global__ void __launch_bounds__(PS_THREADS) k_prescale(const T* __restrict__ x
     }
 }
 
+cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, double q,
+                                 const mxfft_prescale_cfg& c, mxfft_prescale_result* out,
+                                 int32_t* kvec, void* ws, int** fallback, cudaStream_t st);
+int64_t prescale_fast_ws_bytes(int64_t nseg, int64_t npts);
+bool prescale_fast_ok(int64_t npts);
+
 cudaError_t launch_prescale(const void* x, int is_c128, int64_t nseg, int64_t npts,
                             const mxfft_prescale_cfg& c, mxfft_prescale_result* out, int32_t* kvec,
-                            cudaStream_t st) {
+                            void* ws, int64_t ws_bytes, cudaStream_t st) {
     PsCfg cfg;
     cfg.target = c.target;
     cfg.q = c.tau / 100.0;
@@ -363,15 +371,25 @@ cudaError_t launch_prescale(const void* x, int is_c128, int64_t nseg, int64_t np
             done[1] = true;
         }
         k_prescale<double2><<<(unsigned)nseg, PS_THREADS, smem, st>>>(
-            reinterpret_cast<const double2*>(x), npts, cfg, out, kvec);
-    } else {
-        if (!done[0]) {
-            cudaFuncSetAttribute(k_prescale<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            done[0] = true;
-        }
-        k_prescale<float2><<<(unsigned)nseg, PS_THREADS, smem, st>>>(
-            reinterpret_cast<const float2*>(x), npts, cfg, out, kvec);
+            reinterpret_cast<const double2*>(x), npts, cfg, out, kvec, nullptr);
+        note_launch();
+        return cudaGetLastError();
     }
+    if (!done[0]) {
+        cudaFuncSetAttribute(k_prescale<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        done[0] = true;
+    }
+    const int* only_if = nullptr;
+    if (ws && prescale_fast_ok(npts) && ws_bytes >= prescale_fast_ws_bytes(nseg, npts)) {
+        // sampled fast path; segments it cannot settle are flagged for the exact kernel
+        int* fb = nullptr;
+        cudaError_t e = launch_prescale_fast(reinterpret_cast<const float2*>(x), nseg, npts, cfg.q, c,
+                                             out, kvec, ws, &fb, st);
+        if (e != cudaSuccess) return e;
+        only_if = fb;
+    }
+    k_prescale<float2><<<(unsigned)nseg, PS_THREADS, smem, st>>>(reinterpret_cast<const float2*>(x),
+                                                                  npts, cfg, out, kvec, only_if);
     note_launch();
     return cudaGetLastError();
 }

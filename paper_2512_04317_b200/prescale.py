@@ -61,11 +61,29 @@ def k_from_stats(a_max: float, p_tau: float, cfg: PrescaleConfig):
     return min(max(max(k1, k2), cfg.k_min), cfg.k_max), k1, k2
 
 
+_WS = {}  # (device, nbytes) -> reusable workspace of the sampled statistics path
+
+
+def _workspace(device, nbytes: int):
+    import torch
+
+    key = (str(device), nbytes)
+    if nbytes <= 0:
+        return None
+    if key not in _WS:
+        _WS[key] = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    return _WS[key]
+
+
 def prescale_stats_device(x, nseg: int, seg_points: int, cfg: PrescaleConfig, k_out=None,
-                          res_out=None):
-    """Launch the statistics kernel on a CUDA tensor (complex64 or complex128,
+                          res_out=None, workspace=None):
+    """Launch the statistics kernels on a CUDA tensor (complex64 or complex128,
     nseg contiguous segments of seg_points values) without synchronizing.
-    Returns (results uint8 tensor (nseg, 40), k int32 tensor (nseg,))."""
+    Returns (results uint8 tensor (nseg, 40), k int32 tensor (nseg,)).
+
+    complex64 segments use the sampled fast path (needs a device workspace of
+    mxfft_prescale_workspace_bytes; one is cached per size when not given);
+    complex128 and unsettled segments use the exact histogram kernel."""
     import torch
 
     L = _native.lib()
@@ -75,9 +93,16 @@ def prescale_stats_device(x, nseg: int, seg_points: int, cfg: PrescaleConfig, k_
         (nseg, _native.PRESCALE_RESULT_DTYPE.itemsize), dtype=torch.uint8, device=x.device)
     k = k_out if k_out is not None else torch.empty(nseg, dtype=torch.int32, device=x.device)
     c = cfg.as_c()
+    ws_ptr, ws_bytes = None, 0
+    if x.dtype == torch.complex64:
+        need = int(L.mxfft_prescale_workspace_bytes(nseg, seg_points))
+        ws = workspace if workspace is not None and workspace.numel() >= need else \
+            _workspace(x.device, need)
+        if ws is not None:
+            ws_ptr, ws_bytes = ws.data_ptr(), ws.numel()
     _native.check(L.mxfft_prescale_stats(x.data_ptr(), int(x.dtype == torch.complex128), nseg,
                                          seg_points, ctypes.byref(c), res.data_ptr(), k.data_ptr(),
-                                         None, 0, _native.stream_handle()))
+                                         ws_ptr, ws_bytes, _native.stream_handle()))
     return res, k
 
 

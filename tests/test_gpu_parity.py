@@ -363,3 +363,41 @@ def test_butterfly_api(mx, rng):
         u32 = u.astype(np.complex64)
         assert np.array_equal(y0, u32 + wv.astype(np.complex64))
         assert np.array_equal(y1, u32 - wv.astype(np.complex64))
+
+
+def test_prescale_fast_path_many_distributions(mx, torch, rng):
+    """The sampled statistics path (bracket + candidates) against the oracle on
+    256 images from several distributions, incl. heavy tails, discrete values
+    (ties), sparse and constant images that force the exact fallback."""
+    from paper_2512_04317_b200.prescale import decode_results
+
+    cfg = mx.PrescaleConfig()
+    n = 64
+    imgs = []
+    for i in range(256):
+        kind = i % 8
+        if kind == 0:
+            z = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+        elif kind == 1:
+            z = (rng.standard_cauchy((n, n)) + 1j * rng.standard_cauchy((n, n))) * 1e-3
+        elif kind == 2:
+            z = rng.integers(-3, 4, (n, n)) + 1j * rng.integers(-3, 4, (n, n))
+        elif kind == 3:
+            z = np.zeros((n, n), complex)
+            z[rng.random((n, n)) < 0.02] = 1.0 + 2.0j
+        elif kind == 4:
+            z = np.full((n, n), 0.5 - 0.25j)
+        elif kind == 5:
+            z = np.exp(rng.uniform(-40, 40, (n, n))) * np.exp(1j * rng.uniform(0, 6.3, (n, n)))
+        elif kind == 6:
+            z = np.fft.fftshift(np.fft.fft2(rng.random((n, n)) > 0.7)) + 0.01 * rng.standard_normal((n, n))
+        else:
+            z = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) * 2.0 ** rng.integers(-30, 30)
+        imgs.append(z.astype(np.complex64))
+    x = np.stack(imgs)
+    res, k = mx.prescale_stats_device(torch.from_numpy(x).cuda(), 256, n * n, cfg)
+    r = decode_results(res)
+    for i in range(256):
+        o = O.compute_prescale(x[i])
+        got = (int(r["k"][i]), int(r["k1"][i]), int(r["k2"][i]), float(r["a_max"][i]), float(r["p_tau"][i]))
+        assert got == (o.k, o.k1, o.k2, o.a_max, o.p_tau), (i, got, o)
