@@ -117,16 +117,23 @@ int32_t mxfft_fft_cols(mxfft_plan plan, const void* x, void* y, int64_t batch, i
                        uintptr_t stream);
 
 /* Batched 2-D MX transform (fft_2d, fftcore.py:344-353 = rows then columns) of
- * `batch` n x n complex64 images; x may alias y.
+ * `batch` n x n complex64 images; x may alias y (but not the workspace).
  *   mode 0: forward; 1: inverse; 2: round trip = forward, inverse, x 1/n^2
  *           (roundtrip_pipeline's per-coil body, mri.py:100-105).
  *   d_k:    optional per-image int32 prescale exponents (device).  Image i is
  *           multiplied by 2^k[i / k_group] on load (apply_prescale,
  *           prescale.py:76-86) and the result by 2^-k on store (undo_prescale,
  *           prescale.py:89-91).  NULL = no prescale.
+ *   workspace: optional device buffer of mxfft_fft2_workspace_bytes(plan, batch)
+ *           bytes (0 = none needed).  With it each pass is a row pass whose
+ *           output is stored transposed (fftcore.py:351-353 literally), which
+ *           keeps every HBM access a full 128-byte line; NULL = the column pass
+ *           runs in place on y (same results, slower).
  * Exact in FP32 (power-of-two scalings) while results stay in FP32 range. */
 int32_t mxfft_fft2(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t mode,
-                   const int32_t* d_k, int32_t k_group, uintptr_t stream);
+                   const int32_t* d_k, int32_t k_group, void* workspace, int64_t workspace_bytes,
+                   uintptr_t stream);
+int64_t mxfft_fft2_workspace_bytes(mxfft_plan plan, int64_t batch);
 
 /* compute_prescale (prescale.py:61-73) over `nseg` segments of `seg_points`
  * complex values each (complex64 when is_c128 == 0, else complex128),
@@ -162,6 +169,10 @@ int32_t mxfft_fft_rows_debug(mxfft_plan plan, const void* x, void* y, int64_t ba
  * *d_first_bad (device pointers; initialise to 0 / 0xffffffff). */
 int32_t mxfft_selftest_hw_quantizer(const mxfft_format* fmt, uint64_t* d_mismatches,
                                     uint32_t* d_first_bad, uintptr_t stream);
+
+/* Profiling knob: run only the first `limit` butterfly stages of every line
+ * pass (the output is then NOT a transform); limit < 0 restores full passes. */
+void mxfft_profile_stage_limit(int32_t limit);
 
 /* Total number of kernels this library has launched in the process
  * (bookkeeping for the benchmark's gpu_launches count). */

@@ -42,6 +42,7 @@ SIGNATURES = {
     "mxfft_version": ([], _i32),
     "mxfft_last_error": ([], ctypes.c_char_p),
     "mxfft_launch_count": ([], _i64),
+    "mxfft_profile_stage_limit": ([_i32], None),
     "mxfft_quantize_f64": ([_vp, _vp, _i64, _fp, _vp, _u], _i32),
     "mxfft_mx_encode_f64": ([_vp, _i64, _i32, _fp, _vp, _vp, _vp, _u], _i32),
     "mxfft_mx_decode_f64": ([_vp, _vp, _i64, _i32, _vp, _u], _i32),
@@ -50,7 +51,8 @@ SIGNATURES = {
     "mxfft_plan_twiddles": ([_vp, _vp, _vp, _vp], _i32),
     "mxfft_fft_rows": ([_vp, _vp, _vp, _i64, _i32, _u], _i32),
     "mxfft_fft_cols": ([_vp, _vp, _vp, _i64, _i32, _u], _i32),
-    "mxfft_fft2": ([_vp, _vp, _vp, _i64, _i32, _vp, _i32, _u], _i32),
+    "mxfft_fft2": ([_vp, _vp, _vp, _i64, _i32, _vp, _i32, _vp, _i64, _u], _i32),
+    "mxfft_fft2_workspace_bytes": ([_vp, _i64], _i64),
     "mxfft_prescale_stats": ([_vp, _i32, _i64, _i64, ctypes.POINTER(PrescaleCfgC), _vp, _vp,
                               _vp, _i64, _u], _i32),
     "mxfft_prescale_workspace_bytes": ([_i64, _i64], _i64),

@@ -1,10 +1,9 @@
-// Instantiations of the line kernel for E4M3 (split per format so the
-// build compiles formats in parallel).
+// Instantiations of the line kernel for E4M3; one
+// translation unit per format and variant so the build compiles them in parallel.
 #include "mxfft_lines.cuh"
 
 namespace mxfft {
-cudaError_t run_mx_lines_e4m3(const MxLinesArgs& a, int cpb, int nt, size_t smem, bool dbg,
-                             cudaStream_t st) {
-    return dbg ? disp_cpb<F_E4M3, true>(a, cpb, nt, smem, st) : disp_cpb<F_E4M3, false>(a, cpb, nt, smem, st);
+cudaError_t run_mx_lines_e4m3(const MxLinesArgs& a, int cpb, size_t smem, cudaStream_t st) {
+    return disp_cpb<F_E4M3, false>(a, cpb, smem, st);
 }
 }  // namespace mxfft

@@ -85,6 +85,8 @@ const char* mxfft_last_error(void) { return g_err.c_str(); }
 
 int64_t mxfft_launch_count(void) { return g_launches.load(); }
 
+void mxfft_profile_stage_limit(int32_t limit) { mxfft::g_profile_stage_limit = limit; }
+
 int32_t mxfft_quantize_f64(const double* x, double* out, int64_t n, const mxfft_format* fmt,
                            int32_t* d_nonfinite, uintptr_t stream) {
     std::string why;
@@ -225,8 +227,14 @@ int32_t mxfft_fft_cols(mxfft_plan plan, const void* x, void* y, int64_t batch, i
     return MXFFT_OK;
 }
 
+int64_t mxfft_fft2_workspace_bytes(mxfft_plan plan, int64_t batch) {
+    if (!plan || batch <= 0 || !mx_lines_ok(plan->p)) return 0;
+    return batch * (int64_t)plan->p.n * plan->p.n * 8;
+}
+
 int32_t mxfft_fft2(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t mode,
-                   const int32_t* d_k, int32_t k_group, uintptr_t stream) {
+                   const int32_t* d_k, int32_t k_group, void* workspace, int64_t workspace_bytes,
+                   uintptr_t stream) {
     if (!plan) return fail(MXFFT_ERR_VALUE, "null plan");
     if (mode < 0 || mode > 2) return fail(MXFFT_ERR_VALUE, "mode must be 0 (forward), 1 (inverse) or 2 (round trip)");
     if (batch < 0) return fail(MXFFT_ERR_SHAPE, "negative batch");
@@ -235,11 +243,25 @@ int32_t mxfft_fft2(mxfft_plan plan, const void* x, void* y, int64_t batch, int32
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t nn = (int64_t)p.n * p.n;
     const int npass = mode == 2 ? 4 : 2;
+    // With a workspace every pass is a row pass that stores its lines transposed
+    // (rows.T of fft_2d, fftcore.py:351-353): x -> ws -> y [-> ws -> y].  Both
+    // reads and writes then move whole 128-byte lines.  Without one, the
+    // second pass walks the columns in place.
+    const int64_t need = mxfft_fft2_workspace_bytes(plan, batch);
+    const bool tpose = workspace && need > 0;
+    if (workspace && need > 0 && workspace_bytes < need)
+        return fail(MXFFT_ERR_VALUE, "fft2 workspace too small");
     for (int pass = 0; pass < npass; ++pass) {
         LinePass lp;
-        lp.in = pass == 0 ? x : y;
-        lp.out = y;
-        lp.col_mode = pass & 1;
+        if (tpose) {
+            lp.in = pass == 0 ? x : ((pass & 1) ? workspace : y);
+            lp.out = (pass & 1) ? y : workspace;
+            lp.tstore = 1;
+        } else {
+            lp.in = pass == 0 ? x : y;
+            lp.out = y;
+            lp.col_mode = pass & 1;
+        }
         lp.img_elems = nn;
         lp.lines_per_image = p.n;
         lp.total_lines = batch * p.n;
@@ -291,6 +313,7 @@ int32_t mxfft_fft_rows_debug(mxfft_plan plan, const void* x, void* y, int64_t ba
     if (!plan) return fail(MXFFT_ERR_VALUE, "null plan");
     const Plan& p = plan->p;
     if (!mx_lines_ok(p)) return fail(MXFFT_ERR_VALUE, "debug capture needs a line-kernel plan");
+    if (p.n > 4096) return fail(MXFFT_ERR_UNSUPPORTED_SIZE, "debug capture supports n <= 4096");
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t m = p.n / 2, nb = m / p.cpb, st = p.log2n;
     // scratch for any dump array the caller did not ask for

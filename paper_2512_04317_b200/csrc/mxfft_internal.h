@@ -28,6 +28,7 @@ struct LinePass {
     const void* in = nullptr;
     void* out = nullptr;
     int col_mode = 0;            // 0: lines are contiguous rows; 1: columns of n x n images
+    int tstore = 0;              // rows of n x n images, stored transposed (out[i][q][r] = line r, elem q)
     int64_t img_elems = 0;       // complex elements per image
     int lines_per_image = 1;     // rows mode: lines per image (for k lookup)
     int64_t total_lines = 0;     // rows mode: number of lines
@@ -48,7 +49,7 @@ struct LinePass {
 struct MxLinesArgs {
     const float2* in;
     float2* out;
-    int n, log2n, log2T, col_mode;
+    int n, log2n, log2T, col_mode, tstore;
     int lines_per_image;
     int64_t total_lines;
     const unsigned* tw16;
@@ -80,6 +81,7 @@ struct GenericArgs {
     int k_group, kin_sign, kout_sign, kout_const;
 };
 
+extern int g_profile_stage_limit;  // < 0: off (see mxfft_profile_stage_limit)
 bool mx_lines_ok(const Plan& p);
 cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st);
 cudaError_t run_lines(const Plan& p, const LinePass& lp, cudaStream_t st);

@@ -5,23 +5,37 @@
 
 namespace mxfft {
 
-cudaError_t run_mx_lines_e4m3(const MxLinesArgs&, int, int, size_t, bool, cudaStream_t);
-cudaError_t run_mx_lines_e5m2(const MxLinesArgs&, int, int, size_t, bool, cudaStream_t);
-cudaError_t run_mx_lines_e2m3(const MxLinesArgs&, int, int, size_t, bool, cudaStream_t);
-cudaError_t run_mx_lines_e3m2(const MxLinesArgs&, int, int, size_t, bool, cudaStream_t);
-cudaError_t run_mx_lines_e2m1(const MxLinesArgs&, int, int, size_t, bool, cudaStream_t);
+cudaError_t run_mx_lines_e4m3(const MxLinesArgs&, int, size_t, cudaStream_t);
+cudaError_t run_mx_lines_e4m3_dbg(const MxLinesArgs&, int, size_t, cudaStream_t);
+cudaError_t run_mx_lines_e5m2(const MxLinesArgs&, int, size_t, cudaStream_t);
+cudaError_t run_mx_lines_e5m2_dbg(const MxLinesArgs&, int, size_t, cudaStream_t);
+cudaError_t run_mx_lines_e2m3(const MxLinesArgs&, int, size_t, cudaStream_t);
+cudaError_t run_mx_lines_e2m3_dbg(const MxLinesArgs&, int, size_t, cudaStream_t);
+cudaError_t run_mx_lines_e3m2(const MxLinesArgs&, int, size_t, cudaStream_t);
+cudaError_t run_mx_lines_e3m2_dbg(const MxLinesArgs&, int, size_t, cudaStream_t);
+cudaError_t run_mx_lines_e2m1(const MxLinesArgs&, int, size_t, cudaStream_t);
+cudaError_t run_mx_lines_e2m1_dbg(const MxLinesArgs&, int, size_t, cudaStream_t);
 
-static cudaError_t disp_fmt(const MxLinesArgs& a, int id, int cpb, int nt, size_t smem, bool dbg,
+static cudaError_t disp_fmt(const MxLinesArgs& a, int id, int cpb, size_t smem, bool dbg,
                             cudaStream_t st) {
-    switch (id) {
-        case F_E4M3: return run_mx_lines_e4m3(a, cpb, nt, smem, dbg, st);
-        case F_E5M2: return run_mx_lines_e5m2(a, cpb, nt, smem, dbg, st);
-        case F_E2M3: return run_mx_lines_e2m3(a, cpb, nt, smem, dbg, st);
-        case F_E3M2: return run_mx_lines_e3m2(a, cpb, nt, smem, dbg, st);
-        case F_E2M1: return run_mx_lines_e2m1(a, cpb, nt, smem, dbg, st);
+    if (dbg) switch (id) {
+        case F_E4M3: return run_mx_lines_e4m3_dbg(a, cpb, smem, st);
+        case F_E5M2: return run_mx_lines_e5m2_dbg(a, cpb, smem, st);
+        case F_E2M3: return run_mx_lines_e2m3_dbg(a, cpb, smem, st);
+        case F_E3M2: return run_mx_lines_e3m2_dbg(a, cpb, smem, st);
+        case F_E2M1: return run_mx_lines_e2m1_dbg(a, cpb, smem, st);
+    }
+    else switch (id) {
+        case F_E4M3: return run_mx_lines_e4m3(a, cpb, smem, st);
+        case F_E5M2: return run_mx_lines_e5m2(a, cpb, smem, st);
+        case F_E2M3: return run_mx_lines_e2m3(a, cpb, smem, st);
+        case F_E3M2: return run_mx_lines_e3m2(a, cpb, smem, st);
+        case F_E2M1: return run_mx_lines_e2m1(a, cpb, smem, st);
     }
     return cudaErrorInvalidValue;
 }
+
+int g_profile_stage_limit = -1;
 
 bool mx_lines_ok(const Plan& p) {
     if (p.fmt.id == F_GENERIC) return false;
@@ -40,6 +54,7 @@ cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
     a.log2n = p.log2n;
     a.log2T = p.log2n - 5;
     a.col_mode = lp.col_mode;
+    a.tstore = lp.tstore;
     a.lines_per_image = lp.col_mode ? p.n : lp.lines_per_image;
     a.total_lines = lp.col_mode ? lp.batch * p.n : lp.total_lines;
     a.tw16 = lp.inverse ? p.d_tw16_inv : p.d_tw16_fwd;
@@ -52,6 +67,8 @@ cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
     a.kout_sign = lp.kout_sign;
     a.kout_const = lp.kout_const;
     a.stage_limit = lp.stage_limit >= 0 ? lp.stage_limit : p.log2n;
+    if (lp.stage_limit < 0 && g_profile_stage_limit >= 0 && g_profile_stage_limit < p.log2n)
+        a.stage_limit = g_profile_stage_limit;  // profiling knob (mxfft_profile_stage_limit)
     a.d_vexp = lp.d_vexp;
     a.d_vcodes = lp.d_vcodes;
     a.d_pexp = lp.d_pexp;
@@ -62,9 +79,11 @@ cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
     // twiddle prefix rounded up to 1 KB: the data regions must stay 128-byte
     // aligned (run addresses are formed with OR, see radr())
     a.tw_chunks = ((p.n * 5 + 1023) / 1024) * 64;
-    const size_t smem = (size_t)a.tw_chunks * 16 + (size_t)nt * 32 * sizeof(float2);
+    // 128-thread kernels double-buffer their group tile (cp.async pipeline)
+    const size_t nbuf = nt == 128 ? 2 : 1;
+    const size_t smem = (size_t)a.tw_chunks * 16 + nbuf * (size_t)nt * 32 * sizeof(float2);
     const bool dbg = lp.d_vexp != nullptr;
-    return disp_fmt(a, p.fmt.id, p.cpb, nt, smem, dbg, st);
+    return disp_fmt(a, p.fmt.id, p.cpb, smem, dbg, st);
 }
 
 }  // namespace mxfft

@@ -37,7 +37,7 @@ namespace mxfft {
 // into all three.  Any three consecutive chunk bits (layout-A writes) and the
 // bit sets {3,5,6}, {3,4,6}, {3,4,5} (stage-5/6/>=7 runs) map bijectively onto
 // the 8 bank groups -> conflict-free 128-bit accesses.
-__device__ __forceinline__ int dsw(int C) {
+__host__ __device__ __forceinline__ constexpr int dsw(int C) {
     const int x = C >> 3;
     int f = (x ^ (x >> 3) ^ (x >> 6) ^ (x >> 9)) & 7;
     f ^= ((C >> 6) & 1) * 6;
@@ -407,6 +407,11 @@ __device__ __forceinline__ void lds128(unsigned addr, float2& a, float2& b) {
                  : "r"(addr)
                  : "memory");
 }
+__device__ __forceinline__ float2 lds64(unsigned addr) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+    return v;
+}
 __device__ __forceinline__ uint4 lds128u(unsigned addr) {
     uint4 v;
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -428,41 +433,144 @@ __device__ __forceinline__ Run mkrun(unsigned rb, int e) {
 __device__ __forceinline__ unsigned radr(const Run& r, int k) { return r.a0 | (r.f ^ (unsigned)(k << 4)); }
 
 // ---------------------------------------------------------------------------
-// kernel body
+// kernel body.  The hot variants are specialised on LT = log2(T) (n = 32 T):
+// the tile geometry is then compile-time and every swizzled shared address
+// below is a per-thread base XOR an immediate (dsw() is linear over XOR, and
+// the offsets combined are always bit-disjoint, so dsw(a | b) = dsw(a) ^
+// dsw(b)).  LT = -1 instantiates the same code with T taken at run time.
 // ---------------------------------------------------------------------------
+struct LCtx {
+    const unsigned* tw;
+    const signed char* twe;
+    unsigned tw_sh;  // shared address of the (swizzled) twiddle codes
+    int lt, tl, c;
+    bool trivial;
+    float sigma;
+    int slim;
+};
+
+__device__ __forceinline__ void lsync(bool big) {
+    if (big) __syncthreads(); else __syncwarp();
+}
+
+// All butterfly stages of one group.  Registers for stages < 5; stages >= 5
+// exchange through the line's region (element e of the buffer at shared
+// address rb lives in chunk dsw(e/2), half e&1).  On return x[0..15] sit at
+// line positions U.., x[16..31] at V.. .
+// One shared-memory stage s >= 5 (thread t takes butterflies [16t, 16t+16)).
 template <int ID, int CPB, bool DBG>
-__device__ __forceinline__ void lines_body(const MxLinesArgs& a) {
+__device__ __forceinline__ void smem_stage(float2 (&x)[32], int& U, int& V, const LCtx& L, unsigned rb,
+                                           int ebase, int s, bool big, LDbg* dbg) {
     constexpr int NB = CPB < 16 ? CPB : 16;
     constexpr bool PAIR = CPB == 32;
-    extern __shared__ float4 smem4[];
-    const int n = a.n, lt = a.log2T, T = 1 << lt;
-    unsigned* tw = reinterpret_cast<unsigned*>(smem4);
-    signed char* twe = reinterpret_cast<signed char*>(tw + n);
-    const int tid = threadIdx.x, NT = blockDim.x;
+    {  // publish current values at their positions
+        const Run ru = mkrun(rb, ebase + U), rv = mkrun(rb, ebase + V);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            sts128(radr(ru, k), x[2 * k], x[2 * k + 1]);
+            sts128(radr(rv, k), x[16 + 2 * k], x[17 + 2 * k]);
+        }
+    }
+    lsync(big);
+    const int half = 1 << s;
+    const int b0 = 16 * L.tl;
+    const int j0 = b0 & (half - 1);
+    U = ((b0 >> s) << (s + 1)) + j0;
+    V = U + half;
+    {
+        const Run ru = mkrun(rb, ebase + U), rv = mkrun(rb, ebase + V);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            lds128(radr(ru, k), x[2 * k], x[2 * k + 1]);
+            lds128(radr(rv, k), x[16 + 2 * k], x[17 + 2 * k]);
+        }
+    }
+    unsigned w16[16];
+#pragma unroll
+    for (int i = 0; i < 16; i += 4) {
+        const uint4 q = lds128u(L.tw_sh + 4u * (unsigned)tws(half + j0 + i));
+        w16[i] = q.x;
+        w16[i + 1] = q.y;
+        w16[i + 2] = q.z;
+        w16[i + 3] = q.w;
+    }
+    if (DBG) dbg->stage = s;
+#pragma unroll
+    for (int k = 0; k < 16 / NB; ++k) {
+        float2 ub[NB], vb[NB];
+        unsigned wb[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            ub[i] = x[k * NB + i];
+            vb[i] = x[16 + k * NB + i];
+            wb[i] = w16[k * NB + i];
+        }
+        mxb<ID, NB, PAIR, DBG>(ub, vb, wb, L.twe[half + j0 + k * NB], dbg, b0 + k * NB);
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            x[k * NB + i] = ub[i];
+            x[16 + k * NB + i] = vb[i];
+        }
+    }
+}
 
-    // twiddle tables -> shared memory (swizzled codes, plain exponents)
-    for (int i = tid; i < n; i += NT) {
+// All butterfly stages of one group.  Registers for stages < 5; stages >= 5
+// exchange through the line's region (element e of the buffer at shared
+// address rb lives in chunk dsw(e/2), half e&1).  On return x[0..15] sit at
+// line positions U.., x[16..31] at V.. .
+template <int ID, int CPB, bool DBG, int LT>
+__device__ __forceinline__ void run_stages(float2 (&x)[32], int& U, int& V, const LCtx& L,
+                                           unsigned rb, int ebase, LDbg* dbg) {
+    const int lt = LT >= 0 ? LT : L.lt;
+    const bool big = lt > 5;  // a line spans several warps
+    const int lim_loc = L.slim < 5 ? L.slim : 5;
+    if (lim_loc > 0) local_stage<ID, CPB, 0, DBG>(x, L.tw, L.twe, L.c, L.trivial, L.sigma, dbg);
+    if (lim_loc > 1) local_stage<ID, CPB, 1, DBG>(x, L.tw, L.twe, L.c, L.trivial, L.sigma, dbg);
+    if (lim_loc > 2) local_stage<ID, CPB, 2, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg);
+    if (lim_loc > 3) local_stage<ID, CPB, 3, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg);
+    if (lim_loc > 4) local_stage<ID, CPB, 4, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg);
+    U = 32 * L.c;
+    V = U + 16;
+    if constexpr (LT >= 0) {
+#pragma unroll
+        for (int s = 5; s < LT + 5; ++s) {
+            if (s >= L.slim) break;
+            smem_stage<ID, CPB, DBG>(x, U, V, L, rb, ebase, s, big, dbg);
+        }
+    } else {
+        const int last = L.slim < lt + 5 ? L.slim : lt + 5;
+#pragma unroll 1
+        for (int s = 5; s < last; ++s) smem_stage<ID, CPB, DBG>(x, U, V, L, rb, ebase, s, big, dbg);
+    }
+}
+
+__device__ __forceinline__ void cp_async16(unsigned dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async8(unsigned dst, const void* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(valid ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// shared address of the element with swizzled chunk `sch` and half `h`
+__device__ __forceinline__ unsigned caddr(unsigned buf, int sch, int h) {
+    return buf + 16u * (unsigned)sch + 8u * (unsigned)h;
+}
+
+template <int ID, int CPB, bool DBG>
+__device__ __forceinline__ void load_twiddles(unsigned* tw, signed char* twe, const MxLinesArgs& a, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
         tw[tws(i)] = a.tw16[i];
         twe[i] = a.twe[i];
     }
+}
 
-    const int W = T > 32 ? T : 32;  // threads sharing one smem region
-    const bool big = T > 32;
-    const unsigned tw_sh = (unsigned)__cvta_generic_to_shared(tw);
-    const unsigned rbase = (unsigned)__cvta_generic_to_shared(smem4 + a.tw_chunks) +
-                           (unsigned)((tid / W) * (W * 32)) * 8u;
-    if (rbase & 127u) __trap();  // radr() ORs chunk offsets into 128-byte-aligned run bases
-    const int lane_r = tid % W;
-    const int ebase = (lane_r >> lt) * n;  // line offset inside the region
-    const int tl = lane_r & (T - 1);
-    const int c = big ? (int)(__brev((unsigned)tl) >> (32 - lt)) : tl;  // owned chunk
-    const int rcol = big ? tl : (lt ? (int)(__brev((unsigned)c) >> (32 - lt)) : 0);
-    const int lines_per_cta = NT >> lt;
-    const int64_t ngroups = (a.total_lines + lines_per_cta - 1) / lines_per_cta;
-    const float sigma = a.inverse ? -1.f : 1.f;
-    const int stages = a.log2n;
-    const int slim = a.stage_limit;
-    LDbg dbg;
+template <bool DBG>
+__device__ __forceinline__ void init_dbg(LDbg& dbg, const MxLinesArgs& a, int n, int cpb) {
     if (DBG) {
         dbg.vexp = a.d_vexp;
         dbg.vcodes = a.d_vcodes;
@@ -471,177 +579,321 @@ __device__ __forceinline__ void lines_body(const MxLinesArgs& a) {
         dbg.pcodes = a.d_pcodes;
         dbg.rows = a.total_lines;
         dbg.m = n / 2;
-        dbg.cpb = CPB;
+        dbg.cpb = cpb;
     }
-    __syncthreads();
+}
 
-    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-        const int64_t line = grp * lines_per_cta + (tid >> lt);
-        const bool active = line < a.total_lines;
-        const int64_t img = line / a.lines_per_image;
-        int64_t base;
-        int64_t es;
-        if (a.col_mode) {
-            base = img * (int64_t)n * n + (line - img * n);
-            es = n;
+// Lines of n <= 4096 (T <= 128 threads per line; 128-thread CTAs): a software
+// pipeline per CTA.  While group g computes, group g+1's tile streams into the
+// other shared buffer with cp.async (16-byte chunks of contiguous rows, or
+// whole row segments of adjacent columns).  Stores leave through the same
+// buffer so that HBM sees whole lines: 16-byte chunks of contiguous rows, or
+// -- for columns and for rows stored transposed -- LPC adjacent elements of
+// each output row.
+template <int ID, int CPB, bool DBG, int LT>
+__device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
+    constexpr int NT = 128, GEL = NT * 32;  // threads, complex per group tile
+    const int lt = LT >= 0 ? LT : a.log2T;
+    const int T = 1 << lt, N = 32 * T, LN = lt + 5;
+    const int W = T > 32 ? T : 32;         // threads sharing one region
+    const int LPC = NT >> lt, LLPC = 7 - lt;  // lines per group
+    const int LPR = W >> lt;                  // lines per region
+    extern __shared__ float4 smem4[];
+    unsigned* tw = reinterpret_cast<unsigned*>(smem4);
+    signed char* twe = reinterpret_cast<signed char*>(tw + N);
+    const int tid = threadIdx.x;
+    load_twiddles<ID, CPB, DBG>(tw, twe, a, N);
+    LCtx L;
+    L.tw = tw;
+    L.twe = twe;
+    L.tw_sh = (unsigned)__cvta_generic_to_shared(tw);
+    L.lt = lt;
+    L.tl = tid & (T - 1);
+    L.c = L.tl;
+    L.trivial = a.trivial01;
+    L.sigma = a.inverse ? -1.f : 1.f;
+    L.slim = a.stage_limit;
+    const int rcol = lt ? (int)(__brev((unsigned)L.c) >> (32 - lt)) : 0;
+    const unsigned buf0 = (unsigned)__cvta_generic_to_shared(smem4 + a.tw_chunks);
+    constexpr unsigned BUFSZ = (unsigned)GEL * 8u;
+    if (buf0 & 127u) __trap();  // radr() ORs chunk offsets into 128-byte-aligned run bases
+    // this thread's line inside the buffer (tile element belem(j, q) = line j, position q)
+    auto belem = [&](int j, int q) { return (j >> (lt > 5 ? 0 : 5 - lt)) * (W * 32) + (j & (LPR - 1)) * N + q; };
+    const int ebase = belem(tid >> lt, 0);
+    // gather: element ebase + m T + rcol -> chunk dsw(ebase/2) ^ dsw(rcol/2) ^ dsw(m T/2)
+    const int gch = dsw(ebase >> 1) ^ dsw(rcol >> 1);
+    const int gh = rcol & 1;
+    // strided (column / transposed) access: line tj of the group, positions tq0 + T k
+    const int tj = tid & (LPC - 1), tq0 = tid >> LLPC;
+    const int te0 = belem(tj, tq0);
+    const int tch = dsw(te0 >> 1);
+    const int th = te0 & 1;
+    // contiguous access: chunk tid + NT k
+    const int rch = dsw(tid);
+    const bool strided_out = a.col_mode || a.tstore;
+    const int64_t ngroups = (a.total_lines + LPC - 1) / LPC;
+    LDbg dbg;
+    init_dbg<DBG>(dbg, a, N, CPB);
+
+    auto issue_tile = [&](int64_t grp, unsigned buf) {
+        if (!a.col_mode) {
+            const int64_t base = grp * LPC * (int64_t)N;
+            const float4* src = reinterpret_cast<const float4*>(a.in + base) + tid;
+            if ((grp + 1) * LPC <= a.total_lines) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) cp_async16(caddr(buf, rch ^ dsw(NT * k), 0), src + NT * k, true);
+            } else {
+                const int64_t lim = (a.total_lines * (int64_t)N - base) / 2;  // chunks left
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const bool ok = tid + NT * k < lim;
+                    cp_async16(caddr(buf, rch ^ dsw(NT * k), 0), ok ? (const void*)(src + NT * k) : (const void*)a.in, ok);
+                }
+            }
         } else {
-            base = line * n;
+            const int64_t gl = grp * LPC + tj;
+            const bool ok = gl < a.total_lines;
+            const int64_t img = gl >> LN;
+            const float2* src = a.in + (ok ? img * (int64_t)N * N + (int64_t)tq0 * N + (gl & (N - 1)) : 0);
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+                cp_async8(caddr(buf, tch ^ dsw((T * k) >> 1), th ^ ((T * k) & 1)),
+                          ok ? src + (int64_t)k * T * N : src, ok);
+        }
+    };
+
+    if (blockIdx.x < ngroups) issue_tile(blockIdx.x, buf0);
+    cp_commit();
+    int cur = 0;
+    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        const int64_t nxt = grp + gridDim.x;
+        const unsigned bcur = buf0 + (unsigned)cur * BUFSZ, bnxt = buf0 + (unsigned)(cur ^ 1) * BUFSZ;
+        __syncthreads();  // the other buffer's previous readers are done
+        if (nxt < ngroups) issue_tile(nxt, bnxt);
+        cp_commit();
+        cp_wait<1>();     // this thread's copies of group grp have landed
+        __syncthreads();  // ... and everybody's
+
+        const int64_t line = grp * LPC + (tid >> lt);
+        int kin = 0, kout = a.kout_const;
+        if (a.kvec) {
+            const bool active = line < a.total_lines;
+            const int64_t img = line / a.lines_per_image;
+            const int kk = active ? a.kvec[img / a.k_group] : 0;
+            kin = a.kin_sign * kk;
+            kout += a.kout_sign * kk;
+        }
+        if (DBG) dbg.row = line;
+
+        // bit-reversed gather (fftcore.py:262): x[rev5(m)] <- line element m*T + rev_T(c)
+        float2 x[32];
+#pragma unroll
+        for (int m = 0; m < 32; ++m)
+            x[rev_c<5>(m)] = lds64(caddr(bcur, gch ^ dsw((m * T) >> 1), lt ? gh : (m & 1)));
+        if (kin) scale32(x, kin);
+
+        int U, V;
+        run_stages<ID, CPB, DBG, LT>(x, U, V, L, bcur, ebase, &dbg);
+
+        // publish (undo_prescale / 1/n^2 fused), then coalesced stores
+        if (kout) scale32(x, kout);
+        {
+            const Run ru = mkrun(bcur, ebase + U), rv = mkrun(bcur, ebase + V);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                sts128(radr(ru, k), x[2 * k], x[2 * k + 1]);
+                sts128(radr(rv, k), x[16 + 2 * k], x[17 + 2 * k]);
+            }
+        }
+        __syncthreads();
+        if (!strided_out) {
+            const int64_t base = grp * LPC * (int64_t)N;
+            float4* dst = reinterpret_cast<float4*>(a.out + base) + tid;
+            const bool full = (grp + 1) * LPC <= a.total_lines;
+            const int64_t lim = full ? (int64_t)GEL : (a.total_lines * (int64_t)N - base) / 2;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                if (full || tid + NT * k < lim) {
+                    float2 p0, p1;
+                    lds128(caddr(bcur, rch ^ dsw(NT * k), 0), p0, p1);
+                    dst[NT * k] = make_float4(p0.x, p0.y, p1.x, p1.y);
+                }
+            }
+        } else {  // columns, or rows stored transposed: line gl -> column (gl mod n) of image gl/n
+            const int64_t gl = grp * LPC + tj;
+            if (gl < a.total_lines) {
+                const int64_t img = gl >> LN;
+                float2* dst = a.out + img * (int64_t)N * N + (int64_t)tq0 * N + (gl & (N - 1));
+#pragma unroll
+                for (int k = 0; k < 32; ++k)
+                    dst[(int64_t)k * T * N] = lds64(caddr(bcur, tch ^ dsw((T * k) >> 1), th ^ ((T * k) & 1)));
+            }
+        }
+        cur ^= 1;
+    }
+    cp_wait<0>();
+}
+
+// Lines of n = 8192/16384 (T = 256/512; one line per CTA): direct loads from
+// HBM (whole sectors per warp), no prefetch (a second 128 KB buffer would not
+// fit next to the twiddle table).
+template <int ID, int CPB, bool DBG, int LT>
+__device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
+    const int lt = LT >= 0 ? LT : a.log2T;
+    const int T = 1 << lt, N = 32 * T;
+    extern __shared__ float4 smem4[];
+    unsigned* tw = reinterpret_cast<unsigned*>(smem4);
+    signed char* twe = reinterpret_cast<signed char*>(tw + N);
+    const int tid = threadIdx.x;
+    load_twiddles<ID, CPB, DBG>(tw, twe, a, N);
+    LCtx L;
+    L.tw = tw;
+    L.twe = twe;
+    L.tw_sh = (unsigned)__cvta_generic_to_shared(tw);
+    L.lt = lt;
+    L.tl = tid & (T - 1);
+    L.c = (int)(__brev((unsigned)L.tl) >> (32 - lt));  // owned chunk: consecutive lanes load consecutive elements
+    L.trivial = a.trivial01;
+    L.sigma = a.inverse ? -1.f : 1.f;
+    L.slim = a.stage_limit;
+    const int rcol = L.tl;
+    const unsigned rb = (unsigned)__cvta_generic_to_shared(smem4 + a.tw_chunks);
+    if (rb & 127u) __trap();
+    const int ebase = 0;
+    const int64_t ngroups = a.total_lines;
+    LDbg dbg;
+    init_dbg<DBG>(dbg, a, N, CPB);
+    __syncthreads();
+    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        const int64_t line = grp;
+        const int64_t img = line / a.lines_per_image;
+        int64_t base, es, obase, oes;
+        if (a.col_mode) {
+            base = img * (int64_t)N * N + (line - img * N);
+            es = N;
+        } else {
+            base = line * N;
             es = 1;
         }
-        const int kk = (a.kvec && active) ? a.kvec[img / a.k_group] : 0;
+        if (a.tstore) {
+            obase = img * (int64_t)N * N + (line - img * N);
+            oes = N;
+        } else {
+            obase = base;
+            oes = es;
+        }
+        const int kk = a.kvec ? a.kvec[img / a.k_group] : 0;
         const int kin = a.kin_sign * kk;
         const int kout = a.kout_sign * kk + a.kout_const;
         if (DBG) dbg.row = line;
-
-        // ---- load: x[rev5(m)] <- natural index m*T + rev_T(c) (fftcore.py:262) ----
         float2 x[32];
-        if (active) {
+        {
             const float2* src = a.in + base + (int64_t)rcol * es;
             const int64_t stride = (int64_t)T * es;
 #pragma unroll
             for (int m = 0; m < 32; ++m) x[rev_c<5>(m)] = __ldg(src + m * stride);
             if (kin) scale32(x, kin);
+        }
+        int U, V;
+        run_stages<ID, CPB, DBG, LT>(x, U, V, L, rb, ebase, &dbg);
+        if (kout) scale32(x, kout);
+        float2* du = a.out + obase + (int64_t)U * oes;
+        float2* dv = a.out + obase + (int64_t)V * oes;
+        if (oes == 1) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) {
+                *reinterpret_cast<float4*>(du + i) = make_float4(x[i].x, x[i].y, x[i + 1].x, x[i + 1].y);
+                *reinterpret_cast<float4*>(dv + i) =
+                    make_float4(x[16 + i].x, x[16 + i].y, x[17 + i].x, x[17 + i].y);
+            }
         } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) x[i] = make_float2(0.f, 0.f);
-        }
-
-        // ---- register stages ----
-        const int lim_loc = slim < 5 ? slim : 5;
-        if (lim_loc > 0) local_stage<ID, CPB, 0, DBG>(x, tw, twe, c, a.trivial01, sigma, &dbg);
-        if (lim_loc > 1) local_stage<ID, CPB, 1, DBG>(x, tw, twe, c, a.trivial01, sigma, &dbg);
-        if (lim_loc > 2) local_stage<ID, CPB, 2, DBG>(x, tw, twe, c, false, sigma, &dbg);
-        if (lim_loc > 3) local_stage<ID, CPB, 3, DBG>(x, tw, twe, c, false, sigma, &dbg);
-        if (lim_loc > 4) local_stage<ID, CPB, 4, DBG>(x, tw, twe, c, false, sigma, &dbg);
-
-        // ---- shared-memory stages ----
-        int U = 32 * c, V = 32 * c + 16;  // current positions of x[0..15], x[16..31]
-        const int last = slim < stages ? slim : stages;
-        for (int s = 5; s < last; ++s) {
-            {  // publish current values at their positions
-                const Run ru = mkrun(rbase, ebase + U), rv = mkrun(rbase, ebase + V);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    sts128(radr(ru, k), x[2 * k], x[2 * k + 1]);
-                    sts128(radr(rv, k), x[16 + 2 * k], x[17 + 2 * k]);
-                }
-            }
-            if (big) __syncthreads(); else __syncwarp();
-            const int half = 1 << s;
-            const int b0 = 16 * tl;
-            const int j0 = b0 & (half - 1);
-            U = ((b0 >> s) << (s + 1)) + j0;
-            V = U + half;
-            {
-                const Run ru = mkrun(rbase, ebase + U), rv = mkrun(rbase, ebase + V);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    lds128(radr(ru, k), x[2 * k], x[2 * k + 1]);
-                    lds128(radr(rv, k), x[16 + 2 * k], x[17 + 2 * k]);
-                }
-            }
-            unsigned w16[16];
-#pragma unroll
-            for (int i = 0; i < 16; i += 4) {
-                const uint4 q = lds128u(tw_sh + 4u * (unsigned)tws(half + j0 + i));
-                w16[i] = q.x;
-                w16[i + 1] = q.y;
-                w16[i + 2] = q.z;
-                w16[i + 3] = q.w;
-            }
-            if (DBG) dbg.stage = s;
-#pragma unroll
-            for (int k = 0; k < 16 / NB; ++k) {
-                float2 ub[NB], vb[NB];
-                unsigned wb[NB];
-#pragma unroll
-                for (int i = 0; i < NB; ++i) {
-                    ub[i] = x[k * NB + i];
-                    vb[i] = x[16 + k * NB + i];
-                    wb[i] = w16[k * NB + i];
-                }
-                mxb<ID, NB, PAIR, DBG>(ub, vb, wb, twe[half + j0 + k * NB], &dbg, b0 + k * NB);
-#pragma unroll
-                for (int i = 0; i < NB; ++i) {
-                    x[k * NB + i] = ub[i];
-                    x[16 + k * NB + i] = vb[i];
-                }
+            for (int i = 0; i < 16; ++i) {
+                du[i * oes] = x[i];
+                dv[i * oes] = x[16 + i];
             }
         }
-
-        // ---- store (undo_prescale / 1/n^2 fused) ----
-        if (active) {
-            if (kout) scale32(x, kout);
-            float2* dst = a.out + base;
-            if (es == 1) {
-#pragma unroll
-                for (int i = 0; i < 16; i += 2) {
-                    *reinterpret_cast<float4*>(dst + U + i) = make_float4(x[i].x, x[i].y, x[i + 1].x, x[i + 1].y);
-                    *reinterpret_cast<float4*>(dst + V + i) =
-                        make_float4(x[16 + i].x, x[16 + i].y, x[17 + i].x, x[17 + i].y);
-                }
-            } else {
-                float2* du = dst + (int64_t)U * es;
-                float2* dv = dst + (int64_t)V * es;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    du[i * es] = x[i];
-                    dv[i * es] = x[16 + i];
-                }
-            }
-        }
-        // the next group rewrites shared memory: wait for this group's readers
-        if (big) __syncthreads(); else __syncwarp();
+        __syncthreads();
     }
 }
 
-template <int ID, int CPB, bool DBG>
+template <int ID, int CPB, bool DBG, int LT>
 __global__ void __launch_bounds__(128, MXFFT_LINES_MINB) k_mx_lines(MxLinesArgs a) {
-    lines_body<ID, CPB, DBG>(a);
+    lines_body_pipe<ID, CPB, DBG, LT>(a);
 }
 
-template <int ID, int CPB, bool DBG>
+template <int ID, int CPB, bool DBG, int LT>
 __global__ void __launch_bounds__(512, 1) k_mx_lines_big(MxLinesArgs a) {
-    lines_body<ID, CPB, DBG>(a);
+    lines_body_direct<ID, CPB, DBG, LT>(a);
 }
 
 // ---------------------------------------------------------------------------
 // launch
 // ---------------------------------------------------------------------------
-template <int ID, int CPB, bool DBG>
-static cudaError_t launch_t(const MxLinesArgs& a, int nt, size_t smem, cudaStream_t st) {
-    static int occ[2] = {0, 0};
+template <int ID, int CPB, bool DBG, int LT, bool BIGK>
+static cudaError_t launch_t(const MxLinesArgs& a, size_t smem, cudaStream_t st) {
+    static int occ = 0;
     static int sms = 0;
-    const bool bigk = nt > 128;
-    auto k = bigk ? k_mx_lines_big<ID, CPB, DBG> : k_mx_lines<ID, CPB, DBG>;
-    if (!occ[bigk]) {
+    const int nt = BIGK ? (1 << a.log2T) : 128;
+    void (*k)(MxLinesArgs);
+    if constexpr (BIGK) k = k_mx_lines_big<ID, CPB, DBG, LT>;
+    else k = k_mx_lines<ID, CPB, DBG, LT>;
+    if (!occ) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
         int dev;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[bigk], k, nt, smem);
+        int o = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, BIGK ? 512 : 128, smem);
         if (e != cudaSuccess) return e;
-        if (occ[bigk] < 1) occ[bigk] = 1;
+        occ = o < 1 ? 1 : o;
     }
     const int lines_per_cta = nt >> a.log2T;
     const int64_t groups = (a.total_lines + lines_per_cta - 1) / lines_per_cta;
-    const int64_t cap = (int64_t)sms * occ[bigk];
+    const int64_t cap = (int64_t)sms * occ;
     const int grid = (int)(groups < cap ? groups : cap);
     k<<<grid, nt, smem, st>>>(a);
     note_launch();
     return cudaGetLastError();
 }
 
+// Specialised (compile-time n) variants: block sizes 16/32/64 (cpb 8..32),
+// n <= 4096.  Everything else -- smaller blocks, n = 8192/16384 and the
+// debug-capture kernels (test instrumentation, n <= 4096 only) -- runs the
+// same code with n taken at run time.
+template <int ID, int CPB, bool DBG>
+static cudaError_t disp_lt(const MxLinesArgs& a, size_t smem, cudaStream_t st) {
+    if (a.log2T > 7) {
+        if constexpr (!DBG) return launch_t<ID, CPB, false, -1, true>(a, smem, st);
+        return cudaErrorInvalidValue;
+    }
+    if constexpr (!DBG && CPB >= 8) {
+        switch (a.log2T) {
+            case 0: return launch_t<ID, CPB, DBG, 0, false>(a, smem, st);
+            case 1: return launch_t<ID, CPB, DBG, 1, false>(a, smem, st);
+            case 2: return launch_t<ID, CPB, DBG, 2, false>(a, smem, st);
+            case 3: return launch_t<ID, CPB, DBG, 3, false>(a, smem, st);
+            case 4: return launch_t<ID, CPB, DBG, 4, false>(a, smem, st);
+            case 5: return launch_t<ID, CPB, DBG, 5, false>(a, smem, st);
+            case 6: return launch_t<ID, CPB, DBG, 6, false>(a, smem, st);
+            case 7: return launch_t<ID, CPB, DBG, 7, false>(a, smem, st);
+        }
+        return cudaErrorInvalidValue;
+    } else {
+        return launch_t<ID, CPB, DBG, -1, false>(a, smem, st);
+    }
+}
+
 template <int ID, bool DBG>
-static cudaError_t disp_cpb(const MxLinesArgs& a, int cpb, int nt, size_t smem, cudaStream_t st) {
+static cudaError_t disp_cpb(const MxLinesArgs& a, int cpb, size_t smem, cudaStream_t st) {
     switch (cpb) {
-        case 1: return launch_t<ID, 1, DBG>(a, nt, smem, st);
-        case 2: return launch_t<ID, 2, DBG>(a, nt, smem, st);
-        case 4: return launch_t<ID, 4, DBG>(a, nt, smem, st);
-        case 8: return launch_t<ID, 8, DBG>(a, nt, smem, st);
-        case 16: return launch_t<ID, 16, DBG>(a, nt, smem, st);
-        case 32: return launch_t<ID, 32, DBG>(a, nt, smem, st);
+        case 1: return disp_lt<ID, 1, DBG>(a, smem, st);
+        case 2: return disp_lt<ID, 2, DBG>(a, smem, st);
+        case 4: return disp_lt<ID, 4, DBG>(a, smem, st);
+        case 8: return disp_lt<ID, 8, DBG>(a, smem, st);
+        case 16: return disp_lt<ID, 16, DBG>(a, smem, st);
+        case 32: return disp_lt<ID, 32, DBG>(a, smem, st);
     }
     return cudaErrorInvalidValue;
 }

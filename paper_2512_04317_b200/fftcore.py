@@ -214,12 +214,17 @@ def fft_cols_device(x, plan: FftPlan, inverse: bool = False, out=None):
     return y
 
 
-def fft2_device(x, plan: FftPlan, mode: str = "forward", k=None, k_group: int = 1, out=None):
+def fft2_device(x, plan: FftPlan, mode: str = "forward", k=None, k_group: int = 1, out=None,
+                workspace=None):
     """Batched 2-D MX transform of CUDA complex64 images (B, n, n).
 
     mode: "forward" | "inverse" | "roundtrip" (forward, inverse, x 1/n^2).
     k: optional CUDA int32 tensor of prescale exponents, one per k_group
-    images; fuses apply_prescale on load and undo_prescale on store."""
+    images; fuses apply_prescale on load and undo_prescale on store.
+    workspace: None = take a scratch buffer from torch's caching allocator
+    (every pass is then a row pass with a transposed store); a CUDA tensor of
+    at least mxfft_fft2_workspace_bytes bytes; or False = no scratch (the
+    column pass runs in place on the output, same results)."""
     import torch
 
     _require_mx(plan)
@@ -237,9 +242,16 @@ def fft2_device(x, plan: FftPlan, mode: str = "forward", k=None, k_group: int = 
         if k.dtype != torch.int32 or not k.is_cuda:
             raise TypeError("k must be a CUDA int32 tensor")
         kp = k.data_ptr()
-    _native.check(_native.lib().mxfft_fft2(plan.handle, x.data_ptr(), y.data_ptr(), batch,
-                                           MODE_CODES[mode], kp, int(k_group),
-                                           _native.stream_handle()))
+    L = _native.lib()
+    wp, wb = None, 0
+    if workspace is not False:
+        need = int(L.mxfft_fft2_workspace_bytes(plan.handle, batch))
+        if need > 0:
+            if workspace is None:
+                workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+            wp, wb = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+    _native.check(L.mxfft_fft2(plan.handle, x.data_ptr(), y.data_ptr(), batch, MODE_CODES[mode],
+                               kp, int(k_group), wp, wb, _native.stream_handle()))
     return y
 
 

@@ -197,6 +197,38 @@ def test_fft2_golden(mx):
         assert_same(mx.fft_2d(x, p, "inverse"), g[f"c{ci}_inv"], f"{case} inv")
 
 
+@pytest.mark.parametrize("n,batch", [(32, 3), (32, 5), (64, 3), (256, 2), (1024, 1)])
+def test_fft2_transposed_store_vs_inplace_and_oracle(mx, torch, rng, n, batch):
+    """mxfft_fft2 with a workspace (row passes with transposed stores, partial
+    last tile when n=32) == without (column pass in place) == oracle fft_2d."""
+    x = (rng.standard_normal((batch, n, n)) + 1j * rng.standard_normal((batch, n, n)))
+    x = (x * 10.0 ** rng.uniform(-3, 3, (batch, 1, 1))).astype(np.complex64)
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.E4M3, 32))
+    op = O.make_plan(n, O.E4M3, 32)
+    xd = torch.from_numpy(x).cuda()
+    for mode, inv in (("forward", False), ("inverse", True)):
+        a = mx.fft2_device(xd, p, mode).cpu().numpy()
+        b = mx.fft2_device(xd, p, mode, workspace=False).cpu().numpy()
+        assert_same(a, b, f"{n}x{batch} {mode} ws vs in-place")
+        for i in range(batch):
+            assert_same(a[i], O.fft2(x[i], op, inv), f"{n}x{batch} {mode} image {i}")
+    k = torch.tensor([3, -2, 5, 0, 1][:batch], dtype=torch.int32, device="cuda")
+    a = mx.fft2_device(xd, p, "roundtrip", k=k).cpu().numpy()
+    b = mx.fft2_device(xd, p, "roundtrip", k=k, workspace=False).cpu().numpy()
+    assert_same(a, b, f"{n}x{batch} roundtrip ws vs in-place")
+
+
+def test_fft2_transposed_store_big_lines(mx, torch, rng):
+    """n = 8192 (one line per CTA, direct loads): transposed-store path equals
+    the in-place column path bit for bit."""
+    n = 8192
+    x = torch.randn(1, n, n, dtype=torch.complex64, device="cuda")
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.E4M3, 32))
+    a = mx.fft2_device(x, p, "forward")
+    b = mx.fft2_device(x, p, "forward", workspace=False)
+    assert torch.equal(torch.view_as_real(a), torch.view_as_real(b))
+
+
 def test_pipelines_golden(mx):
     g = golden("pipelines")
     cfg = mx.PrescaleConfig()

@@ -43,7 +43,7 @@ def test_sass_uses_hardware_minifloat_packs():
     import subprocess
 
     sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun",
-                           "_ZN5mxfft10k_mx_linesILi0ELi16ELb0EEEvNS_11MxLinesArgsE", _native.LIB_PATH],
+                           "_ZN5mxfft10k_mx_linesILi0ELi16ELb0ELi3EEEvNS_11MxLinesArgsE", _native.LIB_PATH],
                           capture_output=True, text=True).stdout
     assert "F2FP.SATFINITE.E4M3.F32.PACK_AB" in sass
     assert "F2FP.F16.E4M3.UNPACK_B" in sass

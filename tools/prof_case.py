@@ -1,7 +1,7 @@
 """Profiling driver: runs individual passes of the C2 workload so ncu can
 capture one kernel at a time.
 
-usage: python tools/prof_case.py [rows|cols|stats|rt|fwd] [reps]
+usage: python tools/prof_case.py [rows|cols|stats|fft2|rt|fwd] [reps]
 env:   PROF_N (256), PROF_BATCH (256), PROF_FMT (e4m3), PROF_B (32)
 """
 import os
@@ -31,6 +31,8 @@ for _ in range(reps):
         mx.fftcore.fft_cols_device(x, plan, False, out=y)
     elif what == "stats":
         mx.prescale_stats_device(x, batch, n * n, cfg)
+    elif what == "fft2":
+        mx.fft2_device(x, plan, "forward", out=y)
     elif what == "fwd":
         mx.pipeline_device(x, plan, cfg, roundtrip=False, out=y)
     else:
