@@ -58,6 +58,12 @@ struct MxLinesArgs {
     const int32_t* kvec;
     int k_group, kin_sign, kout_sign, kout_const, stage_limit;
     int tw_chunks;
+    // exact replay (replay_lines): reference-literal tables of the plan
+    FmtDesc fmt;
+    int cpb;
+    const double* wcr;
+    const double* wci;
+    const int* wsexp;
     int32_t* d_vexp;
     float* d_vcodes;
     int32_t* d_pexp;

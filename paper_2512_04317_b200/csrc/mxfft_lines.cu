@@ -69,6 +69,11 @@ cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
     a.stage_limit = lp.stage_limit >= 0 ? lp.stage_limit : p.log2n;
     if (lp.stage_limit < 0 && g_profile_stage_limit >= 0 && g_profile_stage_limit < p.log2n)
         a.stage_limit = g_profile_stage_limit;  // profiling knob (mxfft_profile_stage_limit)
+    a.fmt = p.fmt;
+    a.cpb = p.cpb;
+    a.wcr = p.d_wcr;
+    a.wci = p.d_wci;
+    a.wsexp = p.d_wsexp;
     a.d_vexp = lp.d_vexp;
     a.d_vcodes = lp.d_vcodes;
     a.d_pexp = lp.d_pexp;

@@ -25,6 +25,7 @@
 // folded into u +- t).  Twiddles live in shared memory as packed f16 codes.
 #pragma once
 #include "mxfft_common.cuh"
+#include "mxfft_generic.cuh"
 #include "mxfft_internal.h"
 
 namespace mxfft {
@@ -233,7 +234,7 @@ __device__ __forceinline__ float amax_2(const float (&a)[NB], const float (&b)[N
 
 template <int ID, int NB, bool PAIR, bool DBG>
 __device__ __forceinline__ void mxb(float2 (&u)[NB], float2 (&v)[NB], const unsigned (&w)[NB],
-                                    int ew, const LDbg* d, int bfly0) {
+                                    int ew, const LDbg* d, int bfly0, bool& bad) {
     using F = HwFmt<ID>;
     using Rg = DecodeRange<F>;
     const float am = pair_max<PAIR>(amax_c<NB>(v));
@@ -250,7 +251,9 @@ __device__ __forceinline__ void mxb(float2 (&u)[NB], float2 (&v)[NB], const unsi
     const int sh = ap > F::MAXF ? shift_for<F>(ap) : 0;
     const int E = ew + ev + sh;
     const bool fast = (ev >= -127) & (ev <= 126) & (E >= Rg::ELO) & (E <= Rg::EHI);
-    if (__builtin_expect(!fast, 0)) {
+    if constexpr (!DBG) {
+        bad |= !fast;  // the group is replayed exactly (replay_lines); keep going
+    } else if (__builtin_expect(!fast, 0)) {
         float2 tu[NB], tv[NB];
         unsigned tw[NB];
 #pragma unroll
@@ -317,7 +320,7 @@ __device__ __forceinline__ bool trivial_block(float2 (&u)[NB], float2 (&v)[NB], 
 // path).  Stages 2..4 run the general block inline.
 template <int ID, int CPB, int S, bool DBG>
 __device__ __forceinline__ void local_stage(float2 (&x)[32], const unsigned* tw, const signed char* twe,
-                                            int c, bool trivial, float sigma, LDbg* d) {
+                                            int c, bool trivial, float sigma, LDbg* d, bool& bad) {
     constexpr int half = 1 << S;
     constexpr int NB = CPB < 16 ? CPB : 16;
     constexpr bool PAIR = CPB == 32;
@@ -335,7 +338,9 @@ __device__ __forceinline__ void local_stage(float2 (&x)[32], const unsigned* tw,
         const int bfly0 = c * 16 + k * NB;
         if (S <= 1) {
             bool done = trivial && trivial_block<ID, NB, PAIR, S, DBG>(ub, vb, j0, sigma, d, bfly0);
-            if (!done) {
+            if constexpr (!DBG) {
+                bad |= !done;
+            } else if (!done) {
                 // exact out-of-line path (also covers plans whose stage-0/1
                 // twiddles are not exactly 1 / -i)
                 float2 tu[NB], tv[NB];
@@ -361,7 +366,7 @@ __device__ __forceinline__ void local_stage(float2 (&x)[32], const unsigned* tw,
             unsigned w[NB];
 #pragma unroll
             for (int i = 0; i < NB; ++i) w[i] = tw[tws(half + ((k * NB + i) & (half - 1)))];
-            mxb<ID, NB, PAIR, DBG>(ub, vb, w, twe[half + j0], d, bfly0);
+            mxb<ID, NB, PAIR, DBG>(ub, vb, w, twe[half + j0], d, bfly0, bad);
         }
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
@@ -380,8 +385,10 @@ static __device__ __noinline__ void scale32_slow(float2* x, int e) {
     for (int i = 0; i < 32; ++i) x[i] = make_float2((float)((double)x[i].x * f), (float)((double)x[i].y * f));
 }
 
-__device__ __forceinline__ void scale32(float2 (&x)[32], int e) {
-    if (e >= -126 && e <= 127) {
+template <bool DBG>
+__device__ __forceinline__ void scale32(float2 (&x)[32], int e, bool& bad) {
+    if (!DBG || (e >= -126 && e <= 127)) {
+        bad |= !(e >= -126 && e <= 127);  // non-debug kernels replay the group
         const float f = exp2i(e);
 #pragma unroll
         for (int i = 0; i < 32; ++i) x[i] = make_float2(x[i].x * f, x[i].y * f);
@@ -460,7 +467,7 @@ __device__ __forceinline__ void lsync(bool big) {
 // One shared-memory stage s >= 5 (thread t takes butterflies [16t, 16t+16)).
 template <int ID, int CPB, bool DBG>
 __device__ __forceinline__ void smem_stage(float2 (&x)[32], int& U, int& V, const LCtx& L, unsigned rb,
-                                           int ebase, int s, bool big, LDbg* dbg) {
+                                           int ebase, int s, bool big, LDbg* dbg, bool& bad) {
     constexpr int NB = CPB < 16 ? CPB : 16;
     constexpr bool PAIR = CPB == 32;
     {  // publish current values at their positions
@@ -505,7 +512,7 @@ __device__ __forceinline__ void smem_stage(float2 (&x)[32], int& U, int& V, cons
             vb[i] = x[16 + k * NB + i];
             wb[i] = w16[k * NB + i];
         }
-        mxb<ID, NB, PAIR, DBG>(ub, vb, wb, L.twe[half + j0 + k * NB], dbg, b0 + k * NB);
+        mxb<ID, NB, PAIR, DBG>(ub, vb, wb, L.twe[half + j0 + k * NB], dbg, b0 + k * NB, bad);
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
             x[k * NB + i] = ub[i];
@@ -520,28 +527,22 @@ __device__ __forceinline__ void smem_stage(float2 (&x)[32], int& U, int& V, cons
 // line positions U.., x[16..31] at V.. .
 template <int ID, int CPB, bool DBG, int LT>
 __device__ __forceinline__ void run_stages(float2 (&x)[32], int& U, int& V, const LCtx& L,
-                                           unsigned rb, int ebase, LDbg* dbg) {
+                                           unsigned rb, int ebase, LDbg* dbg, bool& bad) {
     const int lt = LT >= 0 ? LT : L.lt;
     const bool big = lt > 5;  // a line spans several warps
     const int lim_loc = L.slim < 5 ? L.slim : 5;
-    if (lim_loc > 0) local_stage<ID, CPB, 0, DBG>(x, L.tw, L.twe, L.c, L.trivial, L.sigma, dbg);
-    if (lim_loc > 1) local_stage<ID, CPB, 1, DBG>(x, L.tw, L.twe, L.c, L.trivial, L.sigma, dbg);
-    if (lim_loc > 2) local_stage<ID, CPB, 2, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg);
-    if (lim_loc > 3) local_stage<ID, CPB, 3, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg);
-    if (lim_loc > 4) local_stage<ID, CPB, 4, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg);
+    if (lim_loc > 0) local_stage<ID, CPB, 0, DBG>(x, L.tw, L.twe, L.c, L.trivial, L.sigma, dbg, bad);
+    if (lim_loc > 1) local_stage<ID, CPB, 1, DBG>(x, L.tw, L.twe, L.c, L.trivial, L.sigma, dbg, bad);
+    if (lim_loc > 2) local_stage<ID, CPB, 2, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg, bad);
+    if (lim_loc > 3) local_stage<ID, CPB, 3, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg, bad);
+    if (lim_loc > 4) local_stage<ID, CPB, 4, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg, bad);
     U = 32 * L.c;
     V = U + 16;
-    if constexpr (LT >= 0) {
-#pragma unroll
-        for (int s = 5; s < LT + 5; ++s) {
-            if (s >= L.slim) break;
-            smem_stage<ID, CPB, DBG>(x, U, V, L, rb, ebase, s, big, dbg);
-        }
-    } else {
-        const int last = L.slim < lt + 5 ? L.slim : lt + 5;
+    // kept rolled: one copy of the stage body keeps the kernel inside the
+    // instruction cache (unrolling measured slower)
+    const int last = L.slim < lt + 5 ? L.slim : lt + 5;
 #pragma unroll 1
-        for (int s = 5; s < last; ++s) smem_stage<ID, CPB, DBG>(x, U, V, L, rb, ebase, s, big, dbg);
-    }
+    for (int s = 5; s < last; ++s) smem_stage<ID, CPB, DBG>(x, U, V, L, rb, ebase, s, big, dbg, bad);
 }
 
 __device__ __forceinline__ void cp_async16(unsigned dst, const void* src, bool valid) {
@@ -583,6 +584,51 @@ __device__ __forceinline__ void init_dbg(LDbg& dbg, const MxLinesArgs& a, int n,
     }
 }
 
+// Exact replay of `nlines` lines (gl0, gl0 + 1, ...) whose regions start at
+// tile elements e0(j): reload each line from HBM into its region and run the
+// reference-literal stages (mxfft_generic.cuh) with all threads of the CTA.
+// Taken when any block of the group left the fast exponent range (or a
+// prescale exponent is not a normal-float power of two); the fast path's
+// results for the group are discarded.  The group's input is still intact:
+// its stores happen after this point.
+static __device__ __noinline__ void replay_lines(const MxLinesArgs& a, int64_t gl0, int nlines, char* tile,
+                                                 int lpr_shift, int region, int lpr_mask) {
+    const int n = a.n, m = n / 2, tid = threadIdx.x, nthr = blockDim.x;
+    for (int j = 0; j < nlines; ++j) {
+        const int64_t gl = gl0 + j;
+        if (gl >= a.total_lines) break;
+        const int e0 = (j >> lpr_shift) * region + (j & lpr_mask) * n;
+        auto acc = [tile, e0](int i) {
+            const int e = e0 + i;
+            return reinterpret_cast<float2*>(tile + 16 * dsw(e >> 1) + 8 * (e & 1));
+        };
+        int64_t base, es;
+        if (a.col_mode) {
+            base = (gl >> a.log2n) * (int64_t)n * n + (gl & (n - 1));
+            es = n;
+        } else {
+            base = gl * n;
+            es = 1;
+        }
+        const int64_t img = gl / a.lines_per_image;
+        const int kk = a.kvec ? a.kvec[img / a.k_group] : 0;
+        const int kin = a.kin_sign * kk, kout = a.kout_sign * kk + a.kout_const;
+        __syncthreads();
+        for (int i = tid; i < n; i += nthr) {
+            const int r = (int)(__brev((unsigned)i) >> (32 - a.log2n));
+            *acc(i) = gscale(a.in[base + (int64_t)r * es], kin);
+        }
+        __syncthreads();
+        const int last = a.stage_limit < a.log2n ? a.stage_limit : a.log2n;
+        for (int s = 0; s < last; ++s) {
+            generic_stage(acc, s, m, a.cpb, a.fmt, a.wcr, a.wci, a.wsexp, a.inverse != 0, tid, nthr);
+            __syncthreads();
+        }
+        for (int i = tid; i < n; i += nthr) *acc(i) = gscale(*acc(i), kout);
+    }
+    __syncthreads();
+}
+
 // Lines of n <= 4096 (T <= 128 threads per line; 128-thread CTAs): a software
 // pipeline per CTA.  While group g computes, group g+1's tile streams into the
 // other shared buffer with cp.async (16-byte chunks of contiguous rows, or
@@ -615,6 +661,7 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
     L.slim = a.stage_limit;
     const int rcol = lt ? (int)(__brev((unsigned)L.c) >> (32 - lt)) : 0;
     const unsigned buf0 = (unsigned)__cvta_generic_to_shared(smem4 + a.tw_chunks);
+    char* const tile_g = reinterpret_cast<char*>(smem4 + a.tw_chunks);  // generic view (replay)
     constexpr unsigned BUFSZ = (unsigned)GEL * 8u;
     if (buf0 & 127u) __trap();  // radr() ORs chunk offsets into 128-byte-aligned run bases
     // this thread's line inside the buffer (tile element belem(j, q) = line j, position q)
@@ -635,42 +682,41 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
     LDbg dbg;
     init_dbg<DBG>(dbg, a, N, CPB);
 
+    // column-mode loads (mxfft_fft_cols / fft2 without workspace) only in the
+    // run-time-n variant: the specialised kernels stay small
+    const bool col_in = LT < 0 && a.col_mode;
     auto issue_tile = [&](int64_t grp, unsigned buf) {
-        if (!a.col_mode) {
+        if (!col_in) {
             const int64_t base = grp * LPC * (int64_t)N;
             const float4* src = reinterpret_cast<const float4*>(a.in + base) + tid;
-            if ((grp + 1) * LPC <= a.total_lines) {
+            const int64_t lim = (a.total_lines * (int64_t)N - base) / 2;  // chunks left
 #pragma unroll
-                for (int k = 0; k < 16; ++k) cp_async16(caddr(buf, rch ^ dsw(NT * k), 0), src + NT * k, true);
-            } else {
-                const int64_t lim = (a.total_lines * (int64_t)N - base) / 2;  // chunks left
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const bool ok = tid + NT * k < lim;
-                    cp_async16(caddr(buf, rch ^ dsw(NT * k), 0), ok ? (const void*)(src + NT * k) : (const void*)a.in, ok);
-                }
+            for (int k = 0; k < 16; ++k) {
+                const bool ok = tid + NT * k < lim;
+                cp_async16(caddr(buf, rch ^ dsw(NT * k), 0), ok ? (const void*)(src + NT * k) : (const void*)a.in, ok);
             }
         } else {
             const int64_t gl = grp * LPC + tj;
             const bool ok = gl < a.total_lines;
             const int64_t img = gl >> LN;
             const float2* src = a.in + (ok ? img * (int64_t)N * N + (int64_t)tq0 * N + (gl & (N - 1)) : 0);
-#pragma unroll
+#pragma unroll 8
             for (int k = 0; k < 32; ++k)
                 cp_async8(caddr(buf, tch ^ dsw((T * k) >> 1), th ^ ((T * k) & 1)),
                           ok ? src + (int64_t)k * T * N : src, ok);
         }
     };
 
-    if (blockIdx.x < ngroups) issue_tile(blockIdx.x, buf0);
-    cp_commit();
-    int cur = 0;
-    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    // iteration "grp - gridDim.x" only issues the first tile (one issue site)
+    int cur = 1;
+    for (int64_t grp = (int64_t)blockIdx.x - gridDim.x; grp < ngroups; grp += gridDim.x) {
         const int64_t nxt = grp + gridDim.x;
         const unsigned bcur = buf0 + (unsigned)cur * BUFSZ, bnxt = buf0 + (unsigned)(cur ^ 1) * BUFSZ;
+        cur ^= 1;
         __syncthreads();  // the other buffer's previous readers are done
         if (nxt < ngroups) issue_tile(nxt, bnxt);
         cp_commit();
+        if (grp < 0) continue;
         cp_wait<1>();     // this thread's copies of group grp have landed
         __syncthreads();  // ... and everybody's
 
@@ -687,17 +733,20 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
 
         // bit-reversed gather (fftcore.py:262): x[rev5(m)] <- line element m*T + rev_T(c)
         float2 x[32];
+        bool bad = false;
 #pragma unroll
         for (int m = 0; m < 32; ++m)
             x[rev_c<5>(m)] = lds64(caddr(bcur, gch ^ dsw((m * T) >> 1), lt ? gh : (m & 1)));
-        if (kin) scale32(x, kin);
+        if (kin) scale32<DBG>(x, kin, bad);
 
         int U, V;
-        run_stages<ID, CPB, DBG, LT>(x, U, V, L, bcur, ebase, &dbg);
+        run_stages<ID, CPB, DBG, LT>(x, U, V, L, bcur, ebase, &dbg, bad);
 
         // publish (undo_prescale / 1/n^2 fused), then coalesced stores
-        if (kout) scale32(x, kout);
-        {
+        if (kout) scale32<DBG>(x, kout, bad);
+        if (!DBG && __syncthreads_or(bad)) {
+            replay_lines(a, grp * LPC, LPC, tile_g + (bcur - buf0), lt > 5 ? 0 : 5 - lt, W * 32, LPR - 1);
+        } else {
             const Run ru = mkrun(bcur, ebase + U), rv = mkrun(bcur, ebase + V);
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -709,11 +758,10 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
         if (!strided_out) {
             const int64_t base = grp * LPC * (int64_t)N;
             float4* dst = reinterpret_cast<float4*>(a.out + base) + tid;
-            const bool full = (grp + 1) * LPC <= a.total_lines;
-            const int64_t lim = full ? (int64_t)GEL : (a.total_lines * (int64_t)N - base) / 2;
+            const int64_t lim = (a.total_lines * (int64_t)N - base) / 2;
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
-                if (full || tid + NT * k < lim) {
+                if (tid + NT * k < lim) {
                     float2 p0, p1;
                     lds128(caddr(bcur, rch ^ dsw(NT * k), 0), p0, p1);
                     dst[NT * k] = make_float4(p0.x, p0.y, p1.x, p1.y);
@@ -729,7 +777,6 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
                     dst[(int64_t)k * T * N] = lds64(caddr(bcur, tch ^ dsw((T * k) >> 1), th ^ ((T * k) & 1)));
             }
         }
-        cur ^= 1;
     }
     cp_wait<0>();
 }
@@ -787,16 +834,25 @@ __device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
         const int kout = a.kout_sign * kk + a.kout_const;
         if (DBG) dbg.row = line;
         float2 x[32];
+        bool bad = false;
         {
             const float2* src = a.in + base + (int64_t)rcol * es;
             const int64_t stride = (int64_t)T * es;
 #pragma unroll
             for (int m = 0; m < 32; ++m) x[rev_c<5>(m)] = __ldg(src + m * stride);
-            if (kin) scale32(x, kin);
+            if (kin) scale32<DBG>(x, kin, bad);
         }
         int U, V;
-        run_stages<ID, CPB, DBG, LT>(x, U, V, L, rb, ebase, &dbg);
-        if (kout) scale32(x, kout);
+        run_stages<ID, CPB, DBG, LT>(x, U, V, L, rb, ebase, &dbg, bad);
+        if (kout) scale32<DBG>(x, kout, bad);
+        if (!DBG && __syncthreads_or(bad)) {
+            char* tile = reinterpret_cast<char*>(smem4 + a.tw_chunks);
+            replay_lines(a, line, 1, tile, 0, N, 0);
+            for (int i = tid; i < N; i += blockDim.x)
+                a.out[obase + (int64_t)i * oes] = *reinterpret_cast<const float2*>(tile + 16 * dsw(i >> 1) + 8 * (i & 1));
+            __syncthreads();
+            continue;
+        }
         float2* du = a.out + obase + (int64_t)U * oes;
         float2* dv = a.out + obase + (int64_t)V * oes;
         if (oes == 1) {
@@ -869,6 +925,7 @@ static cudaError_t disp_lt(const MxLinesArgs& a, size_t smem, cudaStream_t st) {
         return cudaErrorInvalidValue;
     }
     if constexpr (!DBG && CPB >= 8) {
+        if (a.col_mode) return launch_t<ID, CPB, DBG, -1, false>(a, smem, st);
         switch (a.log2T) {
             case 0: return launch_t<ID, CPB, DBG, 0, false>(a, smem, st);
             case 1: return launch_t<ID, CPB, DBG, 1, false>(a, smem, st);
