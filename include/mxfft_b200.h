@@ -173,6 +173,9 @@ int32_t mxfft_selftest_hw_quantizer(const mxfft_format* fmt, uint64_t* d_mismatc
 /* Profiling knob: run only the first `limit` butterfly stages of every line
  * pass (the output is then NOT a transform); limit < 0 restores full passes. */
 void mxfft_profile_stage_limit(int32_t limit);
+/* Profiling knob for the line kernel: bit 0 skips the tile loads, bit 1 the
+ * stores (outputs are then NOT valid); 0 restores normal passes. */
+void mxfft_profile_flags(int32_t flags);
 
 /* Total number of kernels this library has launched in the process
  * (bookkeeping for the benchmark's gpu_launches count). */

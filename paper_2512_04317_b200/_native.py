@@ -14,7 +14,8 @@ import numpy as np
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libmxfft_b200.so")
+# MXFFT_B200_LIB: an alternative build of the same library (A/B profiling)
+LIB_PATH = os.environ.get("MXFFT_B200_LIB") or os.path.join(_HERE, "_lib", "libmxfft_b200.so")
 
 _lib = None
 
@@ -43,6 +44,7 @@ SIGNATURES = {
     "mxfft_last_error": ([], ctypes.c_char_p),
     "mxfft_launch_count": ([], _i64),
     "mxfft_profile_stage_limit": ([_i32], None),
+    "mxfft_profile_flags": ([_i32], None),
     "mxfft_quantize_f64": ([_vp, _vp, _i64, _fp, _vp, _u], _i32),
     "mxfft_mx_encode_f64": ([_vp, _i64, _i32, _fp, _vp, _vp, _vp, _u], _i32),
     "mxfft_mx_decode_f64": ([_vp, _vp, _i64, _i32, _vp, _u], _i32),

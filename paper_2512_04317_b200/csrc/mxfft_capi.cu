@@ -86,6 +86,7 @@ const char* mxfft_last_error(void) { return g_err.c_str(); }
 int64_t mxfft_launch_count(void) { return g_launches.load(); }
 
 void mxfft_profile_stage_limit(int32_t limit) { mxfft::g_profile_stage_limit = limit; }
+void mxfft_profile_flags(int32_t flags) { mxfft::g_profile_flags = flags; }
 
 int32_t mxfft_quantize_f64(const double* x, double* out, int64_t n, const mxfft_format* fmt,
                            int32_t* d_nonfinite, uintptr_t stream) {

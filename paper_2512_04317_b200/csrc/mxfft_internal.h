@@ -57,6 +57,7 @@ struct MxLinesArgs {
     int trivial01, inverse;
     const int32_t* kvec;
     int k_group, kin_sign, kout_sign, kout_const, stage_limit;
+    int prof_flags;  // profiling only: bit 0 skip tile loads, bit 1 skip stores
     int tw_chunks;
     // exact replay (replay_lines): reference-literal tables of the plan
     FmtDesc fmt;
@@ -87,7 +88,8 @@ struct GenericArgs {
     int k_group, kin_sign, kout_sign, kout_const;
 };
 
-extern int g_profile_stage_limit;  // < 0: off (see mxfft_profile_stage_limit)
+extern int g_profile_stage_limit;
+extern int g_profile_flags;  // < 0: off (see mxfft_profile_stage_limit)
 bool mx_lines_ok(const Plan& p);
 cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st);
 cudaError_t run_lines(const Plan& p, const LinePass& lp, cudaStream_t st);

@@ -36,6 +36,7 @@ static cudaError_t disp_fmt(const MxLinesArgs& a, int id, int cpb, size_t smem, 
 }
 
 int g_profile_stage_limit = -1;
+int g_profile_flags = 0;
 
 bool mx_lines_ok(const Plan& p) {
     if (p.fmt.id == F_GENERIC) return false;
@@ -74,6 +75,7 @@ cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
     a.wcr = p.d_wcr;
     a.wci = p.d_wci;
     a.wsexp = p.d_wsexp;
+    a.prof_flags = g_profile_flags;
     a.d_vexp = lp.d_vexp;
     a.d_vcodes = lp.d_vcodes;
     a.d_pexp = lp.d_pexp;
@@ -85,7 +87,10 @@ cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
     // aligned (run addresses are formed with OR, see radr())
     a.tw_chunks = ((p.n * 5 + 1023) / 1024) * 64;
     // 128-thread kernels double-buffer their group tile (cp.async pipeline)
-    const size_t nbuf = nt == 128 ? 2 : 1;
+#ifndef MXFFT_NBUF
+#define MXFFT_NBUF 2
+#endif
+    const size_t nbuf = nt == 128 ? MXFFT_NBUF : 1;
     const size_t smem = (size_t)a.tw_chunks * 16 + nbuf * (size_t)nt * 32 * sizeof(float2);
     const bool dbg = lp.d_vexp != nullptr;
     return disp_fmt(a, p.fmt.id, p.cpb, smem, dbg, st);

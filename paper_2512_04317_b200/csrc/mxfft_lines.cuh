@@ -686,6 +686,7 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
     // run-time-n variant: the specialised kernels stay small
     const bool col_in = LT < 0 && a.col_mode;
     auto issue_tile = [&](int64_t grp, unsigned buf) {
+        if (a.prof_flags & 1) return;
         if (!col_in) {
             const int64_t base = grp * LPC * (int64_t)N;
             const float4* src = reinterpret_cast<const float4*>(a.in + base) + tid;
@@ -737,6 +738,11 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
 #pragma unroll
         for (int m = 0; m < 32; ++m)
             x[rev_c<5>(m)] = lds64(caddr(bcur, gch ^ dsw((m * T) >> 1), lt ? gh : (m & 1)));
+        if (a.prof_flags & 1) {  // profiling without loads: synthetic in-range data
+#pragma unroll
+            for (int m = 0; m < 32; ++m)
+                x[m] = make_float2((float)((tid * 37 + m * 11) & 255) * 0.01f, (float)((tid * 13 + m * 7) & 127) * 0.01f);
+        }
         if (kin) scale32<DBG>(x, kin, bad);
 
         int U, V;
@@ -755,7 +761,8 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
             }
         }
         __syncthreads();
-        if (!strided_out) {
+        if (a.prof_flags & 2) {
+        } else if (!strided_out) {
             const int64_t base = grp * LPC * (int64_t)N;
             float4* dst = reinterpret_cast<float4*>(a.out + base) + tid;
             const int64_t lim = (a.total_lines * (int64_t)N - base) / 2;
