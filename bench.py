@@ -13,8 +13,9 @@ value  = whole-job round-trip Gpoints/s (sum over ranks; each rank owns a
          256-image shard: weak scaling, no collective on the data path);
 e2e    = same, through the public API with pinned host buffers: every step
          copies the batch H2D, runs the pipeline and copies the result D2H;
-roofline = the dominant kernel's algorithmic HBM bytes (16 B per point per
-         launch: one complex64 read + one write) / its CUDA-event duration;
+roofline = the dominant kernel (the MX line pass, k_mx_lines: 4 launches per
+         round trip) -- algorithmic HBM bytes (16 B per point per launch: one
+         complex64 read + one write) / its CUDA-event duration per launch;
 cpu_baseline = the C oracle (oracle/, a port of the reference algorithm)
          on a bounded sample of the same workload, all host threads.
 
@@ -255,12 +256,15 @@ def main():
     # ---- per-kernel timing for the roofline (same stream, CUDA events) ----
     ms_stats = timed(lambda: mx.prescale_stats_device(x, a.batch, a.n * a.n, cfg, k_out=kbuf,
                                                       res_out=rbuf), a.steps, 2)
-    ms_rows = timed(lambda: mx.fft_rows_device(x, plan, False, out=y), a.steps, 2)
-    ms_cols = timed(lambda: mx.fftcore.fft_cols_device(x, plan, False, out=y), a.steps, 2)
-    kernels = {"prescale_stats": ms_stats, "fft_rows": ms_rows, "fft_cols": ms_cols}
-    # share of the round-trip step: stats once, rows twice, cols twice
-    share = {"prescale_stats": ms_stats / ms, "fft_rows": 2 * ms_rows / ms, "fft_cols": 2 * ms_cols / ms}
-    dom = max(("fft_rows", "fft_cols"), key=lambda k: kernels[k])
+    # the line kernel as the pipeline runs it: a forward fft2 = two row passes
+    # with transposed stores (scratch from torch's caching allocator)
+    ws = torch.empty(int(_native.lib().mxfft_fft2_workspace_bytes(plan.handle, a.batch)),
+                     dtype=torch.uint8, device="cuda")
+    ms_pass = timed(lambda: mx.fft2_device(x, plan, "forward", out=y, workspace=ws), a.steps, 2) / 2
+    kernels = {"prescale_stats": ms_stats, "mx_line_pass": ms_pass}
+    # share of the round-trip step: stats once, four line passes
+    share = {"prescale_stats": ms_stats / ms, "mx_line_pass": 4 * ms_pass / ms}
+    dom = "mx_line_pass"
     peak, peak_src = measured_peak_hbm()
     achieved = BYTES_PER_POINT * pts / (kernels[dom] * 1e-3) / 1e9
     traffic = None

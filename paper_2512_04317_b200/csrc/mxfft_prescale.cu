@@ -185,14 +185,9 @@ __device__ double radix_select(const T* x, int64_t npts, int wlo, int whi, unsig
 }
 
 template <typename T>
-__global__ void __launch_bounds__(PS_THREADS) k_prescale(const T* __restrict__ xall, int64_t npts,
-                                                         PsCfg cfg, mxfft_prescale_result* out,
-                                                         int32_t* kvec, const int* only_if) {
-    // exact fallback for segments the sampled fast path flagged (or all)
-    if (only_if && !only_if[blockIdx.x]) return;
-    extern __shared__ unsigned long long ps_smem[];
-    PsShared& S = *reinterpret_cast<PsShared*>(ps_smem);
-    const T* x = xall + (int64_t)blockIdx.x * npts;
+__device__ void ps_segment(const T* __restrict__ xall, int64_t npts, const PsCfg& cfg,
+                           mxfft_prescale_result* out, int32_t* kvec, const int seg, PsShared& S) {
+    const T* x = xall + (int64_t)seg * npts;
     const int tid = threadIdx.x;
     for (int i = tid; i < NBINS; i += blockDim.x) S.hist[i] = 0;
     if (tid == 0) {
@@ -234,8 +229,8 @@ __global__ void __launch_bounds__(PS_THREADS) k_prescale(const T* __restrict__ x
         if (tid == 0) {
             mxfft_prescale_result r{};
             r.flags = 1;
-            out[blockIdx.x] = r;
-            if (kvec) kvec[blockIdx.x] = 0;
+            out[seg] = r;
+            if (kvec) kvec[seg] = 0;
         }
         return;
     }
@@ -343,14 +338,33 @@ __global__ void __launch_bounds__(PS_THREADS) k_prescale(const T* __restrict__ x
         r.k = k;
         r.flags = amb;
         r.nnz = (int64_t)nnz;
-        out[blockIdx.x] = r;
-        if (kvec) kvec[blockIdx.x] = k;
+        out[seg] = r;
+        if (kvec) kvec[seg] = k;
+    }
+}
+
+// Exact kernel: one CTA per segment, or -- after the sampled fast path -- a
+// small grid working through the list of segments the fast path flagged.
+template <typename T>
+__global__ void __launch_bounds__(PS_THREADS) k_prescale(const T* __restrict__ xall, int64_t npts,
+                                                         PsCfg cfg, mxfft_prescale_result* out,
+                                                         int32_t* kvec, const int* list, const int* list_n) {
+    extern __shared__ unsigned long long ps_smem[];
+    PsShared& S = *reinterpret_cast<PsShared*>(ps_smem);
+    if (!list) {
+        ps_segment(xall, npts, cfg, out, kvec, (int)blockIdx.x, S);
+        return;
+    }
+    const int cnt = *list_n;
+    for (int i = blockIdx.x; i < cnt; i += gridDim.x) {
+        ps_segment(xall, npts, cfg, out, kvec, list[i], S);
+        __syncthreads();
     }
 }
 
 cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, double q,
                                  const mxfft_prescale_cfg& c, mxfft_prescale_result* out,
-                                 int32_t* kvec, void* ws, int** fallback, cudaStream_t st);
+                                 int32_t* kvec, void* ws, int** list, int** list_n, cudaStream_t st);
 int64_t prescale_fast_ws_bytes(int64_t nseg, int64_t npts);
 bool prescale_fast_ok(int64_t npts);
 
@@ -371,7 +385,7 @@ cudaError_t launch_prescale(const void* x, int is_c128, int64_t nseg, int64_t np
             done[1] = true;
         }
         k_prescale<double2><<<(unsigned)nseg, PS_THREADS, smem, st>>>(
-            reinterpret_cast<const double2*>(x), npts, cfg, out, kvec, nullptr);
+            reinterpret_cast<const double2*>(x), npts, cfg, out, kvec, nullptr, nullptr);
         note_launch();
         return cudaGetLastError();
     }
@@ -379,17 +393,21 @@ cudaError_t launch_prescale(const void* x, int is_c128, int64_t nseg, int64_t np
         cudaFuncSetAttribute(k_prescale<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         done[0] = true;
     }
-    const int* only_if = nullptr;
     if (ws && prescale_fast_ok(npts) && ws_bytes >= prescale_fast_ws_bytes(nseg, npts)) {
-        // sampled fast path; segments it cannot settle are flagged for the exact kernel
-        int* fb = nullptr;
+        // sampled fast path; segments it cannot settle are listed for the exact kernel
+        int* list = nullptr;
+        int* list_n = nullptr;
         cudaError_t e = launch_prescale_fast(reinterpret_cast<const float2*>(x), nseg, npts, cfg.q, c,
-                                             out, kvec, ws, &fb, st);
+                                             out, kvec, ws, &list, &list_n, st);
         if (e != cudaSuccess) return e;
-        only_if = fb;
+        const unsigned grid = (unsigned)(nseg < 64 ? nseg : 64);
+        k_prescale<float2><<<grid, PS_THREADS, smem, st>>>(reinterpret_cast<const float2*>(x), npts, cfg,
+                                                            out, kvec, list, list_n);
+        note_launch();
+        return cudaGetLastError();
     }
     k_prescale<float2><<<(unsigned)nseg, PS_THREADS, smem, st>>>(reinterpret_cast<const float2*>(x),
-                                                                  npts, cfg, out, kvec, only_if);
+                                                                  npts, cfg, out, kvec, nullptr, nullptr);
     note_launch();
     return cudaGetLastError();
 }

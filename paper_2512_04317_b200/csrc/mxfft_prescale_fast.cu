@@ -1,6 +1,11 @@
 // mxfft_prescale_fast.cu -- sampled selection for compute_prescale on complex64
 // segments (the pipeline hot path).  Exact; segments it cannot settle are
-// flagged and recomputed by the histogram kernel in mxfft_prescale.cu.
+// listed and recomputed by the histogram kernel in mxfft_prescale.cu.
+//
+// Segments of up to 2^18 points (one image / coil stack of the pipelines) run
+// ONE fused kernel, one CTA per segment: the three steps below back to back,
+// with the bracket candidates kept in shared memory (no global atomics, one
+// read of the segment).  Larger segments use the three kernels:
 //
 //   sample : one CTA per segment reads pseudo-random whole 32-byte sectors
 //            (S = 256 points for segments <= 2^16, 1024 <= 2^18, else 4096),
@@ -17,6 +22,7 @@
 //            sort.  Guards: the selected magnitudes must sit clear of the
 //            window edges by more than the FP32 key rounding, else fall back.
 #include <cfloat>
+#include <cstdio>
 
 #include "../../include/mxfft_b200.h"
 #include "mxfft_common.cuh"
@@ -46,6 +52,14 @@ static inline int sample_size(int64_t npts) {
     return npts < 32768 ? 256 : (npts <= 262144 ? 1024 : SAMPLE_MAX);
 }
 
+constexpr int64_t FUSED_MAX = int64_t(1) << 17;
+// fused kernel: 256 threads for segments <= 2^15 points
+// (several CTAs per SM hide each other's select phase), else 512; 4096 candidates
+constexpr int F_TOPCAP = 1024;  // points above the sample maximum
+constexpr int F_UNR = 4;        // float4 loads per thread per round (double-buffered)
+
+static inline int fused_sample_size(int64_t npts) { return npts < 32768 ? 256 : (npts <= 65536 ? 1024 : 4096); }
+
 static inline int64_t cand_cap(int64_t npts) {
     int64_t c = npts / 4;
     return c < 1024 ? 1024 : (c > 16384 ? 16384 : c);
@@ -53,9 +67,11 @@ static inline int64_t cand_cap(int64_t npts) {
 
 bool prescale_fast_ok(int64_t npts) { return npts >= 1024 && npts <= (int64_t(1) << 24); }
 
+// workspace: SegState[nseg] | fallback list int[nseg] + count | candidates
 int64_t prescale_fast_ws_bytes(int64_t nseg, int64_t npts) {
     const int64_t st = ((int64_t)sizeof(SegState) * nseg + 255) / 256 * 256;
-    const int64_t fb = ((int64_t)sizeof(int) * nseg + 255) / 256 * 256;
+    const int64_t fb = ((int64_t)sizeof(int) * (nseg + 1) + 255) / 256 * 256;
+    if (npts <= FUSED_MAX) return st + fb;
     return st + fb + nseg * (cand_cap(npts) + TOPCAP) * (int64_t)sizeof(float2);
 }
 
@@ -70,6 +86,19 @@ __device__ __forceinline__ double np_cabs_f(double re, double im) {
 // squared-magnitude key (FP32); points with |re|,|im| outside [2^-60, 2^60]
 // are flagged and the segment goes to the exact kernel
 __device__ __forceinline__ float skey(float re, float im) { return __fmaf_rn(re, re, __fmul_rn(im, im)); }
+
+template <typename T>
+struct Limits;
+template <>
+struct Limits<unsigned> {
+    static __device__ __forceinline__ unsigned max() { return 0xffffffffu; }
+    static __device__ __forceinline__ unsigned shfl_xor(unsigned v, int j) { return __shfl_xor_sync(0xffffffffu, v, j); }
+};
+template <>
+struct Limits<double> {
+    static __device__ __forceinline__ double max() { return DBL_MAX; }
+    static __device__ __forceinline__ double shfl_xor(double v, int j) { return __shfl_xor_sync(0xffffffffu, v, j); }
+};
 
 template <typename T>
 __device__ void bitonic_sort(T* a, int P) {  // ascending, P a power of two, whole block
@@ -89,9 +118,86 @@ __device__ void bitonic_sort(T* a, int P) {  // ascending, P a power of two, who
         }
 }
 
+// Block-wide ascending bitonic sort of a[0..P) (P <= NT * SLOTS) with the
+// elements in registers: element i = tid + NT * s lives in slot s of thread
+// tid (pads past P sort last).  Compare-exchange distance j < 32: warp shuffle;
+// j >= NT: between two slots of the same thread; otherwise through shared
+// memory.  SLOTS is exact (sort_block picks it), so no slot is predicated off.
+template <typename T, int NT, int SLOTS>
+__device__ void reg_bitonic_sort(T* a, int P) {
+    constexpr int PE = NT * SLOTS;
+    const int tid = threadIdx.x;
+    T r[SLOTS];
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+        const int i = tid + NT * s;
+        r[s] = i < P ? a[i] : Limits<T>::max();
+    }
+#pragma unroll 1
+    for (int k = 2; k <= PE; k <<= 1) {
+#pragma unroll 1
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= NT) {
+#pragma unroll
+                for (int jb = 1; jb < SLOTS; jb <<= 1) {  // compile-time slot pairs
+                    if (jb != j / NT) continue;
+#pragma unroll
+                    for (int s = 0; s < SLOTS; ++s) {
+                        const int sp = s ^ jb;
+                        if (sp > s) {
+                            const bool asc = ((tid + NT * s) & k) == 0;
+                            const T x = r[s], y = r[sp];
+                            if ((x > y) == asc) {
+                                r[s] = y;
+                                r[sp] = x;
+                            }
+                        }
+                    }
+                }
+            } else if (j >= 32) {
+                __syncthreads();
+#pragma unroll
+                for (int s = 0; s < SLOTS; ++s) a[tid + NT * s] = r[s];
+                __syncthreads();
+#pragma unroll
+                for (int s = 0; s < SLOTS; ++s) {
+                    const int i = tid + NT * s, l = i ^ j;
+                    const T y = a[l];
+                    const bool asc = (i & k) == 0, low = i < l;
+                    // the lower index keeps the min when ascending
+                    r[s] = (low == asc) ? (y < r[s] ? y : r[s]) : (y > r[s] ? y : r[s]);
+                }
+            } else {
+#pragma unroll
+                for (int s = 0; s < SLOTS; ++s) {
+                    const int i = tid + NT * s;
+                    const T y = Limits<T>::shfl_xor(r[s], j);
+                    const bool asc = (i & k) == 0, low = (i & j) == 0;
+                    r[s] = (low == asc) ? (y < r[s] ? y : r[s]) : (y > r[s] ? y : r[s]);
+                }
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s)
+        if (tid + NT * s < P) a[tid + NT * s] = r[s];
+    __syncthreads();
+}
+
+// sort a[0..P), P <= NT * MAXS, with the smallest power-of-two slot count
+template <typename T, int NT, int MAXS>
+__device__ void sort_block(T* a, int P) {
+    if (P <= NT || MAXS == 1) return reg_bitonic_sort<T, NT, 1>(a, P);
+    if (P <= 2 * NT || MAXS == 2) return reg_bitonic_sort<T, NT, (MAXS < 2 ? MAXS : 2)>(a, P);
+    if (P <= 4 * NT || MAXS == 4) return reg_bitonic_sort<T, NT, (MAXS < 4 ? MAXS : 4)>(a, P);
+    if (P <= 8 * NT || MAXS == 8) return reg_bitonic_sort<T, NT, (MAXS < 8 ? MAXS : 8)>(a, P);
+    return reg_bitonic_sort<T, NT, MAXS>(a, P);
+}
+
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(SEL_THREADS) k_ps_sample(const float2* __restrict__ xall, int64_t npts,
-                                                           int S, double q, SegState* st, int* fb) {
+                                                           int S, double q, SegState* st, int* list_n) {
     __shared__ unsigned keys[SAMPLE_MAX];
     __shared__ int snz;
     const int seg = blockIdx.x, tid = threadIdx.x;
@@ -143,7 +249,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_ps_sample(const float2* __restr
         g.nnz = 0;
         g.below = g.ncand = g.ntop = g.flags = 0;
         st[seg] = g;
-        fb[seg] = 0;
+        if (seg == 0) *list_n = 0;
     }
 }
 
@@ -261,7 +367,11 @@ __device__ __forceinline__ unsigned bin_lo(int b, unsigned klo, float inv) {
     return klo + (unsigned)ceilf((float)b / inv);
 }
 
-__global__ void __launch_bounds__(SEL_THREADS) k_ps_select(SegState* st, int* fb, const float2* cand,
+__device__ __forceinline__ void fail_seg(int* list, int* list_n, int seg) { list[atomicAdd(list_n, 1)] = seg; }
+__device__ void finish_result(const mxfft_prescale_cfg& c, double a_max, double p_tau, unsigned long long nnz,
+                              mxfft_prescale_result* out, int32_t* kvec, int seg);
+
+__global__ void __launch_bounds__(SEL_THREADS) k_ps_select(SegState* st, int* list, int* list_n, const float2* cand,
                                                            int64_t cap, const float2* top, double q,
                                                            mxfft_prescale_cfg c,
                                                            mxfft_prescale_result* out, int32_t* kvec) {
@@ -270,7 +380,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_ps_select(SegState* st, int* fb
     const SegState g = st[seg];
     const unsigned long long nnz = g.nnz;
     if (g.flags) {
-        if (tid == 0) fb[seg] = 1;
+        if (tid == 0) fail_seg(list, list_n, seg);
         return;
     }
     double a_max = 0.0, p_tau = 0.0;
@@ -288,7 +398,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_ps_select(SegState* st, int* fb
         }
         const unsigned nc = g.ncand, nt = g.ntop;
         if (!(nc <= cap && nt <= TOPCAP && nt >= 1 && g.below <= r_lo && r_hi < g.below + nc)) {
-            if (tid == 0) fb[seg] = 1;
+            if (tid == 0) fail_seg(list, list_n, seg);
             return;
         }
         const unsigned t = (unsigned)(r_lo - g.below), t1 = (unsigned)(r_hi - g.below);
@@ -345,7 +455,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_ps_select(SegState* st, int* fb
         const int wlo = S.bt > 0 ? S.bt - 1 : 0, whi = S.bt1 < NBIN - 1 ? S.bt1 + 1 : NBIN - 1;
         const unsigned woff = S.woff, wcount = S.wend - S.woff;
         if (wcount > WCAP) {
-            if (tid == 0) fb[seg] = 1;
+            if (tid == 0) fail_seg(list, list_n, seg);
             return;
         }
         for (unsigned i = tid; i < nc; i += SEL_THREADS) {
@@ -368,7 +478,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_ps_select(SegState* st, int* fb
         if (elo > 0.f && !(elo >= 0x1p-100f && vlo * vlo > (double)elo * (1.0 + 0x1p-18))) good = false;
         if (ehi <= FLT_MAX && !(vhi * vhi < (double)ehi * (1.0 - 0x1p-18))) good = false;
         if (!good) {
-            if (tid == 0) fb[seg] = 1;
+            if (tid == 0) fail_seg(list, list_n, seg);
             return;
         }
         a_max = __longlong_as_double((long long)S.amax_b);
@@ -376,50 +486,360 @@ __global__ void __launch_bounds__(SEL_THREADS) k_ps_select(SegState* st, int* fb
         p_tau = gamma >= 0.5 ? __dsub_rn(vhi, __dmul_rn(diff, __dsub_rn(1.0, gamma)))
                              : __dadd_rn(vlo, __dmul_rn(diff, gamma));
     }
+    if (tid == 0) finish_result(c, a_max, p_tau, nnz, out, kvec, seg);
+}
+
+// k (prescale.py:61-73) from a_max / p_tau; flags bit 1 marks a log2 within a
+// few ulps of a rounding boundary (the host re-checks it)
+__device__ void finish_result(const mxfft_prescale_cfg& c, double a_max, double p_tau, unsigned long long nnz,
+                              mxfft_prescale_result* out, int32_t* kvec, int seg) {
+    const double EPS = 1e-30;
+    const double r1 = __ddiv_rn(c.target, a_max > EPS ? a_max : EPS);
+    const double r2 = __ddiv_rn(c.tau_min, p_tau > EPS ? p_tau : EPS);
+    const double L1 = log2(r1), L2 = log2(r2);
+    const int k1 = round_half_away_d(L1);
+    const int k2 = (int)ceil(L2);
+    int k = max(k1, k2);
+    k = min(max(k, c.k_min), c.k_max);
+    const double d1 = fabs(fabs(L1 - trunc(L1)) - 0.5);
+    const double d2 = fabs(L2 - rint(L2));
+    const bool pow2 = (__double_as_longlong(r2) & 0xFFFFFFFFFFFFFll) == 0;
+    const int amb = (d1 < 1e-12 * fmax(1.0, fabs(L1)) || (d2 < 1e-12 * fmax(1.0, fabs(L2)) && !pow2)) ? 2 : 0;
+    mxfft_prescale_result r;
+    r.a_max = a_max;
+    r.p_tau = p_tau;
+    r.k1 = k1;
+    r.k2 = k2;
+    r.k = k;
+    r.flags = amb;
+    r.nnz = (int64_t)nnz;
+    out[seg] = r;
+    if (kvec) kvec[seg] = k;
+}
+
+// ---------------------------------------------------------------------------
+// fused sample -> count -> select, one CTA per segment (segments <= 2^18 points)
+// ---------------------------------------------------------------------------
+template <int NT, int CCAP>
+struct FusedShared {
+    union {
+        unsigned keys[SAMPLE_MAX];  // sample phase
+        double w[WCAP];             // exact-sort window (select phase)
+    } u;
+    float2 cand[CCAP];
+    float2 topb[F_TOPCAP];
+    unsigned hist[NBIN];
+    unsigned warp_sums[NT / 32];
+    unsigned long long amax_b;
+    unsigned snz, nnz, below, ncand, ntop, flags, wn;
+    float lo, hi, top;
+    int bt, bt1;
+    unsigned woff, wend;
+};
+
+template <int NT, int CCAP>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_ps_fused(const float2* __restrict__ xall, int64_t npts, int S,
+                                                           double q, mxfft_prescale_cfg c,
+                                                           mxfft_prescale_result* out, int32_t* kvec, int* list,
+                                                           int* list_n) {
+    constexpr int F_THREADS = NT, F_CCAP = CCAP;
+    extern __shared__ unsigned long long fused_smem[];
+    FusedShared<NT, CCAP>& F = *reinterpret_cast<FusedShared<NT, CCAP>*>(fused_smem);
+    const int seg = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+#ifdef PS_TIMING
+    long long T0 = clock64(), TS[8];
+#define PS_T(i) if (tid == 0) TS[i] = clock64() - T0;
+#else
+#define PS_T(i)
+#endif
+    const float2* x = xall + (int64_t)seg * npts;
     if (tid == 0) {
-        const double EPS = 1e-30;
-        const double r1 = __ddiv_rn(c.target, a_max > EPS ? a_max : EPS);
-        const double r2 = __ddiv_rn(c.tau_min, p_tau > EPS ? p_tau : EPS);
-        const double L1 = log2(r1), L2 = log2(r2);
-        const int k1 = round_half_away_d(L1);
-        const int k2 = (int)ceil(L2);
-        int k = max(k1, k2);
-        k = min(max(k, c.k_min), c.k_max);
-        const double d1 = fabs(fabs(L1 - trunc(L1)) - 0.5);
-        const double d2 = fabs(L2 - rint(L2));
-        const bool pow2 = (__double_as_longlong(r2) & 0xFFFFFFFFFFFFFll) == 0;
-        const int amb = (d1 < 1e-12 * fmax(1.0, fabs(L1)) || (d2 < 1e-12 * fmax(1.0, fabs(L2)) && !pow2)) ? 2 : 0;
-        mxfft_prescale_result r;
-        r.a_max = a_max;
-        r.p_tau = p_tau;
-        r.k1 = k1;
-        r.k2 = k2;
-        r.k = k;
-        r.flags = amb;
-        r.nnz = (int64_t)nnz;
-        out[seg] = r;
-        if (kvec) kvec[seg] = k;
+        F.snz = F.nnz = F.below = F.ncand = F.ntop = F.flags = F.wn = 0;
+        F.amax_b = 0;
     }
+    for (int i = tid; i < NBIN; i += F_THREADS) F.hist[i] = 0;
+    __syncthreads();
+
+    // ---- sample: pseudo-random whole sectors, sorted squared magnitudes ----
+    {
+        const int64_t nsec = npts / 4;
+        int cnt = 0;
+        for (int j = tid; j < S / 4; j += F_THREADS) {
+            const uint64_t h = (uint64_t)j * 2654435761ull;
+            const uint64_t sec = (nsec & (nsec - 1)) == 0 ? (h & (uint64_t)(nsec - 1)) : h % (uint64_t)nsec;
+            const float4* p = reinterpret_cast<const float4*>(x + sec * 4);
+            const float4 a = __ldg(p), b = __ldg(p + 1);
+            const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int hh = 0; hh < 4; ++hh) {
+                const float re = v[2 * hh], im = v[2 * hh + 1];
+                const float m = fmaxf(fabsf(re), fabsf(im));
+                unsigned k = 0xffffffffu;
+                if (m > 0.f) {
+                    const float sk = (m >= 0x1p-60f && m <= 0x1p60f) ? skey(re, im) : (m < 1.f ? 0.f : 0x1p125f);
+                    k = __float_as_uint(sk);
+                    ++cnt;
+                }
+                F.u.keys[j * 4 + hh] = k;
+            }
+        }
+        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (lane == 0) atomicAdd(&F.snz, (unsigned)cnt);
+        __syncthreads();
+        PS_T(0)
+        sort_block<unsigned, F_THREADS, SAMPLE_MAX / F_THREADS>(F.u.keys, S);
+        PS_T(1)
+        if (tid == 0) {
+            const int n = (int)F.snz;
+            if (n == 0) {
+                F.lo = 0.f;
+                F.hi = __int_as_float(0x7f800000);
+                F.top = 0.f;
+            } else {
+                const double rs = (double)(n - 1) * q;
+                const int d = 8 + (int)(4.0 * sqrt(rs + 1.0));
+                const int ilo = (int)floor(rs) - d, ihi = (int)ceil(rs) + 1 + d;
+                F.lo = ilo <= 0 ? 0.f : __uint_as_float(F.u.keys[ilo]) * (1.f - 0x1p-20f);
+                F.hi = ihi >= n ? __int_as_float(0x7f800000) : __uint_as_float(F.u.keys[ihi]) * (1.f + 0x1p-20f);
+                F.top = __uint_as_float(F.u.keys[n - 1]) * (1.f - 0x1p-20f);
+            }
+        }
+        __syncthreads();
+    }
+    const float glo = F.lo, ghi = F.hi, gtop = F.top;
+    PS_T(2)
+
+    // ---- count: one streaming pass, candidates appended to shared memory ----
+    {
+        unsigned nnz = 0, below = 0;
+        float ksum = 0.f;
+        const int64_t npairs = npts / 2;
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        constexpr int64_t STEP = (int64_t)F_THREADS * F_UNR;
+        float4 vn[F_UNR];  // next round's loads are in flight while this one is classified
+#pragma unroll
+        for (int it = 0; it < F_UNR; ++it) {
+            const int64_t pi = it * F_THREADS + tid;
+            vn[it] = pi < npairs ? __ldg(x4 + pi) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (int64_t base = 0; base < npairs; base += STEP) {
+            float4 v[F_UNR];
+#pragma unroll
+            for (int it = 0; it < F_UNR; ++it) {
+                v[it] = vn[it];
+                const int64_t pi = base + STEP + it * F_THREADS + tid;
+                vn[it] = pi < npairs ? __ldg(x4 + pi) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            unsigned cbits = 0, tbits = 0;
+#pragma unroll
+            for (int it = 0; it < F_UNR; ++it) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const float re = h ? v[it].z : v[it].x, im = h ? v[it].w : v[it].y;
+                    const bool nz = (re != 0.f) | (im != 0.f);
+                    const float sk = skey(re, im);
+                    ksum += sk;
+                    nnz += nz;
+                    below += nz & (sk < glo);
+                    cbits |= (unsigned)(nz & (sk >= glo) & (sk <= ghi)) << (2 * it + h);
+                    tbits |= (unsigned)(nz & (sk >= gtop)) << (2 * it + h);
+                }
+            }
+            // candidates are a few percent of the points: one shared atomic per
+            // lane that has any is cheaper than a warp scan every round
+            if (cbits) {
+                unsigned slot = atomicAdd(&F.ncand, (unsigned)__popc(cbits));
+#pragma unroll
+                for (int it = 0; it < F_UNR; ++it)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        if ((cbits >> (2 * it + h)) & 1) {
+                            if (slot < F_CCAP) F.cand[slot] = h ? make_float2(v[it].z, v[it].w) : make_float2(v[it].x, v[it].y);
+                            ++slot;
+                        }
+            }
+            if (tbits) {
+                unsigned slot = atomicAdd(&F.ntop, (unsigned)__popc(tbits));
+#pragma unroll
+                for (int it = 0; it < F_UNR; ++it)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        if ((tbits >> (2 * it + h)) & 1) {
+                            if (slot < F_TOPCAP) F.topb[slot] = h ? make_float2(v[it].z, v[it].w) : make_float2(v[it].x, v[it].y);
+                            ++slot;
+                        }
+            }
+        }
+        unsigned flags = (ksum <= 0x1p126f) ? 0u : 1u;  // non-finite / keys beyond FP32 range
+        for (int o = 16; o; o >>= 1) {
+            nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
+            below += __shfl_xor_sync(0xffffffffu, below, o);
+            flags |= __shfl_xor_sync(0xffffffffu, flags, o);
+        }
+        if (lane == 0) {
+            atomicAdd(&F.nnz, nnz);
+            atomicAdd(&F.below, below);
+            if (flags) atomicOr(&F.flags, flags);
+        }
+        __syncthreads();
+    }
+
+    // ---- select: histogram of the candidates, exact sort of a small window ----
+    PS_T(3)
+    const unsigned long long nnz = F.nnz;
+    if (F.flags) {
+        if (tid == 0) fail_seg(list, list_n, seg);
+        return;
+    }
+    double a_max = 0.0, p_tau = 0.0;
+    if (nnz > 0) {
+        const double virt = __dmul_rn((double)(nnz - 1), q);
+        unsigned long long r_lo, r_hi;
+        double gamma;
+        if (virt >= (double)(nnz - 1)) {
+            r_lo = r_hi = nnz - 1;
+            gamma = __dadd_rn(virt, 1.0);
+        } else {
+            r_lo = (unsigned long long)floor(virt);
+            r_hi = r_lo + 1;
+            gamma = __dsub_rn(virt, (double)r_lo);
+        }
+        const unsigned nc = F.ncand, nt = F.ntop, below = F.below;
+        if (!(nc <= F_CCAP && nt <= F_TOPCAP && nt >= 1 && below <= r_lo && r_hi < below + nc)) {
+            if (tid == 0) fail_seg(list, list_n, seg);
+            return;
+        }
+        const unsigned t = (unsigned)(r_lo - below), t1 = (unsigned)(r_hi - below);
+        const unsigned klo = __float_as_uint(glo), khi = __float_as_uint(ghi);
+        const float inv = (float)NBIN / ((float)(khi - klo) + 1.f);
+        for (unsigned i = tid; i < nc; i += F_THREADS) {
+            const float2 v = F.cand[i];
+            atomicAdd(&F.hist[kbin(__float_as_uint(skey(v.x, v.y)), klo, inv)], 1u);
+        }
+        unsigned long long am = 0;
+        for (unsigned i = tid; i < nt; i += F_THREADS) {
+            const float2 v = F.topb[i];
+            am = max(am, (unsigned long long)__double_as_longlong(np_cabs_f((double)v.x, (double)v.y)));
+        }
+        for (int o = 16; o; o >>= 1) am = max(am, __shfl_xor_sync(0xffffffffu, am, o));
+        if (lane == 0) atomicMax(&F.amax_b, am);
+        __syncthreads();
+        {  // exclusive scan of the histogram (2 bins per thread; threads >= NBIN/2 hold none)
+            const bool has = tid < NBIN / 2;
+            const unsigned h0 = has ? F.hist[2 * tid] : 0u, h1 = has ? F.hist[2 * tid + 1] : 0u;
+            unsigned incl = h0 + h1;
+            const int wp = tid >> 5;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) F.warp_sums[wp] = incl;
+            __syncthreads();
+            unsigned wbase = 0;
+            for (int w2 = 0; w2 < wp; ++w2) wbase += F.warp_sums[w2];
+            const unsigned e0 = wbase + incl - h0 - h1, e1 = e0 + h0;
+            if (has) {
+                if (e0 <= t && t < e1) F.bt = 2 * tid;
+                if (e1 <= t && t < e1 + h1) F.bt = 2 * tid + 1;
+                if (e0 <= t1 && t1 < e1) F.bt1 = 2 * tid;
+                if (e1 <= t1 && t1 < e1 + h1) F.bt1 = 2 * tid + 1;
+            }
+            __syncthreads();
+            const int wlo = F.bt > 0 ? F.bt - 1 : 0, whi = F.bt1 < NBIN - 1 ? F.bt1 + 1 : NBIN - 1;
+            if (has) {
+                if (2 * tid == wlo) F.woff = e0;
+                if (2 * tid + 1 == wlo) F.woff = e1;
+                if (2 * tid == whi) F.wend = e1;
+                if (2 * tid + 1 == whi) F.wend = e1 + h1;
+            }
+        }
+        __syncthreads();
+        const int wlo = F.bt > 0 ? F.bt - 1 : 0, whi = F.bt1 < NBIN - 1 ? F.bt1 + 1 : NBIN - 1;
+        const unsigned woff = F.woff, wcount = F.wend - F.woff;
+        if (wcount > WCAP) {
+            if (tid == 0) fail_seg(list, list_n, seg);
+            return;
+        }
+        PS_T(4)
+        for (unsigned i = tid; i < nc; i += F_THREADS) {
+            const float2 v = F.cand[i];
+            const int b = kbin(__float_as_uint(skey(v.x, v.y)), klo, inv);
+            if (b >= wlo && b <= whi) F.u.w[atomicAdd(&F.wn, 1u)] = np_cabs_f((double)v.x, (double)v.y);
+        }
+        __syncthreads();
+        PS_T(5)
+        int P = 1;
+        while (P < (int)wcount) P <<= 1;
+        for (int i = (int)wcount + tid; i < P; i += F_THREADS) F.u.w[i] = DBL_MAX;
+        __syncthreads();
+        sort_block<double, F_THREADS, WCAP / F_THREADS>(F.u.w, P);
+        PS_T(6)
+#ifdef PS_TIMING
+        if (tid == 0 && (seg == 0 || seg == 100))
+            printf("seg %d S=%d nc=%u wcount=%u P=%d | sampled %lld sorted %lld stream0 %lld streamed %lld hist+scan %lld window %lld wsorted %lld\n",
+                   seg, S, nc, wcount, P, TS[0], TS[1], TS[2], TS[3], TS[4], TS[5], TS[6]);
+#endif
+        const double vlo = F.u.w[t - woff], vhi = F.u.w[t1 - woff];
+        const float elo = wlo > 0 ? __uint_as_float(bin_lo(wlo, klo, inv)) : glo;
+        const float ehi = whi < NBIN - 1 ? __uint_as_float(bin_lo(whi + 1, klo, inv)) : ghi;
+        bool good = true;
+        if (elo > 0.f && !(elo >= 0x1p-100f && vlo * vlo > (double)elo * (1.0 + 0x1p-18))) good = false;
+        if (ehi <= FLT_MAX && !(vhi * vhi < (double)ehi * (1.0 - 0x1p-18))) good = false;
+        if (!good) {
+            if (tid == 0) fail_seg(list, list_n, seg);
+            return;
+        }
+        a_max = __longlong_as_double((long long)F.amax_b);
+        const double diff = __dsub_rn(vhi, vlo);
+        p_tau = gamma >= 0.5 ? __dsub_rn(vhi, __dmul_rn(diff, __dsub_rn(1.0, gamma)))
+                             : __dadd_rn(vlo, __dmul_rn(diff, gamma));
+    }
+    if (tid == 0) finish_result(c, a_max, p_tau, nnz, out, kvec, seg);
 }
 
 cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, double q,
                                  const mxfft_prescale_cfg& c, mxfft_prescale_result* out,
-                                 int32_t* kvec, void* ws, int** fallback, cudaStream_t st) {
+                                 int32_t* kvec, void* ws, int** list_out, int** list_n_out, cudaStream_t st) {
     char* w = reinterpret_cast<char*>(ws);
     SegState* sst = reinterpret_cast<SegState*>(w);
     w += ((int64_t)sizeof(SegState) * nseg + 255) / 256 * 256;
-    int* fb = reinterpret_cast<int*>(w);
-    w += ((int64_t)sizeof(int) * nseg + 255) / 256 * 256;
+    int* list = reinterpret_cast<int*>(w);
+    int* list_n = list + nseg;
+    w += ((int64_t)sizeof(int) * (nseg + 1) + 255) / 256 * 256;
+    *list_out = list;
+    *list_n_out = list_n;
+    if (npts <= FUSED_MAX) {
+        static bool attr = false;
+        if (!attr) {
+            cudaError_t e = cudaFuncSetAttribute(k_ps_fused<256, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)sizeof(FusedShared<256, 4096>));
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(k_ps_fused<512, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(FusedShared<512, 4096>));
+            if (e != cudaSuccess) return e;
+            attr = true;
+        }
+        cudaError_t e = cudaMemsetAsync(list_n, 0, sizeof(int), st);
+        if (e != cudaSuccess) return e;
+        if (npts <= 32768)
+            k_ps_fused<256, 4096><<<(unsigned)nseg, 256, sizeof(FusedShared<256, 4096>), st>>>(
+                x, npts, fused_sample_size(npts), q, c, out, kvec, list, list_n);
+        else
+            k_ps_fused<512, 4096><<<(unsigned)nseg, 512, sizeof(FusedShared<512, 4096>), st>>>(
+                x, npts, fused_sample_size(npts), q, c, out, kvec, list, list_n);
+        note_launch();
+        return cudaGetLastError();
+    }
     const int64_t cap = cand_cap(npts);
     float2* cand = reinterpret_cast<float2*>(w);
     float2* top = cand + nseg * cap;
-    *fallback = fb;
-    k_ps_sample<<<(unsigned)nseg, SEL_THREADS, 0, st>>>(x, npts, sample_size(npts), q, sst, fb);
+    k_ps_sample<<<(unsigned)nseg, SEL_THREADS, 0, st>>>(x, npts, sample_size(npts), q, sst, list_n);
     note_launch();
     const int cps = (int)((npts + CHUNK - 1) / CHUNK);
     k_ps_count<<<(unsigned)(nseg * cps), CNT_THREADS, 0, st>>>(x, npts, cps, sst, cand, cap, top);
     note_launch();
-    k_ps_select<<<(unsigned)nseg, SEL_THREADS, 0, st>>>(sst, fb, cand, cap, top, q, c, out, kvec);
+    k_ps_select<<<(unsigned)nseg, SEL_THREADS, 0, st>>>(sst, list, list_n, cand, cap, top, q, c, out, kvec);
     note_launch();
     return cudaGetLastError();
 }
