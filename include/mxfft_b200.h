@@ -110,6 +110,13 @@ int32_t mxfft_plan_twiddles(mxfft_plan plan, double* h_codes_re, double* h_codes
 int32_t mxfft_fft_rows(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t inverse,
                        uintptr_t stream);
 
+/* mxfft_fft_rows with exact power-of-two scalings fused into the load and the
+ * store: y = 2^exp_out * rows(2^exp_in * x) (apply_prescale / undo_prescale /
+ * 1/n^2, prescale.py:76-91, mri.py:100).  The row passes of a distributed 2-D
+ * transform (paper_2512_04317_b200/distributed.py) use it. */
+int32_t mxfft_fft_rows_scaled(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t inverse,
+                              int32_t exp_in, int32_t exp_out, uintptr_t stream);
+
 /* Batched 1-D MX transform along the COLUMNS of `batch` n x n complex64 images
  * (the second pass of fft_2d, fftcore.py:352, without materialising rows.T);
  * x may alias y.  With mxfft_fft_rows this gives either pass of fft_2d alone. */
@@ -145,6 +152,26 @@ int32_t mxfft_prescale_stats(const void* x, int32_t is_c128, int64_t nseg, int64
                              int32_t* d_k, void* workspace, int64_t workspace_bytes,
                              uintptr_t stream);
 int64_t mxfft_prescale_workspace_bytes(int64_t nseg, int64_t seg_points);
+
+/* Building blocks of compute_prescale over ONE segment that is too large for
+ * a CTA or split across calls / ranks (the C5 global prescale);
+ * paper_2512_04317_b200/prescale.py compute_prescale_global combines them.
+ *  - sample_keys: FP32 squared magnitudes of `nsamples` points taken as
+ *    pseudo-random whole 32-byte sectors of x (complex64, npts a multiple of
+ *    4); zero -> +inf, |re|,|im| outside [2^-60, 2^60] -> 0 or 2^125.
+ *  - count_range: one streaming pass over x (complex64): d_state (40 bytes:
+ *    float lo, hi, top; int pad; uint64 nnz; uint32 below, ncand, ntop,
+ *    flags) receives the nonzero count, the points with key < lo, and the
+ *    numbers of points with key in [lo, hi] and key >= top, which are copied
+ *    (as complex64) to d_cand / d_top up to their capacities.  flags bit 0:
+ *    a non-finite value, or a key beyond FP32 range, was seen.
+ *  - cabs: |z| exactly as numpy's np.abs(complex128), FP64 out. */
+int32_t mxfft_prescale_sample_keys(const void* x, int64_t npts, int64_t nsamples, float* d_keys,
+                                   uintptr_t stream);
+int32_t mxfft_prescale_count_range(const void* x, int64_t npts, float lo, float hi, float top, void* d_state,
+                                   void* d_cand, int64_t cand_cap, void* d_top, int64_t top_cap,
+                                   uintptr_t stream);
+int32_t mxfft_cabs(const void* x, int32_t is_c128, int64_t n, double* out, uintptr_t stream);
 
 /* Root-sum-square coil combine (rss, mri.py:70-81) of per-coil complex images
  * (complex64 when is_c128 == 0, else complex128): x (groups, coils, npix) ->

@@ -53,12 +53,17 @@ SIGNATURES = {
     "mxfft_plan_twiddles": ([_vp, _vp, _vp, _vp], _i32),
     "mxfft_fft_rows": ([_vp, _vp, _vp, _i64, _i32, _u], _i32),
     "mxfft_fft_cols": ([_vp, _vp, _vp, _i64, _i32, _u], _i32),
+    "mxfft_fft_rows_scaled": ([_vp, _vp, _vp, _i64, _i32, _i32, _i32, _u], _i32),
     "mxfft_fft2": ([_vp, _vp, _vp, _i64, _i32, _vp, _i32, _vp, _i64, _u], _i32),
     "mxfft_fft2_workspace_bytes": ([_vp, _i64], _i64),
     "mxfft_prescale_stats": ([_vp, _i32, _i64, _i64, ctypes.POINTER(PrescaleCfgC), _vp, _vp,
                               _vp, _i64, _u], _i32),
     "mxfft_prescale_workspace_bytes": ([_i64, _i64], _i64),
     "mxfft_rss": ([_vp, _i32, _i64, _i32, _i64, _vp, _u], _i32),
+    "mxfft_cabs": ([_vp, _i32, _i64, _vp, _u], _i32),
+    "mxfft_prescale_sample_keys": ([_vp, _i64, _i64, _vp, _u], _i32),
+    "mxfft_prescale_count_range": ([_vp, _i64, ctypes.c_float, ctypes.c_float, ctypes.c_float, _vp, _vp,
+                                    _i64, _vp, _i64, _u], _i32),
     "mxfft_selftest_hw_quantizer": ([_fp, _vp, _vp, _u], _i32),
     "mxfft_fft_rows_debug": ([_vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _u], _i32),
 }

@@ -210,6 +210,24 @@ int32_t mxfft_fft_rows(mxfft_plan plan, const void* x, void* y, int64_t batch, i
     return MXFFT_OK;
 }
 
+int32_t mxfft_fft_rows_scaled(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t inverse,
+                              int32_t exp_in, int32_t exp_out, uintptr_t stream) {
+    if (!plan) return fail(MXFFT_ERR_VALUE, "null plan");
+    if (batch < 0) return fail(MXFFT_ERR_SHAPE, "negative batch");
+    if (batch == 0) return MXFFT_OK;
+    LinePass lp;
+    lp.in = x;
+    lp.out = y;
+    lp.lines_per_image = 1;
+    lp.total_lines = batch;
+    lp.img_elems = plan->p.n;
+    lp.inverse = inverse ? 1 : 0;
+    lp.kin_const = exp_in;
+    lp.kout_const = exp_out;
+    CK(run_lines(plan->p, lp, (cudaStream_t)stream), "fft_rows_scaled");
+    return MXFFT_OK;
+}
+
 int32_t mxfft_fft_cols(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t inverse,
                        uintptr_t stream) {
     if (!plan) return fail(MXFFT_ERR_VALUE, "null plan");
@@ -298,6 +316,33 @@ int32_t mxfft_prescale_stats(const void* x, int32_t is_c128, int64_t nseg, int64
     CK(launch_prescale(x, is_c128, nseg, seg_points, *cfg, d_out, d_k, workspace, workspace_bytes,
                        (cudaStream_t)stream),
        "prescale_stats");
+    return MXFFT_OK;
+}
+
+int32_t mxfft_cabs(const void* x, int32_t is_c128, int64_t n, double* out, uintptr_t stream) {
+    if (n < 0) return fail(MXFFT_ERR_SHAPE, "negative size");
+    CK(launch_cabs(x, is_c128, n, out, (cudaStream_t)stream), "cabs");
+    return MXFFT_OK;
+}
+
+int32_t mxfft_prescale_sample_keys(const void* x, int64_t npts, int64_t nsamples, float* d_keys,
+                                   uintptr_t stream) {
+    if (npts < 4 || (npts & 3)) return fail(MXFFT_ERR_SHAPE, "sampling needs a multiple of 4 points");
+    if (nsamples < 0 || (nsamples & 3)) return fail(MXFFT_ERR_VALUE, "nsamples must be a multiple of 4");
+    CK(launch_prescale_sample_keys(reinterpret_cast<const float2*>(x), npts, nsamples, d_keys,
+                                   (cudaStream_t)stream),
+       "prescale_sample_keys");
+    return MXFFT_OK;
+}
+
+int32_t mxfft_prescale_count_range(const void* x, int64_t npts, float lo, float hi, float top, void* d_state,
+                                   void* d_cand, int64_t cand_cap, void* d_top, int64_t top_cap,
+                                   uintptr_t stream) {
+    if (npts < 0 || (npts & 1)) return fail(MXFFT_ERR_SHAPE, "count needs an even number of points");
+    CK(launch_prescale_count_range(reinterpret_cast<const float2*>(x), npts, lo, hi, top, d_state,
+                                   reinterpret_cast<float2*>(d_cand), cand_cap, reinterpret_cast<float2*>(d_top),
+                                   top_cap, (cudaStream_t)stream),
+       "prescale_count_range");
     return MXFFT_OK;
 }
 

@@ -221,6 +221,26 @@ __global__ void k_rss(const T* __restrict__ x, int64_t groups, int coils, int64_
     }
 }
 
+// |z| exactly as numpy's np.abs(complex128) (the prescale magnitude,
+// prescale.py:66), FP64 out.
+template <typename T>
+__global__ void k_cabs(const T* __restrict__ x, int64_t n, double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const T v = x[i];
+        out[i] = np_cabs((double)v.x, (double)v.y);
+    }
+}
+
+cudaError_t launch_cabs(const void* x, int is_c128, int64_t n, double* out, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    if (is_c128)
+        k_cabs<double2><<<grid_for(n, 256), 256, 0, st>>>(reinterpret_cast<const double2*>(x), n, out);
+    else
+        k_cabs<float2><<<grid_for(n, 256), 256, 0, st>>>(reinterpret_cast<const float2*>(x), n, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_rss(const void* x, int is_c128, int64_t groups, int coils, int64_t npix,
                        double* out, cudaStream_t st) {
     if (groups * npix <= 0) return cudaSuccess;

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(256) k_lines_generic(GenericArgs a) {
         base = line * n;
     }
     const int64_t es = a.col_mode ? n : 1;
-    const int kin = a.kin_sign * (a.kvec ? a.kvec[img / a.k_group] : 0);
+    const int kin = a.kin_sign * (a.kvec ? a.kvec[img / a.k_group] : 0) + a.kin_const;
     const int kout = a.kout_sign * (a.kvec ? a.kvec[img / a.k_group] : 0) + a.kout_const;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         int r = (int)(__brev((unsigned)i) >> (32 - a.log2n));
@@ -71,6 +71,7 @@ cudaError_t run_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
     g.kin_sign = lp.kin_sign;
     g.kout_sign = lp.kout_sign;
     g.kout_const = lp.kout_const;
+    g.kin_const = lp.kin_const;
     const size_t smem = (size_t)p.n * sizeof(float2);
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
     static bool attr_done = false;

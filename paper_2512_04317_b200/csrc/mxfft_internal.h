@@ -36,7 +36,7 @@ struct LinePass {
     int inverse = 0;
     const int32_t* kvec = nullptr;
     int k_group = 1;
-    int kin_sign = 0, kout_sign = 0, kout_const = 0;
+    int kin_sign = 0, kout_sign = 0, kout_const = 0, kin_const = 0;
     int stage_limit = -1;
     int32_t* d_vexp = nullptr;
     float* d_vcodes = nullptr;
@@ -56,7 +56,7 @@ struct MxLinesArgs {
     const signed char* twe;
     int trivial01, inverse;
     const int32_t* kvec;
-    int k_group, kin_sign, kout_sign, kout_const, stage_limit;
+    int k_group, kin_sign, kout_sign, kout_const, kin_const, stage_limit;
     int prof_flags;  // profiling only: bit 0 skip tile loads, bit 1 skip stores
     int tw_chunks;
     // exact replay (replay_lines): reference-literal tables of the plan
@@ -85,7 +85,7 @@ struct GenericArgs {
     int64_t img_elems;
     int lines_per_image;
     const int32_t* kvec;
-    int k_group, kin_sign, kout_sign, kout_const;
+    int k_group, kin_sign, kout_sign, kout_const, kin_const;
 };
 
 extern int g_profile_stage_limit;
@@ -103,6 +103,12 @@ cudaError_t launch_encode_f64(const double* v, int64_t nblocks, int block_len, c
 cudaError_t launch_decode_f64(const double* codes, const double* scales, int64_t nblocks,
                               int block_len, double* out, cudaStream_t st);
 cudaError_t plan_encode(Plan& p, const double* d_tw, cudaStream_t st);
+cudaError_t launch_cabs(const void* x, int is_c128, int64_t n, double* out, cudaStream_t st);
+cudaError_t launch_prescale_sample_keys(const float2* x, int64_t npts, int64_t nsamples, float* keys,
+                                        cudaStream_t st);
+cudaError_t launch_prescale_count_range(const float2* x, int64_t npts, float lo, float hi, float top,
+                                        void* state, float2* cand, int64_t cap, float2* topb,
+                                        int64_t topcap, cudaStream_t st);
 cudaError_t launch_rss(const void* x, int is_c128, int64_t groups, int coils, int64_t npix,
                        double* out, cudaStream_t st);
 cudaError_t launch_selftest_hwq(const FmtDesc& f, unsigned long long* mism, unsigned* first_bad,

@@ -67,6 +67,7 @@ cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
     a.kin_sign = lp.kin_sign;
     a.kout_sign = lp.kout_sign;
     a.kout_const = lp.kout_const;
+    a.kin_const = lp.kin_const;
     a.stage_limit = lp.stage_limit >= 0 ? lp.stage_limit : p.log2n;
     if (lp.stage_limit < 0 && g_profile_stage_limit >= 0 && g_profile_stage_limit < p.log2n)
         a.stage_limit = g_profile_stage_limit;  // profiling knob (mxfft_profile_stage_limit)

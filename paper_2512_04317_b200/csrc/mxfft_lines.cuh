@@ -612,7 +612,7 @@ static __device__ __noinline__ void replay_lines(const MxLinesArgs& a, int64_t g
         }
         const int64_t img = gl / a.lines_per_image;
         const int kk = a.kvec ? a.kvec[img / a.k_group] : 0;
-        const int kin = a.kin_sign * kk, kout = a.kout_sign * kk + a.kout_const;
+        const int kin = a.kin_sign * kk + a.kin_const, kout = a.kout_sign * kk + a.kout_const;
         __syncthreads();
         for (int i = tid; i < n; i += nthr) {
             const int r = (int)(__brev((unsigned)i) >> (32 - a.log2n));
@@ -722,12 +722,12 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
         __syncthreads();  // ... and everybody's
 
         const int64_t line = grp * LPC + (tid >> lt);
-        int kin = 0, kout = a.kout_const;
+        int kin = a.kin_const, kout = a.kout_const;
         if (a.kvec) {
             const bool active = line < a.total_lines;
             const int64_t img = line / a.lines_per_image;
             const int kk = active ? a.kvec[img / a.k_group] : 0;
-            kin = a.kin_sign * kk;
+            kin += a.kin_sign * kk;
             kout += a.kout_sign * kk;
         }
         if (DBG) dbg.row = line;
@@ -837,7 +837,7 @@ __device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
             oes = es;
         }
         const int kk = a.kvec ? a.kvec[img / a.k_group] : 0;
-        const int kin = a.kin_sign * kk;
+        const int kin = a.kin_sign * kk + a.kin_const;
         const int kout = a.kout_sign * kk + a.kout_const;
         if (DBG) dbg.row = line;
         float2 x[32];

@@ -271,7 +271,8 @@ __device__ __forceinline__ unsigned warp_reserve(unsigned cnt, unsigned* counter
 
 __global__ void __launch_bounds__(CNT_THREADS, 4) k_ps_count(const float2* __restrict__ xall, int64_t npts,
                                                           int chunks_per_seg, SegState* st,
-                                                          float2* cand, int64_t cap, float2* top) {
+                                                          float2* cand, int64_t cap, float2* top,
+                                                          int64_t topcap) {
     const int64_t chunk = blockIdx.x;
     const int seg = (int)(chunk / chunks_per_seg);
     const int64_t start = (chunk - (int64_t)seg * chunks_per_seg) * CHUNK;
@@ -316,13 +317,13 @@ __global__ void __launch_bounds__(CNT_THREADS, 4) k_ps_count(const float2* __res
     }
     slot = warp_reserve(__popc(tbits), &st[seg].ntop);
     if (tbits) {
-        float2* tb = top + (int64_t)seg * TOPCAP;
+        float2* tb = top + (int64_t)seg * topcap;
 #pragma unroll
         for (int it = 0; it < CNT_PER_THREAD / 2; ++it)
 #pragma unroll
             for (int h = 0; h < 2; ++h)
                 if ((tbits >> (2 * it + h)) & 1) {
-                    if (slot < TOPCAP) tb[slot] = h ? make_float2(v[it].z, v[it].w) : make_float2(v[it].x, v[it].y);
+                    if (slot < topcap) tb[slot] = h ? make_float2(v[it].z, v[it].w) : make_float2(v[it].x, v[it].y);
                     ++slot;
                 }
     }
@@ -837,10 +838,72 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
     k_ps_sample<<<(unsigned)nseg, SEL_THREADS, 0, st>>>(x, npts, sample_size(npts), q, sst, list_n);
     note_launch();
     const int cps = (int)((npts + CHUNK - 1) / CHUNK);
-    k_ps_count<<<(unsigned)(nseg * cps), CNT_THREADS, 0, st>>>(x, npts, cps, sst, cand, cap, top);
+    k_ps_count<<<(unsigned)(nseg * cps), CNT_THREADS, 0, st>>>(x, npts, cps, sst, cand, cap, top, TOPCAP);
     note_launch();
     k_ps_select<<<(unsigned)nseg, SEL_THREADS, 0, st>>>(sst, list, list_n, cand, cap, top, q, c, out, kvec);
     note_launch();
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Building blocks of the global statistics (one segment split over calls or
+// ranks; combined on the host, prescale.py compute_prescale_global).
+// ---------------------------------------------------------------------------
+// nsamples keys (squared magnitudes, FP32) of pseudo-random whole 32-byte
+// sectors of the segment: zero -> +inf (excluded), |re|,|im| outside
+// [2^-60, 2^60] -> 0 / 2^125 (the count then flags the segment).
+__global__ void k_ps_sample_keys(const float2* __restrict__ x, int64_t npts, int64_t nsamples, float* keys) {
+    const int64_t nsec = npts / 4;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nsamples / 4;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t h = (uint64_t)j * 2654435761ull;
+        const uint64_t sec = (nsec & (nsec - 1)) == 0 ? (h & (uint64_t)(nsec - 1)) : h % (uint64_t)nsec;
+        const float4* p = reinterpret_cast<const float4*>(x + sec * 4);
+        const float4 a = __ldg(p), b = __ldg(p + 1);
+        const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) {
+            const float re = v[2 * hh], im = v[2 * hh + 1];
+            const float m = fmaxf(fabsf(re), fabsf(im));
+            float k = __int_as_float(0x7f800000);
+            if (m > 0.f) k = (m >= 0x1p-60f && m <= 0x1p60f) ? skey(re, im) : (m < 1.f ? 0.f : 0x1p125f);
+            keys[j * 4 + hh] = k;
+        }
+    }
+}
+
+__global__ void k_ps_state_init(SegState* st, float lo, float hi, float top) {
+    SegState g;
+    g.lo = lo;
+    g.hi = hi;
+    g.top = top;
+    g.pad0 = 0;
+    g.nnz = 0;
+    g.below = g.ncand = g.ntop = g.flags = 0;
+    *st = g;
+}
+
+cudaError_t launch_prescale_sample_keys(const float2* x, int64_t npts, int64_t nsamples, float* keys,
+                                        cudaStream_t st) {
+    const int64_t work = nsamples / 4;
+    const unsigned grid = (unsigned)((work + 255) / 256 < 1184 ? (work + 255) / 256 : 1184);
+    if (work <= 0) return cudaSuccess;
+    k_ps_sample_keys<<<grid, 256, 0, st>>>(x, npts, nsamples, keys);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prescale_count_range(const float2* x, int64_t npts, float lo, float hi, float top,
+                                        void* state, float2* cand, int64_t cap, float2* topb,
+                                        int64_t topcap, cudaStream_t st) {
+    SegState* s = reinterpret_cast<SegState*>(state);
+    k_ps_state_init<<<1, 1, 0, st>>>(s, lo, hi, top);
+    note_launch();
+    const int cps = (int)((npts + CHUNK - 1) / CHUNK);
+    if (cps > 0) {
+        k_ps_count<<<(unsigned)cps, CNT_THREADS, 0, st>>>(x, npts, cps, s, cand, cap, topb, topcap);
+        note_launch();
+    }
     return cudaGetLastError();
 }
 
