@@ -47,19 +47,44 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=256)
-    ap.add_argument("--n", type=int, default=256)
-    ap.add_argument("--fmt", default="e4m3")
-    ap.add_argument("--block", type=int, default=32)
-    ap.add_argument("--noise", type=float, default=0.01)
+    ap.add_argument("--config", default="c2", choices=sorted(PRESETS),
+                    help="BASELINE.json configs[0..4] (c2 = configs[1], the headline)")
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--fmt", default=None)
+    ap.add_argument("--block", type=int, default=None)
+    ap.add_argument("--noise", type=float, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    for key, v in PRESETS[a.config].items():
+        if getattr(a, key) is None:
+            setattr(a, key, v)
+    return a
+
+
+# BASELINE.json configs (per rank for c1-c4; c5 is one image split by rows)
+PRESETS = {
+    "c1": dict(batch=1, n=256, fmt="e4m3", block=32, noise=0.01),
+    "c2": dict(batch=256, n=256, fmt="e4m3", block=32, noise=0.01),
+    "c3": dict(batch=64, n=512, fmt="e3m2", block=32, noise=0.01),
+    "c4": dict(batch=4096, n=128, fmt="e4m3", block=32, noise=0.05),
+    "c5": dict(batch=1, n=16384, fmt="e4m3", block=32, noise=0.01),
+}
 
 
 def config_of(a, world):
+    if a.config == "c5":
+        return {
+            "workload": f"C5: one {a.n}^2 complex64 synthetic k-space image, rows split over {world} "
+                        f"GPU(s), {a.fmt.upper()} B={a.block}, global prescale + forward + inverse",
+            "n": a.n, "format": a.fmt, "block_size": a.block, "noise": a.noise,
+            "parallelism": f"row slabs x{world}, all-to-all transposes (NCCL)" if world > 1 else
+                           "1 GPU: transposed-store row passes",
+            "l2": "image (%.1f GB) far exceeds the 126 MB L2" % (a.n * a.n * 8 / 1e9),
+        }
     return {
-        "workload": f"C2: {a.batch} x {a.n}^2 complex64 synthetic k-space per rank, "
+        "workload": f"{a.config.upper()}: {a.batch} x {a.n}^2 complex64 synthetic k-space per rank, "
                     f"{a.fmt.upper()} B={a.block}, prescale + forward + inverse (round trip)",
         "batch_per_rank": a.batch, "n": a.n, "format": a.fmt, "block_size": a.block,
         "noise": a.noise, "parallelism": f"batch-shard x{world} (no collective)",
@@ -154,6 +179,24 @@ def cpu_baseline(x, fmt, block, seconds, threads=None):
 def run_reference(a, rank, world):
     if rank != 0:
         return
+    if a.config == "c5":
+        vals = []
+        t0 = time.perf_counter()
+        per_step = max(1.0, a.cpu_seconds / max(1, a.steps))
+        for _ in range(a.steps):
+            rate, cores, sample = cpu_rows_rate(a.n, a.fmt, a.block, per_step)
+            vals.append(rate / 4 / 1e9)
+        value = float(statistics.mean(vals))
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": value, "unit": "Gpoints/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": (time.perf_counter() - t0) / a.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 carry / fp8-e4m3 codes", "data": "synthetic", "config": config_of(a, world),
+            "cpu_baseline": {"value": value, "unit": "Gpoints/s", "cores": cores, "kind": "port",
+                             "sample": f"per step: {sample}; round trip = 4 row passes"},
+            "e2e": {"value": value, "unit": "Gpoints/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }), flush=True)
+        return
     from paper_2512_04317_b200.workloads import ellipse_kspace_batch
 
     nimg = max(8, os.cpu_count() or 8)
@@ -180,6 +223,136 @@ def run_reference(a, rank, world):
     }), flush=True)
 
 
+def cpu_rows_rate(n, fmt, block, seconds, threads=None):
+    """The oracle's row pass on seeded n-point rows, all host threads, for
+    `seconds`; returns row-points per second (one pass)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    from concurrent.futures import ThreadPoolExecutor
+
+    threads = threads or os.cpu_count() or 1
+    rng = np.random.default_rng(0)
+    rows = (rng.standard_normal((threads, 4, n)) + 1j * rng.standard_normal((threads, 4, n))).astype(np.complex64)
+    plan = O.make_plan(n, O.ALL_MX[fmt], block)
+    done, t0 = 0, time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        while True:
+            list(ex.map(lambda i: O.fft_batch(rows[i], plan, False), range(threads)))
+            done += threads * 4
+            if time.perf_counter() - t0 >= seconds:
+                break
+    dt = time.perf_counter() - t0
+    return done * n / dt, threads, f"{done} oracle row transforms of {n} points ({dt:.1f} s)"
+
+
+def run_c5(a, rank, world, local):
+    """C5: one n^2 image.  1 GPU: global prescale + fft2 with transposed-store
+    passes.  N GPUs: row slabs, global prescale over all ranks, all-to-all
+    transposes (paper_2512_04317_b200/distributed.py)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_04317_b200 as mx
+    from paper_2512_04317_b200 import _native, distributed as D
+    from paper_2512_04317_b200.workloads import ellipse_kspace_device
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = D.Comm()
+    n = a.n
+    r0, r1 = D.shard_range(n, rank, world)
+    x = ellipse_kspace_device(n, 7, noise=a.noise, rows=(r0, r1))
+    plan = mx.make_plan(n, mx.ModeSpec.mx(mx.get_mx_format(a.fmt), a.block))
+    cfg = mx.PrescaleConfig()
+    ws = torch.empty(int(_native.lib().mxfft_fft2_workspace_bytes(plan.handle, 1)) if world == 1 else 1,
+                     dtype=torch.uint8, device="cuda")
+    y = torch.empty_like(x)
+    kt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step(roundtrip=True, xin=None):
+        xin = x if xin is None else xin
+        res = D.compute_prescale_global(xin, cfg, comm)
+        if world == 1:
+            kt.fill_(res.k)
+            return mx.fft2_device(xin[None], plan, "roundtrip" if roundtrip else "forward", k=kt,
+                                  out=y[None], workspace=ws)
+        return D.fft2_slab(xin, plan, "roundtrip" if roundtrip else "forward", comm, k=res.k)
+
+    def timed(fn, steps, warmup):
+        for _ in range(warmup):
+            fn()
+        comm.sum_(torch.zeros(1, device="cuda"))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device="cuda")
+        return float(comm.max_(ms).item())
+
+    pts = n * n
+    for _ in range(a.warmup):
+        step()
+    launches0 = _native.launch_count()
+    with ClockSampler(local) as clk:
+        ms = timed(step, a.steps, 0)
+    launches = (_native.launch_count() - launches0) // max(1, a.steps)
+    ms_fwd = timed(lambda: step(False), max(2, a.steps // 2), 1)
+    # line pass (the dominant kernel): a plain forward fft2 on one GPU = 2 passes
+    ms_pass = None
+    if world == 1:
+        ms_pass = timed(lambda: mx.fft2_device(x[None], plan, "forward", out=y[None], workspace=ws),
+                        max(2, a.steps // 2), 1) / 2
+    # e2e: pinned host slab in, result out, every step
+    h_in = x.cpu().pin_memory()
+    h_out = torch.empty(h_in.shape, dtype=h_in.dtype).pin_memory()
+    xd = torch.empty_like(x)
+
+    def e2e_step():
+        xd.copy_(h_in, non_blocking=True)
+        out = step(True, xd)
+        h_out.copy_(out.reshape(h_out.shape), non_blocking=True)
+
+    ms_e2e = timed(e2e_step, 2, 1)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        rate, cores, sample = cpu_rows_rate(n, a.fmt, a.block, a.cpu_seconds)
+        # a round trip is four row passes over the n^2 points
+        cpu = {"value": rate / 4 / 1e9, "unit": "Gpoints/s", "cores": cores, "kind": "port",
+               "sample": sample + "; round trip = 4 row passes of the image"}
+    if rank == 0:
+        peak, peak_src = measured_peak_hbm()
+        value = pts / (ms * 1e-3) / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gpoints/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 carry / fp8-e4m3 codes", "data": "synthetic",
+            "config": config_of(a, world),
+            "forward": {"value": pts / (ms_fwd * 1e-3) / 1e9, "unit": "Gpoints/s", "ms_per_step": ms_fwd},
+            "roofline": None if ms_pass is None else {
+                "bound": "hbm", "kernel": "mx_line_pass (n=16384, k_mx_lines_big)",
+                "achieved": BYTES_PER_POINT * pts / (ms_pass * 1e-3) / 1e9, "peak": peak,
+                "peak_source": peak_src, "unit": "GB/s",
+                "frac": BYTES_PER_POINT * pts / (ms_pass * 1e-3) / 1e9 / peak, "traffic": None,
+                "kernel_ms": {"mx_line_pass": ms_pass}},
+            "e2e": {"value": pts / (ms_e2e * 1e-3) / 1e9, "unit": "Gpoints/s",
+                    "h2d_bytes_per_step": (r1 - r0) * n * 8 * world, "d2h_bytes_per_step": (r1 - r0) * n * 8 * world,
+                    "ms_per_step": ms_e2e},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "parity": "tests/test_gpu_parity.py::test_c5_full_size_16384 (exact global prescale; rows and "
+                      "columns equal to the oracle)",
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     a = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -187,6 +360,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if a.impl == "reference":
         run_reference(a, rank, world)
+        return
+    if a.config == "c5":
+        run_c5(a, rank, world, local)
         return
 
     import torch

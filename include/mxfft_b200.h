@@ -142,6 +142,11 @@ int32_t mxfft_fft2(mxfft_plan plan, const void* x, void* y, int64_t batch, int32
                    uintptr_t stream);
 int64_t mxfft_fft2_workspace_bytes(mxfft_plan plan, int64_t batch);
 
+/* Batched out-of-place transpose of `batch` n x n complex64 images,
+ * y[b][j][i] = x[b][i][j] (the rows.T between the passes of fft_2d,
+ * fftcore.py:352); n a multiple of 64. */
+int32_t mxfft_transpose_c64(const void* x, void* y, int64_t batch, int32_t n, uintptr_t stream);
+
 /* compute_prescale (prescale.py:61-73) over `nseg` segments of `seg_points`
  * complex values each (complex64 when is_c128 == 0, else complex128),
  * contiguous.  Writes one mxfft_prescale_result per segment to d_out and, when

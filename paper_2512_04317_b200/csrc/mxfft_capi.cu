@@ -270,9 +270,16 @@ int32_t mxfft_fft2(mxfft_plan plan, const void* x, void* y, int64_t batch, int32
     const bool tpose = workspace && need > 0;
     if (workspace && need > 0 && workspace_bytes < need)
         return fail(MXFFT_ERR_VALUE, "fft2 workspace too small");
+    // n >= 8192 (one line per CTA): a transposed store would scatter 8-byte
+    // elements over n rows, so those passes store plain rows and a tiled
+    // transpose kernel follows: x -> y -T-> ws -> ws -T-> y [-> y -T-> ws -> ws -T-> y]
+    const bool split_t = tpose && p.n > 4096;
     for (int pass = 0; pass < npass; ++pass) {
         LinePass lp;
-        if (tpose) {
+        if (split_t) {
+            lp.in = pass == 0 ? x : ((pass & 1) ? workspace : y);
+            lp.out = (pass & 1) ? workspace : y;
+        } else if (tpose) {
             lp.in = pass == 0 ? x : ((pass & 1) ? workspace : y);
             lp.out = (pass & 1) ? y : workspace;
             lp.tstore = 1;
@@ -294,7 +301,17 @@ int32_t mxfft_fft2(mxfft_plan plan, const void* x, void* y, int64_t batch, int32
             if (mode == 2) lp.kout_const = -2 * p.log2n;  // x 1/n^2 (mri.py:100)
         }
         CK(run_lines(p, lp, s), "fft2");
+        if (split_t)
+            CK(launch_transpose_c64(lp.out, (pass & 1) ? y : workspace, batch, p.n, s), "fft2 transpose");
     }
+    return MXFFT_OK;
+}
+
+int32_t mxfft_transpose_c64(const void* x, void* y, int64_t batch, int32_t n, uintptr_t stream) {
+    if (batch < 0 || n <= 0) return fail(MXFFT_ERR_SHAPE, "bad transpose shape");
+    if (n % 64) return fail(MXFFT_ERR_UNSUPPORTED_SIZE, "transpose needs n to be a multiple of 64");
+    if (x == y) return fail(MXFFT_ERR_VALUE, "transpose is out of place");
+    CK(launch_transpose_c64(x, y, batch, n, (cudaStream_t)stream), "transpose");
     return MXFFT_OK;
 }
 

@@ -508,3 +508,15 @@ def test_c5_full_size_16384(mx, torch):
     for j in (0, 4097, 16383):
         col = r[:, j].contiguous().cpu().numpy()[None]
         assert_same(y[:, j].cpu().numpy(), O.fft_batch(col, op, False)[0], f"column {j}")
+
+
+def test_transpose_kernel(mx, torch):
+    from paper_2512_04317_b200 import _native
+
+    for b, n in ((3, 64), (2, 256), (1, 1024)):
+        x = torch.randn(b, n, n, dtype=torch.complex64, device="cuda")
+        y = torch.empty_like(x)
+        _native.check(_native.lib().mxfft_transpose_c64(x.data_ptr(), y.data_ptr(), b, n, 0))
+        assert torch.equal(torch.view_as_real(y), torch.view_as_real(x.transpose(1, 2).contiguous()))
+    with pytest.raises(mx.UnsupportedSize):
+        _native.check(_native.lib().mxfft_transpose_c64(x.data_ptr(), y.data_ptr(), 1, 96, 0))
