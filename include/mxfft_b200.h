@@ -142,6 +142,20 @@ int32_t mxfft_fft2(mxfft_plan plan, const void* x, void* y, int64_t batch, int32
                    uintptr_t stream);
 int64_t mxfft_fft2_workspace_bytes(mxfft_plan plan, int64_t batch);
 
+/* The non-MX modes of ModeSpec (fftcore.py:32-64), batched rows of length n
+ * (power of two <= 16384).  d_tw: n device entries, entry 2^s + j = twiddle j
+ * of stage s (j < 2^s) of the plan's FP64 table (fftcore.py:101-105):
+ *  - fp16 (_fft_batch_fp16, fftcore.py:285-311): entries are half2 (re, im)
+ *    rounded from FP64 by the plan builder; x complex64 or complex128
+ *    (x_is_c128); y complex64 holding FP16 values.  *d_nonfinite is set when
+ *    an intermediate overflowed (the reference's quantize_array raises).
+ *  - reference (_fft_batch_reference, fftcore.py:243-256): entries complex128;
+ *    x, y complex128, out of place. */
+int32_t mxfft_fft_rows_fp16(const void* x, int32_t x_is_c128, void* y, int64_t batch, int32_t n,
+                            const void* d_tw, int32_t inverse, int32_t* d_nonfinite, uintptr_t stream);
+int32_t mxfft_fft_rows_f64(const void* x, void* y, int64_t batch, int32_t n, const void* d_tw, int32_t inverse,
+                           uintptr_t stream);
+
 /* Batched out-of-place transpose of `batch` n x n complex64 images,
  * y[b][j][i] = x[b][i][j] (the rows.T between the passes of fft_2d,
  * fftcore.py:352); n a multiple of 64. */

@@ -307,6 +307,25 @@ int32_t mxfft_fft2(mxfft_plan plan, const void* x, void* y, int64_t batch, int32
     return MXFFT_OK;
 }
 
+static bool pow2_len(int32_t n) { return n >= 2 && n <= 16384 && !(n & (n - 1)); }
+
+int32_t mxfft_fft_rows_fp16(const void* x, int32_t x_is_c128, void* y, int64_t batch, int32_t n,
+                            const void* d_tw, int32_t inverse, int32_t* d_nonfinite, uintptr_t stream) {
+    if (batch < 0) return fail(MXFFT_ERR_SHAPE, "negative batch");
+    if (!pow2_len(n)) return fail(MXFFT_ERR_UNSUPPORTED_SIZE, "fp16 rows: n must be a power of two in [2, 16384]");
+    CK(launch_fp16_rows(x, x_is_c128, y, batch, n, d_tw, inverse, d_nonfinite, (cudaStream_t)stream), "fft_rows_fp16");
+    return MXFFT_OK;
+}
+
+int32_t mxfft_fft_rows_f64(const void* x, void* y, int64_t batch, int32_t n, const void* d_tw, int32_t inverse,
+                           uintptr_t stream) {
+    if (batch < 0) return fail(MXFFT_ERR_SHAPE, "negative batch");
+    if (!pow2_len(n)) return fail(MXFFT_ERR_UNSUPPORTED_SIZE, "f64 rows: n must be a power of two in [2, 16384]");
+    if (x == y) return fail(MXFFT_ERR_VALUE, "f64 rows are out of place (bit-reversed gather)");
+    CK(launch_f64_rows(x, y, batch, n, d_tw, inverse, (cudaStream_t)stream), "fft_rows_f64");
+    return MXFFT_OK;
+}
+
 int32_t mxfft_transpose_c64(const void* x, void* y, int64_t batch, int32_t n, uintptr_t stream) {
     if (batch < 0 || n <= 0) return fail(MXFFT_ERR_SHAPE, "bad transpose shape");
     if (n % 64) return fail(MXFFT_ERR_UNSUPPORTED_SIZE, "transpose needs n to be a multiple of 64");

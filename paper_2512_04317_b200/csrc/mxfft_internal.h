@@ -105,6 +105,10 @@ cudaError_t launch_decode_f64(const double* codes, const double* scales, int64_t
 cudaError_t plan_encode(Plan& p, const double* d_tw, cudaStream_t st);
 cudaError_t launch_cabs(const void* x, int is_c128, int64_t n, double* out, cudaStream_t st);
 cudaError_t launch_transpose_c64(const void* x, void* y, int64_t batch, int n, cudaStream_t st);
+cudaError_t launch_fp16_rows(const void* x, int x_is_c128, void* y, int64_t batch, int n, const void* tw,
+                             int inverse, int* nonfinite, cudaStream_t st);
+cudaError_t launch_f64_rows(const void* x, void* y, int64_t batch, int n, const void* tw, int inverse,
+                            cudaStream_t st);
 cudaError_t launch_prescale_sample_keys(const float2* x, int64_t npts, int64_t nsamples, float* keys,
                                         cudaStream_t st);
 cudaError_t launch_prescale_count_range(const float2* x, int64_t npts, float lo, float hi, float top,

@@ -20,7 +20,7 @@ import dataclasses
 import numpy as np
 
 from . import _native, mxblock
-from .errors import ShapeError, UnsupportedSize
+from .errors import InvalidValue, ShapeError, UnsupportedSize
 from .minifloat import MinifloatFormat, get_format, quantize_device
 
 MODE_CODES = {"forward": 0, "inverse": 1, "roundtrip": 2}
@@ -112,6 +112,32 @@ class FftPlan:
         elif mode.kind == "fp16":
             self.fp16_twiddles = [(w.real.astype(np.float16), w.imag.astype(np.float16))
                                   for w in self.ref_twiddles]
+
+    def device_twiddles(self):
+        """fp16 / reference plans: the n-entry device table (entry 2^s + j =
+        twiddle j of stage s) the non-MX kernels read; built once from the
+        plan's FP64 table (fp16: rounded by numpy exactly as the reference's
+        plan, fftcore.py:115-117)."""
+        import torch
+
+        if getattr(self, "_dev_tw", None) is None:
+            n = self.n
+            if self.mode.kind == "fp16":
+                t = np.zeros((n, 2), dtype=np.float16)
+                for s, (wr, wi) in enumerate(self.fp16_twiddles):
+                    half = 1 << s
+                    t[half:2 * half, 0] = wr[:half]
+                    t[half:2 * half, 1] = wi[:half]
+                self._dev_tw = torch.from_numpy(t.view(np.uint8).reshape(-1).copy()).cuda()
+            elif self.mode.kind == "reference":
+                t = np.zeros(n, dtype=np.complex128)
+                for s, w in enumerate(self.ref_twiddles):
+                    half = 1 << s
+                    t[half:2 * half] = w[:half]
+                self._dev_tw = torch.from_numpy(t).cuda()
+            else:
+                raise ValueError("MX plans keep their tables behind the plan handle")
+        return self._dev_tw
 
     @property
     def handle(self):
@@ -298,8 +324,41 @@ def _fft_batch(x: np.ndarray, plan: FftPlan, direction: str) -> np.ndarray:
     x = np.asarray(x)
     if x.shape[1] != plan.n:
         raise ShapeError(f"expected length {plan.n}, got {x.shape[1]}")
-    _require_mx(plan)
-    y = fft_rows_device(_to_c64_device(x), plan, direction == "inverse")
+    inverse = direction == "inverse"
+    if plan.mode.kind == "fp16":
+        return _fft_rows_fp16(x, plan, inverse)
+    if plan.mode.kind == "reference":
+        return _fft_rows_f64(x, plan, inverse)
+    y = fft_rows_device(_to_c64_device(x), plan, inverse)
+    return y.cpu().numpy()
+
+
+def _fft_rows_fp16(x: np.ndarray, plan: FftPlan, inverse: bool) -> np.ndarray:
+    """_fft_batch_fp16 (fftcore.py:285-311) on the GPU: complex64 input is
+    quantized from FP32, anything else from FP64, as the reference does."""
+    import torch
+
+    c64 = x.dtype == np.complex64
+    xd = torch.from_numpy(np.ascontiguousarray(x, dtype=np.complex64 if c64 else np.complex128)).cuda()
+    y = torch.empty(xd.shape, dtype=torch.complex64, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _native.check(_native.lib().mxfft_fft_rows_fp16(xd.data_ptr(), int(not c64), y.data_ptr(), xd.shape[0],
+                                                    plan.n, plan.device_twiddles().data_ptr(), int(inverse),
+                                                    flag.data_ptr(), _native.stream_handle()))
+    if int(flag.item()):
+        raise InvalidValue("non-finite value in the FP16 transform (quantize_array)")
+    return y.cpu().numpy()
+
+
+def _fft_rows_f64(x: np.ndarray, plan: FftPlan, inverse: bool) -> np.ndarray:
+    """_fft_batch_reference (fftcore.py:243-256) on the GPU, complex128."""
+    import torch
+
+    xd = torch.from_numpy(np.ascontiguousarray(x, dtype=np.complex128)).cuda()
+    y = torch.empty_like(xd)
+    _native.check(_native.lib().mxfft_fft_rows_f64(xd.data_ptr(), y.data_ptr(), xd.shape[0], plan.n,
+                                                   plan.device_twiddles().data_ptr(), int(inverse),
+                                                   _native.stream_handle()))
     return y.cpu().numpy()
 
 
@@ -326,6 +385,10 @@ def fft_2d(x, plan: FftPlan, direction: str = "forward") -> np.ndarray:
         raise UnsupportedSize(f"grid size {x.shape[0]} does not match plan size {plan.n}")
     if direction not in ("forward", "inverse"):
         raise ValueError(f"direction must be 'forward' or 'inverse', got {direction!r}")
+    if plan.mode.kind != "mx":  # fp16 / reference: rows, rows.T, cols.T as fftcore.py:351-353
+        rows = _fft_batch(x, plan, direction)
+        cols = _fft_batch(np.ascontiguousarray(rows.T), plan, direction)
+        return np.asarray(cols.T, dtype=np.complex128)
     y = fft2_device(_to_c64_device(x[None]), plan, direction)
     return y[0].cpu().numpy().astype(np.complex128)
 

@@ -167,6 +167,29 @@ def fft2_fixture(rng):
     return out
 
 
+def modes_fixture(rng):
+    """The non-MX ModeSpec kinds: FP16 positive control and FP64 reference,
+    1-D batches (complex128 and complex64 inputs) and 2-D transforms."""
+    out = {}
+    cases = [("fp16", 8), ("fp16", 64), ("fp16", 256), ("reference", 8), ("reference", 64), ("reference", 1024)]
+    for ci, (kind, n) in enumerate(cases):
+        plan = R.make_plan(n, R.ModeSpec.from_name(kind))
+        x = (rng.standard_normal((3, n)) + 1j * rng.standard_normal((3, n))) * 10.0 ** rng.uniform(-2, 2, (3, 1))
+        x32 = x.astype(np.complex64)
+        out[f"c{ci}_x"] = x
+        out[f"c{ci}_x32"] = x32
+        for d in ("forward", "inverse"):
+            out[f"c{ci}_{d}"] = R.fftcore._fft_batch(x, plan, d)
+            out[f"c{ci}_{d}32"] = R.fftcore._fft_batch(x32, plan, d)
+        if n <= 256:
+            img = ellipse_kspace(n, seed=300 + ci, noise=0.01).astype(np.complex128) * 2.0 ** -12
+            out[f"c{ci}_img"] = img
+            out[f"c{ci}_fft2"] = R.fft_2d(img, plan, "forward")
+            out[f"c{ci}_ifft2"] = R.fft_2d(img, plan, "inverse")
+    out["cases"] = np.array([f"{a}:{b}" for a, b in cases])
+    return out
+
+
 def prescale_fixture(rng):
     cfg = R.PrescaleConfig()
     inputs = []
@@ -238,7 +261,7 @@ def main():
     for name, fn in [("quantize", quantize_fixture), ("batch", batch_fixture),
                      ("stages", stage_fixture), ("fft2", fft2_fixture),
                      ("prescale", prescale_fixture), ("pipelines", pipeline_fixture),
-                     ("twiddles", twiddle_fixture)]:
+                     ("twiddles", twiddle_fixture), ("modes", modes_fixture)]:
         data = fn(rng)
         path = os.path.join(OUT, f"{name}.npz")
         np.savez_compressed(path, **data)

@@ -520,3 +520,31 @@ def test_transpose_kernel(mx, torch):
         assert torch.equal(torch.view_as_real(y), torch.view_as_real(x.transpose(1, 2).contiguous()))
     with pytest.raises(mx.UnsupportedSize):
         _native.check(_native.lib().mxfft_transpose_c64(x.data_ptr(), y.data_ptr(), 1, 96, 0))
+
+
+# ---------------------------------------------------------------------------
+# non-MX modes: FP16 positive control and FP64 reference
+# ---------------------------------------------------------------------------
+def test_modes_golden(mx):
+    """_fft_batch / fft_2d in fp16 and reference mode == the reference's own
+    outputs (tests/golden/modes.npz), for complex128 and complex64 inputs."""
+    g = golden("modes")
+    for ci, case in enumerate(g["cases"]):
+        kind, n = str(case).split(":")
+        p = mx.make_plan(int(n), mx.ModeSpec.from_name(kind))
+        for d in ("forward", "inverse"):
+            assert_same(mx.fftcore._fft_batch(g[f"c{ci}_x"], p, d), g[f"c{ci}_{d}"], f"{case} {d}")
+            assert_same(mx.fftcore._fft_batch(g[f"c{ci}_x32"], p, d), g[f"c{ci}_{d}32"], f"{case} {d} c64")
+        if f"c{ci}_img" in g.files:
+            assert_same(mx.fft_2d(g[f"c{ci}_img"], p, "forward"), g[f"c{ci}_fft2"], f"{case} fft2")
+            assert_same(mx.fft_2d(g[f"c{ci}_img"], p, "inverse"), g[f"c{ci}_ifft2"], f"{case} ifft2")
+
+
+def test_fp16_overflow_raises_and_fft_1d_fp16(mx):
+    p = mx.make_plan(16, mx.ModeSpec.fp16())
+    with pytest.raises(mx.InvalidValue):
+        mx.fft_1d_fp16(np.full(16, 60000.0 + 0j), p)
+    with pytest.raises(ValueError):
+        mx.fft_1d_fp16(np.ones(16), mx.make_plan(16, mx.ModeSpec.reference()))
+    y = mx.fft_1d_fp16(np.eye(16)[0] * (1 + 0j), p)
+    assert np.array_equal(y, np.ones(16))
