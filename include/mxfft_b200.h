@@ -156,6 +156,15 @@ int32_t mxfft_fft_rows_fp16(const void* x, int32_t x_is_c128, void* y, int64_t b
 int32_t mxfft_fft_rows_f64(const void* x, void* y, int64_t batch, int32_t n, const void* d_tw, int32_t inverse,
                            uintptr_t stream);
 
+/* Image-quality metrics of an h x w FP64 test image against a reference
+ * (metrics.py:38-93), device pointers.  d_out (5 doubles): sum (ref-test)^2,
+ * sum ref^2, max ref, min ref, and -- when do_ssim -- the sum over the
+ * (h-10) x (w-10) valid positions of the local SSIM with the 11 x 11 window
+ * d_window (row-major) and constants c1, c2.  FP64; the summation order is
+ * not numpy's (agreement ~1e-15 relative). */
+int32_t mxfft_metrics(const double* ref, const double* test, int64_t h, int64_t w, int32_t do_ssim,
+                      const double* d_window, double c1, double c2, double* d_out, uintptr_t stream);
+
 /* Batched out-of-place transpose of `batch` n x n complex64 images,
  * y[b][j][i] = x[b][i][j] (the rows.T between the passes of fft_2d,
  * fftcore.py:352); n a multiple of 64. */

@@ -326,6 +326,14 @@ int32_t mxfft_fft_rows_f64(const void* x, void* y, int64_t batch, int32_t n, con
     return MXFFT_OK;
 }
 
+int32_t mxfft_metrics(const double* ref, const double* test, int64_t h, int64_t w, int32_t do_ssim,
+                      const double* d_window, double c1, double c2, double* d_out, uintptr_t stream) {
+    if (h < 0 || w < 0) return fail(MXFFT_ERR_SHAPE, "negative image size");
+    if (do_ssim && (h < 11 || w < 11)) return fail(MXFFT_ERR_SHAPE, "image smaller than the 11x11 SSIM window");
+    CK(launch_metrics(ref, test, h, w, do_ssim, d_window, c1, c2, d_out, (cudaStream_t)stream), "metrics");
+    return MXFFT_OK;
+}
+
 int32_t mxfft_transpose_c64(const void* x, void* y, int64_t batch, int32_t n, uintptr_t stream) {
     if (batch < 0 || n <= 0) return fail(MXFFT_ERR_SHAPE, "bad transpose shape");
     if (n % 64) return fail(MXFFT_ERR_UNSUPPORTED_SIZE, "transpose needs n to be a multiple of 64");

@@ -190,6 +190,20 @@ def modes_fixture(rng):
     return out
 
 
+def metrics_fixture(rng):
+    """Reference PSNR / NMSE / SSIM (metrics.py) on seeded magnitude-image pairs."""
+    out = {}
+    cases = [(64, 0.01), (128, 0.1), (33, 0.5), (256, 1e-4)]
+    for ci, (n, eps) in enumerate(cases):
+        ref = np.abs(ellipse_kspace(n, seed=400 + ci, noise=0.0)).astype(np.float64) ** 0.5
+        test = ref + eps * ref.max() * rng.standard_normal(ref.shape)
+        out[f"c{ci}_ref"] = ref
+        out[f"c{ci}_test"] = test
+        out[f"c{ci}_vals"] = np.array([R.psnr(ref, test), R.nmse(ref, test), R.ssim(ref, test)])
+    out["cases"] = np.array([f"{a}:{b}" for a, b in cases])
+    return out
+
+
 def prescale_fixture(rng):
     cfg = R.PrescaleConfig()
     inputs = []
@@ -261,7 +275,8 @@ def main():
     for name, fn in [("quantize", quantize_fixture), ("batch", batch_fixture),
                      ("stages", stage_fixture), ("fft2", fft2_fixture),
                      ("prescale", prescale_fixture), ("pipelines", pipeline_fixture),
-                     ("twiddles", twiddle_fixture), ("modes", modes_fixture)]:
+                     ("twiddles", twiddle_fixture), ("modes", modes_fixture),
+                     ("metrics", metrics_fixture)]:
         data = fn(rng)
         path = os.path.join(OUT, f"{name}.npz")
         np.savez_compressed(path, **data)

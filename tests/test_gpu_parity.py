@@ -548,3 +548,25 @@ def test_fp16_overflow_raises_and_fft_1d_fp16(mx):
         mx.fft_1d_fp16(np.ones(16), mx.make_plan(16, mx.ModeSpec.reference()))
     y = mx.fft_1d_fp16(np.eye(16)[0] * (1 + 0j), p)
     assert np.array_equal(y, np.ones(16))
+
+
+def test_metrics_match_reference(mx):
+    """psnr / nmse / ssim on the GPU vs the reference's numpy/scipy values
+    (tests/golden/metrics.npz); FP64 sums in a different order: 1e-12 rel."""
+    g = golden("metrics")
+    for ci, case in enumerate(g["cases"]):
+        ref, test = g[f"c{ci}_ref"], g[f"c{ci}_test"]
+        p, e, s = g[f"c{ci}_vals"]
+        assert abs(mx.psnr(ref, test) - p) <= 1e-12 * abs(p), case
+        assert abs(mx.nmse(ref, test) - e) <= 1e-12 * abs(e), case
+        assert abs(mx.ssim(ref, test) - s) <= 1e-12, case
+        rep = mx.report(ref, test)
+        assert isinstance(rep, mx.MetricsReport) and abs(rep.ssim - s) <= 1e-12
+    r = g["c0_ref"]
+    assert mx.psnr(r, r) == float("inf") and mx.nmse(r, r) == 0.0 and abs(mx.ssim(r, r) - 1.0) < 1e-15
+    with pytest.raises(mx.ShapeError):
+        mx.psnr(r, r[:-1])
+    with pytest.raises(mx.DegenerateReference):
+        mx.psnr(np.zeros((16, 16)), np.ones((16, 16)))
+    with pytest.raises(mx.WindowTooLarge):
+        mx.ssim(np.ones((8, 8)), np.ones((8, 8)))
