@@ -24,6 +24,8 @@
 #include <cfloat>
 #include <cstdio>
 
+#include <cooperative_groups.h>
+
 #include "../../include/mxfft_b200.h"
 #include "mxfft_common.cuh"
 #include "mxfft_internal.h"
@@ -521,14 +523,14 @@ __device__ void finish_result(const mxfft_prescale_cfg& c, double a_max, double 
 // ---------------------------------------------------------------------------
 // fused sample -> count -> select, one CTA per segment (segments <= 2^18 points)
 // ---------------------------------------------------------------------------
-template <int NT, int CCAP>
+template <int NT, int CCAP, int SMAX, int WC, int TC>
 struct FusedShared {
     union {
-        unsigned keys[SAMPLE_MAX];  // sample phase
-        double w[WCAP];             // exact-sort window (select phase)
+        unsigned keys[SMAX];  // sample phase
+        double w[WC];         // exact-sort window (select phase)
     } u;
     float2 cand[CCAP];
-    float2 topb[F_TOPCAP];
+    float2 topb[TC];
     unsigned hist[NBIN];
     unsigned warp_sums[NT / 32];
     unsigned long long amax_b;
@@ -538,15 +540,21 @@ struct FusedShared {
     unsigned woff, wend;
 };
 
-template <int NT, int CCAP>
+// CL = 2 (not dispatched): a 2-CTA cluster per segment -- both CTAs draw the
+// same sample (so the same bracket), each streams half of the segment, and
+// CTA 0 merges CTA 1's counts and candidates through distributed shared
+// memory and selects.  Measured slower on C2 (78 vs 57 us, 256-thread CTAs).
+template <int NT, int CCAP, int CL, int SMAX, int WC, int TC>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_ps_fused(const float2* __restrict__ xall, int64_t npts, int S,
                                                            double q, mxfft_prescale_cfg c,
                                                            mxfft_prescale_result* out, int32_t* kvec, int* list,
                                                            int* list_n) {
-    constexpr int F_THREADS = NT, F_CCAP = CCAP;
+    constexpr int F_THREADS = NT, F_CCAP = CCAP, F_TOPCAP = TC, SAMPLE_MAX = SMAX, WCAP = WC;
+    using Shared = FusedShared<NT, CCAP, SMAX, WC, TC>;
     extern __shared__ unsigned long long fused_smem[];
-    FusedShared<NT, CCAP>& F = *reinterpret_cast<FusedShared<NT, CCAP>*>(fused_smem);
-    const int seg = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+    Shared& F = *reinterpret_cast<Shared*>(fused_smem);
+    const int seg = blockIdx.x / CL, crank = CL > 1 ? (int)(blockIdx.x % CL) : 0;
+    const int tid = threadIdx.x, lane = tid & 31;
 #ifdef PS_TIMING
     long long T0 = clock64(), TS[8];
 #define PS_T(i) if (tid == 0) TS[i] = clock64() - T0;
@@ -614,8 +622,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_ps_fused(const float2* __rest
     {
         unsigned nnz = 0, below = 0;
         float ksum = 0.f;
-        const int64_t npairs = npts / 2;
-        const float4* x4 = reinterpret_cast<const float4*>(x);
+        const int64_t part = (npts / 2 + CL - 1) / CL;  // this CTA's pairs of the segment
+        const int64_t p_begin = crank * part;
+        const int64_t npairs = (npts / 2 - p_begin) < part ? (npts / 2 - p_begin) : part;
+        const float4* x4 = reinterpret_cast<const float4*>(x) + p_begin;
         constexpr int64_t STEP = (int64_t)F_THREADS * F_UNR;
         float4 vn[F_UNR];  // next round's loads are in flight while this one is classified
 #pragma unroll
@@ -683,6 +693,29 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_ps_fused(const float2* __rest
             if (flags) atomicOr(&F.flags, flags);
         }
         __syncthreads();
+    }
+    if constexpr (CL > 1) {  // merge the other CTA's half into CTA 0
+        namespace cg = cooperative_groups;
+        cg::cluster_group cluster = cg::this_cluster();
+        cluster.sync();
+        if (crank == 0) {
+            const Shared& R = *cluster.map_shared_rank(&F, 1);
+            const unsigned nc0 = F.ncand, nc1 = R.ncand, nt0 = F.ntop, nt1 = R.ntop;
+            for (unsigned i = tid; i < nc1; i += F_THREADS)
+                if (nc0 + i < F_CCAP && i < F_CCAP) F.cand[nc0 + i] = R.cand[i];
+            for (unsigned i = tid; i < nt1; i += F_THREADS)
+                if (nt0 + i < F_TOPCAP && i < F_TOPCAP) F.topb[nt0 + i] = R.topb[i];
+            __syncthreads();
+            if (tid == 0) {
+                F.ncand = nc0 + nc1;
+                F.ntop = nt0 + nt1;
+                F.nnz += R.nnz;
+                F.below += R.below;
+                F.flags |= R.flags;
+            }
+        }
+        cluster.sync();  // CTA 1's shared memory stays alive until CTA 0 has read it
+        if (crank != 0) return;
     }
 
     // ---- select: histogram of the candidates, exact sort of a small window ----
@@ -813,22 +846,26 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
     if (npts <= FUSED_MAX) {
         static bool attr = false;
         if (!attr) {
-            cudaError_t e = cudaFuncSetAttribute(k_ps_fused<256, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)sizeof(FusedShared<256, 4096>));
+            cudaError_t e = cudaFuncSetAttribute(k_ps_fused<256, 4096, 1, 4096, 2048, 1024>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)sizeof(FusedShared<256, 4096, 4096, 2048, 1024>));
             if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(k_ps_fused<512, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(FusedShared<512, 4096>));
+                e = cudaFuncSetAttribute(k_ps_fused<512, 4096, 1, 4096, 2048, 1024>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(FusedShared<512, 4096, 4096, 2048, 1024>));
             if (e != cudaSuccess) return e;
             attr = true;
         }
         cudaError_t e = cudaMemsetAsync(list_n, 0, sizeof(int), st);
         if (e != cudaSuccess) return e;
-        if (npts <= 32768)
-            k_ps_fused<256, 4096><<<(unsigned)nseg, 256, sizeof(FusedShared<256, 4096>), st>>>(
-                x, npts, fused_sample_size(npts), q, c, out, kvec, list, list_n);
-        else
-            k_ps_fused<512, 4096><<<(unsigned)nseg, 512, sizeof(FusedShared<512, 4096>), st>>>(
-                x, npts, fused_sample_size(npts), q, c, out, kvec, list, list_n);
+        const int S = fused_sample_size(npts);
+        if (npts <= 32768) {
+            k_ps_fused<256, 4096, 1, 4096, 2048, 1024><<<(unsigned)nseg, 256, sizeof(FusedShared<256, 4096, 4096, 2048, 1024>), st>>>(
+                x, npts, S, q, c, out, kvec, list, list_n);
+        } else {
+            k_ps_fused<512, 4096, 1, 4096, 2048, 1024><<<(unsigned)nseg, 512, sizeof(FusedShared<512, 4096, 4096, 2048, 1024>), st>>>(
+                x, npts, S, q, c, out, kvec, list, list_n);
+        }
         note_launch();
         return cudaGetLastError();
     }
