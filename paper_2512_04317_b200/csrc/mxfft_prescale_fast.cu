@@ -187,6 +187,34 @@ __device__ void reg_bitonic_sort(T* a, int P) {
     __syncthreads();
 }
 
+// Order statistics without sorting: the elements of rank r0, r1, r2 of
+// a[0..P) (ascending; ties broken by index, so ranks are a permutation) go to
+// out[0..2] (a rank < 0 is skipped).  Each element's rank is counted against
+// broadcast shared-memory reads -- no barriers between phases.
+template <typename T, int NT>
+__device__ void rank_select(const T* a, int P, int r0, int r1, int r2, T* out) {
+    for (int i = threadIdx.x; i < P; i += NT) {
+        const T v = a[i];
+        int r = 0;
+        int j = 0;
+        for (; j + 4 <= P; j += 4) {
+            const T u0 = a[j], u1 = a[j + 1], u2 = a[j + 2], u3 = a[j + 3];
+            r += (u0 < v) | ((u0 == v) & (j < i));
+            r += (u1 < v) | ((u1 == v) & (j + 1 < i));
+            r += (u2 < v) | ((u2 == v) & (j + 2 < i));
+            r += (u3 < v) | ((u3 == v) & (j + 3 < i));
+        }
+        for (; j < P; ++j) {
+            const T u = a[j];
+            r += (u < v) | ((u == v) & (j < i));
+        }
+        if (r == r0) out[0] = v;
+        if (r == r1) out[1] = v;
+        if (r == r2) out[2] = v;
+    }
+    __syncthreads();
+}
+
 // sort a[0..P), P <= NT * MAXS, with the smallest power-of-two slot count
 template <typename T, int NT, int MAXS>
 __device__ void sort_block(T* a, int P) {
@@ -535,6 +563,8 @@ struct FusedShared {
     unsigned warp_sums[NT / 32];
     unsigned long long amax_b;
     unsigned snz, nnz, below, ncand, ntop, flags, wn;
+    unsigned sel[3];  // selected sample keys
+    double wsel[3];   // selected window magnitudes
     float lo, hi, top;
     int bt, bt1;
     unsigned woff, wend;
@@ -596,21 +626,32 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_ps_fused(const float2* __rest
         if (lane == 0) atomicAdd(&F.snz, (unsigned)cnt);
         __syncthreads();
         PS_T(0)
-        sort_block<unsigned, F_THREADS, SAMPLE_MAX / F_THREADS>(F.u.keys, S);
+        // the bracket needs three order statistics of the sample
+        const int n = (int)F.snz;
+        const double rs = (double)(n - 1) * q;
+        const int d = 8 + (int)(4.0 * sqrt(rs + 1.0));
+        const int ilo = (int)floor(rs) - d, ihi = (int)ceil(rs) + 1 + d;
+        if (S <= F_THREADS) {
+            rank_select<unsigned, F_THREADS>(F.u.keys, S, ilo > 0 ? ilo : -1, ihi < n ? ihi : -1, n - 1, F.sel);
+        } else {
+            sort_block<unsigned, F_THREADS, SAMPLE_MAX / F_THREADS>(F.u.keys, S);
+            if (tid == 0) {
+                if (ilo > 0) F.sel[0] = F.u.keys[ilo];
+                if (ihi < n) F.sel[1] = F.u.keys[ihi];
+                if (n > 0) F.sel[2] = F.u.keys[n - 1];
+            }
+            __syncthreads();
+        }
         PS_T(1)
         if (tid == 0) {
-            const int n = (int)F.snz;
             if (n == 0) {
                 F.lo = 0.f;
                 F.hi = __int_as_float(0x7f800000);
                 F.top = 0.f;
             } else {
-                const double rs = (double)(n - 1) * q;
-                const int d = 8 + (int)(4.0 * sqrt(rs + 1.0));
-                const int ilo = (int)floor(rs) - d, ihi = (int)ceil(rs) + 1 + d;
-                F.lo = ilo <= 0 ? 0.f : __uint_as_float(F.u.keys[ilo]) * (1.f - 0x1p-20f);
-                F.hi = ihi >= n ? __int_as_float(0x7f800000) : __uint_as_float(F.u.keys[ihi]) * (1.f + 0x1p-20f);
-                F.top = __uint_as_float(F.u.keys[n - 1]) * (1.f - 0x1p-20f);
+                F.lo = ilo <= 0 ? 0.f : __uint_as_float(F.sel[0]) * (1.f - 0x1p-20f);
+                F.hi = ihi >= n ? __int_as_float(0x7f800000) : __uint_as_float(F.sel[1]) * (1.f + 0x1p-20f);
+                F.top = __uint_as_float(F.sel[2]) * (1.f - 0x1p-20f);
             }
         }
         __syncthreads();
@@ -803,18 +844,15 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_ps_fused(const float2* __rest
         }
         __syncthreads();
         PS_T(5)
-        int P = 1;
-        while (P < (int)wcount) P <<= 1;
-        for (int i = (int)wcount + tid; i < P; i += F_THREADS) F.u.w[i] = DBL_MAX;
-        __syncthreads();
-        sort_block<double, F_THREADS, WCAP / F_THREADS>(F.u.w, P);
+        const int P = (int)wcount;
+        rank_select<double, F_THREADS>(F.u.w, P, (int)(t - woff), (int)(t1 - woff), -1, F.wsel);
         PS_T(6)
 #ifdef PS_TIMING
         if (tid == 0 && (seg == 0 || seg == 100))
             printf("seg %d S=%d nc=%u wcount=%u P=%d | sampled %lld sorted %lld stream0 %lld streamed %lld hist+scan %lld window %lld wsorted %lld\n",
                    seg, S, nc, wcount, P, TS[0], TS[1], TS[2], TS[3], TS[4], TS[5], TS[6]);
 #endif
-        const double vlo = F.u.w[t - woff], vhi = F.u.w[t1 - woff];
+        const double vlo = F.wsel[0], vhi = F.wsel[1];
         const float elo = wlo > 0 ? __uint_as_float(bin_lo(wlo, klo, inv)) : glo;
         const float ehi = whi < NBIN - 1 ? __uint_as_float(bin_lo(whi + 1, klo, inv)) : ghi;
         bool good = true;
