@@ -108,6 +108,67 @@ def pipeline_device(x, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, coil
     return y, k, res
 
 
+_HOST_PIPE = {}  # per device: (streams, events) of pipeline_host
+
+
+def pipeline_host(x_host, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, out_host=None,
+                  coils: int = 1, chunks: int = 8):
+    """pipeline_device for a batch that lives in (pinned) host memory: the batch
+    is cut into `chunks` slices of whole coil stacks; slice i+1 is copied in on
+    one stream while slice i is transformed on another and slice i-1 is copied
+    out on a third (PCIe is full duplex).  Two device buffers ping-pong.
+    x_host: CPU complex64 (B*coils, N, N), pinned for overlap.  Returns
+    out_host (allocated pinned if None) once every copy has finished."""
+    import torch
+
+    if x_host.is_cuda or x_host.dtype != torch.complex64:
+        raise TypeError("pipeline_host takes a host complex64 tensor")
+    n = plan.n
+    nstack = x_host.shape[0] // coils
+    chunks = max(1, min(chunks, nstack))
+    per = (nstack + chunks - 1) // chunks * coils  # images per slice
+    if out_host is None:
+        out_host = torch.empty(x_host.shape, dtype=x_host.dtype).pin_memory()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    key = str(dev)
+    if key not in _HOST_PIPE:
+        _HOST_PIPE[key] = [torch.cuda.Stream(dev) for _ in range(3)]
+    s_in, s_cmp, s_out = _HOST_PIPE[key]
+    cur = torch.cuda.current_stream(dev)
+    xb = [torch.empty((per, n, n), dtype=torch.complex64, device=dev) for _ in range(2)]
+    yb = [torch.empty((per, n, n), dtype=torch.complex64, device=dev) for _ in range(2)]
+    kb = [torch.empty(per // coils, dtype=torch.int32, device=dev) for _ in range(2)]
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_cmp = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
+    for s in (s_in, s_cmp, s_out):
+        s.wait_stream(cur)  # buffers were allocated on the current stream
+    for i, start in enumerate(range(0, x_host.shape[0], per)):
+        b = i & 1
+        m = min(per, x_host.shape[0] - start)
+        if i >= 2:
+            s_in.wait_event(ev_cmp[b])  # slice i-2 no longer reads xb[b]
+        with torch.cuda.stream(s_in):
+            xb[b][:m].copy_(x_host[start:start + m], non_blocking=True)
+            ev_in[b].record(s_in)
+        s_cmp.wait_event(ev_in[b])
+        if i >= 2:
+            s_cmp.wait_event(ev_out[b])  # slice i-2 has left yb[b]
+        with torch.cuda.stream(s_cmp):
+            pipeline_device(xb[b][:m], plan, cfg, roundtrip, coils=coils, out=yb[b][:m], k=kb[b][:m // coils])
+            ev_cmp[b].record(s_cmp)
+        s_out.wait_event(ev_cmp[b])
+        with torch.cuda.stream(s_out):
+            out_host[start:start + m].copy_(yb[b][:m], non_blocking=True)
+            ev_out[b].record(s_out)
+    for t in xb + yb + kb:
+        for s in (s_in, s_cmp, s_out):
+            t.record_stream(s)
+    cur.wait_stream(s_out)
+    s_out.synchronize()
+    return out_host
+
+
 def _run_grid(grid: ComplexGrid, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool) -> RssImage:
     import torch
 

@@ -570,3 +570,18 @@ def test_metrics_match_reference(mx):
         mx.psnr(np.zeros((16, 16)), np.ones((16, 16)))
     with pytest.raises(mx.WindowTooLarge):
         mx.ssim(np.ones((8, 8)), np.ones((8, 8)))
+
+
+def test_pipeline_host_matches_device(mx, torch):
+    """The sliced, stream-overlapped host API equals the device pipeline."""
+    from paper_2512_04317_b200.workloads import ellipse_kspace_batch
+
+    x = ellipse_kspace_batch(10, 64, seed=3)
+    p = mx.make_plan(64, mx.ModeSpec.mx(mx.E4M3, 32))
+    cfg = mx.PrescaleConfig()
+    want, _, _ = mx.pipeline_device(torch.from_numpy(x).cuda(), p, cfg, True)
+    got = mx.pipeline_host(torch.from_numpy(x).pin_memory(), p, cfg, True, chunks=3)
+    assert torch.equal(torch.view_as_real(got), torch.view_as_real(want.cpu()))
+    got2 = mx.pipeline_host(torch.from_numpy(x), p, cfg, False, chunks=4)
+    want2, _, _ = mx.pipeline_device(torch.from_numpy(x).cuda(), p, cfg, False)
+    assert torch.equal(torch.view_as_real(got2), torch.view_as_real(want2.cpu()))
