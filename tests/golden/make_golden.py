@@ -204,6 +204,24 @@ def metrics_fixture(rng):
     return out
 
 
+def phantoms_fixture(rng):
+    """gen_phantom / coil_sensitivities outputs and MXCG file bytes."""
+    import tempfile
+
+    out = {}
+    cases = [(32, 2, 5, "blobs", 0.1, 1e-4), (64, 1, 6, "bars", 0.0, 1e-4), (16, 3, 7, "blobs", 0.0, 0.0)]
+    for ci, (n, coils, seed, kind, tail, noise) in enumerate(cases):
+        img, ksp = R.gen_phantom(n, coils, seed, kind=kind, tail=tail, noise=noise)
+        out[f"c{ci}_img"] = img.data
+        out[f"c{ci}_ksp"] = ksp.data
+        with tempfile.NamedTemporaryFile(suffix=".mxcg") as f:
+            R.write_grid(ksp, f.name)
+            out[f"c{ci}_mxcg"] = np.frombuffer(open(f.name, "rb").read(), dtype=np.uint8)
+    out["sens"] = R.coil_sensitivities(16, 4, 3)
+    out["cases"] = np.array([f"{a}:{b}:{c}:{d}:{e}:{f}" for a, b, c, d, e, f in cases])
+    return out
+
+
 def prescale_fixture(rng):
     cfg = R.PrescaleConfig()
     inputs = []
@@ -276,7 +294,7 @@ def main():
                      ("stages", stage_fixture), ("fft2", fft2_fixture),
                      ("prescale", prescale_fixture), ("pipelines", pipeline_fixture),
                      ("twiddles", twiddle_fixture), ("modes", modes_fixture),
-                     ("metrics", metrics_fixture)]:
+                     ("metrics", metrics_fixture), ("phantoms", phantoms_fixture)]:
         data = fn(rng)
         path = os.path.join(OUT, f"{name}.npz")
         np.savez_compressed(path, **data)

@@ -585,3 +585,13 @@ def test_pipeline_host_matches_device(mx, torch):
     got2 = mx.pipeline_host(torch.from_numpy(x), p, cfg, False, chunks=4)
     want2, _, _ = mx.pipeline_device(torch.from_numpy(x).cuda(), p, cfg, False)
     assert torch.equal(torch.view_as_real(got2), torch.view_as_real(want2.cpu()))
+
+
+def test_gen_phantom_matches_reference(mx):
+    """gen_phantom's k-space comes from the GPU FP64 transform: identical grids."""
+    g = golden("phantoms")
+    for ci, case in enumerate(g["cases"]):
+        n, coils, seed, kind, tail, noise = str(case).split(":")
+        img, ksp = mx.gen_phantom(int(n), int(coils), int(seed), kind=kind, tail=float(tail), noise=float(noise))
+        assert_same(img.data, g[f"c{ci}_img"], f"{case} image")
+        assert_same(ksp.data, g[f"c{ci}_ksp"], f"{case} kspace")
