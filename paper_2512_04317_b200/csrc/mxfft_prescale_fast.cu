@@ -73,7 +73,7 @@ bool prescale_fast_ok(int64_t npts) { return npts >= 1024 && npts <= (int64_t(1)
 int64_t prescale_fast_ws_bytes(int64_t nseg, int64_t npts) {
     const int64_t st = ((int64_t)sizeof(SegState) * nseg + 255) / 256 * 256;
     const int64_t fb = ((int64_t)sizeof(int) * (nseg + 1) + 255) / 256 * 256;
-    if (npts <= FUSED_MAX) return st + fb;
+    if (npts <= FUSED_MAX && nseg >= 32) return st + fb;
     return st + fb + nseg * (cand_cap(npts) + TOPCAP) * (int64_t)sizeof(float2);
 }
 
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_ps_sample(const float2* __restr
     for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if ((tid & 31) == 0) atomicAdd(&snz, cnt);
     __syncthreads();
-    bitonic_sort<unsigned>(keys, S);
+    sort_block<unsigned, SEL_THREADS, SAMPLE_MAX / SEL_THREADS>(keys, S);
     if (tid == 0) {
         SegState g;
         const int n = snz;
@@ -379,6 +379,7 @@ __device__ __forceinline__ int round_half_away_d(double v) {
 struct SelShared {
     unsigned hist[NBIN];
     double w[WCAP];
+    double wsel[3];
     unsigned warp_sums[SEL_THREADS / 32];
     unsigned long long amax_b;
     unsigned wn;
@@ -495,12 +496,8 @@ __global__ void __launch_bounds__(SEL_THREADS) k_ps_select(SegState* st, int* li
             if (b >= wlo && b <= whi) S.w[atomicAdd(&S.wn, 1u)] = np_cabs_f((double)v.x, (double)v.y);
         }
         __syncthreads();
-        int P = 1;
-        while (P < (int)wcount) P <<= 1;
-        for (int i = (int)wcount + tid; i < P; i += SEL_THREADS) S.w[i] = DBL_MAX;
-        __syncthreads();
-        bitonic_sort<double>(S.w, P);
-        const double vlo = S.w[t - woff], vhi = S.w[t1 - woff];
+        rank_select<double, SEL_THREADS>(S.w, (int)wcount, (int)(t - woff), (int)(t1 - woff), -1, S.wsel);
+        const double vlo = S.wsel[0], vhi = S.wsel[1];
         // every point outside the window must order strictly on its side:
         // the picks must clear the window's key edges by more than the key rounding
         const float elo = wlo > 0 ? __uint_as_float(bin_lo(wlo, klo, inv)) : g.lo;
@@ -881,7 +878,9 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
     w += ((int64_t)sizeof(int) * (nseg + 1) + 255) / 256 * 256;
     *list_out = list;
     *list_n_out = list_n;
-    if (npts <= FUSED_MAX) {
+    // the fused kernel streams a segment with ONE CTA: with few segments the
+    // grid-wide path (sample / multi-CTA count / select) fills the GPU better
+    if (npts <= FUSED_MAX && nseg >= 32) {
         static bool attr = false;
         if (!attr) {
             cudaError_t e = cudaFuncSetAttribute(k_ps_fused<256, 4096, 1, 4096, 2048, 1024>,
