@@ -595,3 +595,44 @@ def test_gen_phantom_matches_reference(mx):
         img, ksp = mx.gen_phantom(int(n), int(coils), int(seed), kind=kind, tail=float(tail), noise=float(noise))
         assert_same(img.data, g[f"c{ci}_img"], f"{case} image")
         assert_same(ksp.data, g[f"c{ci}_ksp"], f"{case} kspace")
+
+
+def test_small_sizes_generic_kernel_and_empty_batches(mx, torch, rng):
+    """n = 2..16 (the generic reference-literal kernel), every format, against
+    the oracle; block sizes above n (cpb = min(B/2, n/2)); empty batches."""
+    for name in FMTS:
+        for n in (2, 4, 8, 16):
+            for bsz in (2, 8, 64):
+                x = ((rng.standard_normal((5, n)) + 1j * rng.standard_normal((5, n)))
+                     * 10.0 ** rng.uniform(-3, 3, (5, 1))).astype(np.complex64)
+                p = mx.make_plan(n, mx.ModeSpec.mx(mx.get_mx_format(name), bsz))
+                op = O.make_plan(n, O.ALL_MX[name], bsz)
+                for inv in (False, True):
+                    got = mx.fftcore.fft_rows_device(torch.from_numpy(x).cuda(), p, inv).cpu().numpy()
+                    assert_same(got, O.fft_batch(x, op, inv), f"{name}:{bsz}:{n}:{inv}")
+            img = ((rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))).astype(np.complex64)
+            p = mx.make_plan(n, mx.ModeSpec.mx(mx.get_mx_format(name), 32))
+            assert_same(mx.fft_2d(img, p), O.fft2(img, O.make_plan(n, O.ALL_MX[name], 32), False), f"2d {name} {n}")
+    p = mx.make_plan(64, mx.ModeSpec.mx(mx.E4M3, 32))
+    e = torch.empty((0, 64, 64), dtype=torch.complex64, device="cuda")
+    assert mx.fft2_device(e, p).shape == (0, 64, 64)
+    assert mx.fft_rows_device(torch.empty((0, 64), dtype=torch.complex64, device="cuda"), p).shape == (0, 64)
+    y, k, _ = mx.pipeline_device(e, p, mx.PrescaleConfig(), True)
+    assert y.shape == (0, 64, 64) and k.numel() == 0
+
+
+def test_every_format_block_size_c3_shapes(mx, torch):
+    """C3's formats (E3M2, E2M3, E2M1) and block sweep {16, 32, 64} at 512^2:
+    pipeline outputs equal the oracle's for one image each."""
+    from paper_2512_04317_b200.workloads import ellipse_kspace
+
+    x = ellipse_kspace(512, 9, noise=0.01)
+    xd = torch.from_numpy(x[None]).cuda()
+    for name in ("e3m2", "e2m3", "e2m1", "e5m2"):
+        for bsz in (16, 32, 64):
+            p = mx.make_plan(512, mx.ModeSpec.mx(mx.get_mx_format(name), bsz))
+            op = O.make_plan(512, O.ALL_MX[name], bsz)
+            y, k, _ = mx.pipeline_device(xd, p, mx.PrescaleConfig(), True)
+            out_o, _, k_o = O.pipeline(x, op, True)
+            assert int(k[0]) == k_o
+            assert_same(y[0].cpu().numpy().astype(np.complex128), out_o[0], f"{name}:{bsz}")
