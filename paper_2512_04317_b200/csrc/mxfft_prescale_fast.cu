@@ -55,6 +55,9 @@ static inline int sample_size(int64_t npts) {
 }
 
 constexpr int64_t FUSED_MAX = int64_t(1) << 17;
+#ifndef MXFFT_FUSED_MIN_SEG
+#define MXFFT_FUSED_MIN_SEG 32  // fewer segments: the grid-wide path
+#endif
 // fused kernel: 256 threads for segments <= 2^15 points
 // (several CTAs per SM hide each other's select phase), else 512; 4096 candidates
 constexpr int F_TOPCAP = 1024;  // points above the sample maximum
@@ -73,7 +76,7 @@ bool prescale_fast_ok(int64_t npts) { return npts >= 1024 && npts <= (int64_t(1)
 int64_t prescale_fast_ws_bytes(int64_t nseg, int64_t npts) {
     const int64_t st = ((int64_t)sizeof(SegState) * nseg + 255) / 256 * 256;
     const int64_t fb = ((int64_t)sizeof(int) * (nseg + 1) + 255) / 256 * 256;
-    if (npts <= FUSED_MAX && nseg >= 32) return st + fb;
+    if (npts <= FUSED_MAX && nseg >= MXFFT_FUSED_MIN_SEG) return st + fb;
     return st + fb + nseg * (cand_cap(npts) + TOPCAP) * (int64_t)sizeof(float2);
 }
 
@@ -880,7 +883,7 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
     *list_n_out = list_n;
     // the fused kernel streams a segment with ONE CTA: with few segments the
     // grid-wide path (sample / multi-CTA count / select) fills the GPU better
-    if (npts <= FUSED_MAX && nseg >= 32) {
+    if (npts <= FUSED_MAX && nseg >= MXFFT_FUSED_MIN_SEG) {
         static bool attr = false;
         if (!attr) {
             cudaError_t e = cudaFuncSetAttribute(k_ps_fused<256, 4096, 1, 4096, 2048, 1024>,
