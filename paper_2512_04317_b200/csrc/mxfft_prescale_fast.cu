@@ -218,6 +218,25 @@ __device__ void rank_select(const T* a, int P, int r0, int r1, int r2, T* out) {
     __syncthreads();
 }
 
+template <typename T, int NT, int MAXS>
+__device__ void sort_block(T* a, int P);
+
+// The elements of rank r0 and r1 of a[0..P) -> out[0], out[1]: counted ranks
+// for small P (P^2 / NT compares, no barriers), a register sort beyond.
+template <typename T, int NT, int MAXS>
+__device__ void pick_two(T* a, int P, int r0, int r1, T* out) {
+    if (P <= 2 * NT) {
+        rank_select<T, NT>(a, P, r0, r1, -1, out);
+        return;
+    }
+    sort_block<T, NT, MAXS>(a, P);
+    if (threadIdx.x == 0) {
+        out[0] = a[r0];
+        out[1] = a[r1];
+    }
+    __syncthreads();
+}
+
 // sort a[0..P), P <= NT * MAXS, with the smallest power-of-two slot count
 template <typename T, int NT, int MAXS>
 __device__ void sort_block(T* a, int P) {
@@ -499,7 +518,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_ps_select(SegState* st, int* li
             if (b >= wlo && b <= whi) S.w[atomicAdd(&S.wn, 1u)] = np_cabs_f((double)v.x, (double)v.y);
         }
         __syncthreads();
-        rank_select<double, SEL_THREADS>(S.w, (int)wcount, (int)(t - woff), (int)(t1 - woff), -1, S.wsel);
+        pick_two<double, SEL_THREADS, WCAP / SEL_THREADS>(S.w, (int)wcount, (int)(t - woff), (int)(t1 - woff), S.wsel);
         const double vlo = S.wsel[0], vhi = S.wsel[1];
         // every point outside the window must order strictly on its side:
         // the picks must clear the window's key edges by more than the key rounding
@@ -845,7 +864,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_ps_fused(const float2* __rest
         __syncthreads();
         PS_T(5)
         const int P = (int)wcount;
-        rank_select<double, F_THREADS>(F.u.w, P, (int)(t - woff), (int)(t1 - woff), -1, F.wsel);
+        pick_two<double, F_THREADS, WCAP / F_THREADS>(F.u.w, P, (int)(t - woff), (int)(t1 - woff), F.wsel);
         PS_T(6)
 #ifdef PS_TIMING
         if (tid == 0 && (seg == 0 || seg == 100))
