@@ -222,6 +222,23 @@ def phantoms_fixture(rng):
     return out
 
 
+def multicoil_fixture(rng):
+    """forward_pipeline / roundtrip_pipeline on multi-coil phantom stacks (one
+    global prescale per stack, RSS over coils)."""
+    out = {}
+    cases = [("e4m3", 32, 64, 4, "blobs"), ("e5m2", 16, 32, 3, "bars"), ("e2m1", 32, 64, 2, "blobs")]
+    cfg = R.PrescaleConfig()
+    for ci, (name, bsz, n, coils, kind) in enumerate(cases):
+        img, ksp = R.gen_phantom(n, coils, 50 + ci, kind=kind, tail=0.05)
+        plan = R.make_plan(n, R.ModeSpec.mx(FMTS[name], bsz))
+        out[f"c{ci}_ksp"] = ksp.data
+        out[f"c{ci}_img"] = img.data
+        out[f"c{ci}_fwd"] = R.forward_pipeline(ksp, plan, cfg).pixels
+        out[f"c{ci}_rt"] = R.roundtrip_pipeline(img, plan, cfg).pixels
+    out["cases"] = np.array([f"{a}:{b}:{c}:{d}:{e}" for a, b, c, d, e in cases])
+    return out
+
+
 def prescale_fixture(rng):
     cfg = R.PrescaleConfig()
     inputs = []
@@ -294,7 +311,8 @@ def main():
                      ("stages", stage_fixture), ("fft2", fft2_fixture),
                      ("prescale", prescale_fixture), ("pipelines", pipeline_fixture),
                      ("twiddles", twiddle_fixture), ("modes", modes_fixture),
-                     ("metrics", metrics_fixture), ("phantoms", phantoms_fixture)]:
+                     ("metrics", metrics_fixture), ("phantoms", phantoms_fixture),
+                     ("multicoil", multicoil_fixture)]:
         data = fn(rng)
         path = os.path.join(OUT, f"{name}.npz")
         np.savez_compressed(path, **data)
