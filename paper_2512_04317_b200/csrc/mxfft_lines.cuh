@@ -28,6 +28,10 @@
 #include "mxfft_generic.cuh"
 #include "mxfft_internal.h"
 
+#ifndef MXFFT_LOCAL_STAGES
+#define MXFFT_LOCAL_STAGES 5  // unrolled register stages before the shared-memory loop
+#endif
+
 namespace mxfft {
 
 // ---------------------------------------------------------------------------
@@ -530,19 +534,21 @@ __device__ __forceinline__ void run_stages(float2 (&x)[32], int& U, int& V, cons
                                            unsigned rb, int ebase, LDbg* dbg, bool& bad) {
     const int lt = LT >= 0 ? LT : L.lt;
     const bool big = lt > 5;  // a line spans several warps
-    const int lim_loc = L.slim < 5 ? L.slim : 5;
+    constexpr int LOCAL = MXFFT_LOCAL_STAGES;  // unrolled register stages (4 or 5)
+    const int lim_loc = L.slim < LOCAL ? L.slim : LOCAL;
     if (lim_loc > 0) local_stage<ID, CPB, 0, DBG>(x, L.tw, L.twe, L.c, L.trivial, L.sigma, dbg, bad);
     if (lim_loc > 1) local_stage<ID, CPB, 1, DBG>(x, L.tw, L.twe, L.c, L.trivial, L.sigma, dbg, bad);
     if (lim_loc > 2) local_stage<ID, CPB, 2, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg, bad);
     if (lim_loc > 3) local_stage<ID, CPB, 3, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg, bad);
-    if (lim_loc > 4) local_stage<ID, CPB, 4, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg, bad);
+    if constexpr (LOCAL > 4)
+        if (lim_loc > 4) local_stage<ID, CPB, 4, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg, bad);
     U = 32 * L.c;
     V = U + 16;
     // kept rolled: one copy of the stage body keeps the kernel inside the
     // instruction cache (unrolling measured slower)
     const int last = L.slim < lt + 5 ? L.slim : lt + 5;
 #pragma unroll 1
-    for (int s = 5; s < last; ++s) smem_stage<ID, CPB, DBG>(x, U, V, L, rb, ebase, s, big, dbg, bad);
+    for (int s = LOCAL; s < last; ++s) smem_stage<ID, CPB, DBG>(x, U, V, L, rb, ebase, s, big, dbg, bad);
 }
 
 __device__ __forceinline__ void cp_async16(unsigned dst, const void* src, bool valid) {

@@ -105,22 +105,6 @@ struct Limits<double> {
     static __device__ __forceinline__ double shfl_xor(double v, int j) { return __shfl_xor_sync(0xffffffffu, v, j); }
 };
 
-template <typename T>
-__device__ void bitonic_sort(T* a, int P) {  // ascending, P a power of two, whole block
-    for (int k = 2; k <= P; k <<= 1)
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < P; i += blockDim.x) {
-                const int l = i ^ j;
-                if (l > i) {
-                    const T x = a[i], y = a[l];
-                    if ((x > y) == ((i & k) == 0)) {
-                        a[i] = y;
-                        a[l] = x;
-                    }
-                }
-            }
-            __syncthreads();
-        }
 }
 
 // Block-wide ascending bitonic sort of a[0..P) (P <= NT * SLOTS) with the
