@@ -105,8 +105,6 @@ struct Limits<double> {
     static __device__ __forceinline__ double shfl_xor(double v, int j) { return __shfl_xor_sync(0xffffffffu, v, j); }
 };
 
-}
-
 // Block-wide ascending bitonic sort of a[0..P) (P <= NT * SLOTS) with the
 // elements in registers: element i = tid + NT * s lives in slot s of thread
 // tid (pads past P sort last).  Compare-exchange distance j < 32: warp shuffle;
