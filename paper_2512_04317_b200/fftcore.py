@@ -433,10 +433,11 @@ def _mx_multiply_device(vr, vi, w_enc, fmt: MinifloatFormat, cpb: int):
     mm, em = np.frexp(fmt.max_finite)
     shift = torch.where(amax > fmt.max_finite, ea - int(em) + (ma > float(mm)).to(torch.int32),
                         torch.zeros_like(ea))
-    fac = torch.ldexp(torch.ones((), dtype=torch.float64, device="cuda"), -shift).to(pdt)
+    one = torch.ones_like(shift, dtype=torch.float64)
+    fac = torch.ldexp(one, -shift).to(pdt)
     p_r = p_r * fac[..., None]
     p_i = p_i * fac[..., None]
-    s_out = s_out * torch.ldexp(torch.ones((), dtype=torch.float64, device="cuda"), shift)
+    s_out = s_out * torch.ldexp(one, shift)
     c_r = quantize_device(p_r.to(torch.float64), fmt)
     c_i = quantize_device(p_i.to(torch.float64), fmt)
     so = s_out[..., None]
