@@ -169,6 +169,12 @@ int32_t mxfft_metrics(const double* ref, const double* test, int64_t h, int64_t 
  * y[b][j][i] = x[b][i][j] (the rows.T between the passes of fft_2d,
  * fftcore.py:352); n a multiple of 64. */
 int32_t mxfft_transpose_c64(const void* x, void* y, int64_t batch, int32_t n, uintptr_t stream);
+/* Same from n x n blocks of a larger array: block b starts at
+ * x + b * batch_stride_x, rows ld_x apart (0 = the dense defaults n*n / n);
+ * y stays dense.  The row-slab all-to-all uses it to transpose the (N/G)^2
+ * blocks of a slab straight into send order. */
+int32_t mxfft_transpose_c64_strided(const void* x, int64_t ld_x, int64_t batch_stride_x, void* y, int64_t batch,
+                                    int32_t n, uintptr_t stream);
 
 /* compute_prescale (prescale.py:61-73) over `nseg` segments of `seg_points`
  * complex values each (complex64 when is_c128 == 0, else complex128),

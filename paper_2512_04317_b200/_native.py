@@ -57,6 +57,7 @@ SIGNATURES = {
     "mxfft_fft2": ([_vp, _vp, _vp, _i64, _i32, _vp, _i32, _vp, _i64, _u], _i32),
     "mxfft_fft2_workspace_bytes": ([_vp, _i64], _i64),
     "mxfft_transpose_c64": ([_vp, _vp, _i64, _i32, _u], _i32),
+    "mxfft_transpose_c64_strided": ([_vp, _i64, _i64, _vp, _i64, _i32, _u], _i32),
     "mxfft_metrics": ([_vp, _vp, _i64, _i64, _i32, _vp, ctypes.c_double, ctypes.c_double, _vp, _u], _i32),
     "mxfft_fft_rows_fp16": ([_vp, _i32, _vp, _i64, _i32, _vp, _i32, _vp, _u], _i32),
     "mxfft_fft_rows_f64": ([_vp, _vp, _i64, _i32, _vp, _i32, _u], _i32),

@@ -335,10 +335,16 @@ int32_t mxfft_metrics(const double* ref, const double* test, int64_t h, int64_t 
 }
 
 int32_t mxfft_transpose_c64(const void* x, void* y, int64_t batch, int32_t n, uintptr_t stream) {
+    return mxfft_transpose_c64_strided(x, 0, 0, y, batch, n, stream);
+}
+
+int32_t mxfft_transpose_c64_strided(const void* x, int64_t ld_x, int64_t batch_stride_x, void* y, int64_t batch,
+                                    int32_t n, uintptr_t stream) {
     if (batch < 0 || n <= 0) return fail(MXFFT_ERR_SHAPE, "bad transpose shape");
     if (n % 64) return fail(MXFFT_ERR_UNSUPPORTED_SIZE, "transpose needs n to be a multiple of 64");
     if (x == y) return fail(MXFFT_ERR_VALUE, "transpose is out of place");
-    CK(launch_transpose_c64(x, y, batch, n, (cudaStream_t)stream), "transpose");
+    if (ld_x != 0 && ld_x < n) return fail(MXFFT_ERR_SHAPE, "source row stride below n");
+    CK(launch_transpose_c64(x, y, batch, n, (cudaStream_t)stream, ld_x, batch_stride_x), "transpose");
     return MXFFT_OK;
 }
 

@@ -226,7 +226,8 @@ __global__ void k_rss(const T* __restrict__ x, int64_t groups, int coils, int64_
 // shared memory; every global access is a 512-byte warp-contiguous run.
 constexpr int TT = 64;
 __global__ void __launch_bounds__(256) k_transpose_c64(const float2* __restrict__ x, float2* __restrict__ y,
-                                                       int n, int tiles_per_dim, int64_t ntiles) {
+                                                       int n, int tiles_per_dim, int64_t ntiles, int64_t ldx,
+                                                       int64_t bsx) {
     __shared__ float2 tile[TT][TT + 1];
     const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4 threads
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -234,10 +235,10 @@ __global__ void __launch_bounds__(256) k_transpose_c64(const float2* __restrict_
         const int64_t b = t / per;
         const int r = (int)(t - b * per);
         const int i0 = (r / tiles_per_dim) * TT, j0 = (r % tiles_per_dim) * TT;
-        const float2* xb = x + b * (int64_t)n * n;
+        const float2* xb = x + b * bsx;
         float2* yb = y + b * (int64_t)n * n;
 #pragma unroll 4
-        for (int k = ty; k < TT; k += 4) tile[k][tx] = xb[(int64_t)(i0 + k) * n + j0 + tx];
+        for (int k = ty; k < TT; k += 4) tile[k][tx] = xb[(int64_t)(i0 + k) * ldx + j0 + tx];
         __syncthreads();
 #pragma unroll 4
         for (int k = ty; k < TT; k += 4) yb[(int64_t)(j0 + k) * n + i0 + tx] = tile[tx][k];
@@ -245,14 +246,17 @@ __global__ void __launch_bounds__(256) k_transpose_c64(const float2* __restrict_
     }
 }
 
-cudaError_t launch_transpose_c64(const void* x, void* y, int64_t batch, int n, cudaStream_t st) {
+cudaError_t launch_transpose_c64(const void* x, void* y, int64_t batch, int n, cudaStream_t st,
+                                 int64_t ldx, int64_t bsx) {
     if (batch <= 0) return cudaSuccess;
     if (n % TT) return cudaErrorInvalidValue;
+    if (ldx <= 0) ldx = n;
+    if (bsx <= 0) bsx = (int64_t)n * n;
     const int tpd = n / TT;
     const int64_t ntiles = batch * (int64_t)tpd * tpd;
     const unsigned grid = (unsigned)(ntiles < 148 * 8 ? ntiles : 148 * 8);
     k_transpose_c64<<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(x), reinterpret_cast<float2*>(y), n,
-                                          tpd, ntiles);
+                                          tpd, ntiles, ldx, bsx);
     note_launch();
     return cudaGetLastError();
 }

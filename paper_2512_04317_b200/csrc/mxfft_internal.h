@@ -104,7 +104,8 @@ cudaError_t launch_decode_f64(const double* codes, const double* scales, int64_t
                               int block_len, double* out, cudaStream_t st);
 cudaError_t plan_encode(Plan& p, const double* d_tw, cudaStream_t st);
 cudaError_t launch_cabs(const void* x, int is_c128, int64_t n, double* out, cudaStream_t st);
-cudaError_t launch_transpose_c64(const void* x, void* y, int64_t batch, int n, cudaStream_t st);
+cudaError_t launch_transpose_c64(const void* x, void* y, int64_t batch, int n, cudaStream_t st,
+                                 int64_t ldx = 0, int64_t bsx = 0);
 cudaError_t launch_metrics(const double* r, const double* t, int64_t h, int64_t w, int do_ssim, const double* win,
                            double c1, double c2, double* out, cudaStream_t st);
 cudaError_t launch_fp16_rows(const void* x, int x_is_c128, void* y, int64_t batch, int n, const void* tw,

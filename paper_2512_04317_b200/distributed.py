@@ -127,6 +127,20 @@ class CudaOps:
         below, ncand, ntop, flags = (int(v) for v in np.frombuffer(s, dtype="<u4", count=4, offset=24))
         return (nnz, below, ncand, ntop, flags), cand[: min(ncand, cand_cap)], topb[: min(ntop, top_cap)]
 
+    def block_transpose(self, a, g: int):
+        """(R, G*R) slab -> (G, R, R) send buffer, block j = (a[:, jR:(j+1)R])^T
+        (mxfft_transpose_c64_strided; torch's copy for R not a multiple of 64)."""
+        import torch
+
+        R = a.shape[0]
+        out = torch.empty((g, R, R), dtype=a.dtype, device=a.device)
+        if R % 64 or a.dtype != torch.complex64:
+            out.copy_(a.reshape(R, g, R).permute(1, 2, 0))
+            return out
+        _native.check(_native.lib().mxfft_transpose_c64_strided(a.data_ptr(), a.shape[1], R, out.data_ptr(), g, R,
+                                                                _native.stream_handle()))
+        return out
+
     def cabs(self, z):
         import torch
 
@@ -226,17 +240,19 @@ def compute_prescale_global(x_local, cfg: PrescaleConfig, comm: Comm = None, ops
     return PrescaleResult(k=k, a_max=a_max, p_tau=p_tau, k1=k1, k2=k2)
 
 
-def _transpose_slabs(a, comm: Comm):
+def _transpose_slabs(a, comm: Comm, ops):
     """(R, N) = this rank's rows of A  ->  (R, N) = this rank's rows of A^T
-    (one all-to-all of R x R blocks)."""
+    (one all-to-all of R x R blocks).  The sender transposes
+    each block on the way into the send buffer; the receiver only interleaves
+    contiguous runs of R."""
     import torch
 
     G = comm.world
     R, N = a.shape
-    send = a.reshape(R, G, R).permute(1, 0, 2).contiguous()  # [j][r][c] = A[me*R + r][j*R + c]
+    send = ops.block_transpose(a, G)  # [j][c][r] = A[me*R + r][j*R + c]
     recv = torch.empty_like(send)
-    comm.all_to_all(recv, send)  # recv[i][r][c] = A[i*R + r][me*R + c]
-    return recv.permute(2, 0, 1).reshape(R, N).contiguous()  # [c][i*R + r] = A^T[me*R + c][i*R + r]
+    comm.all_to_all(recv, send)  # recv[i][c][r] = A[i*R + r][me*R + c]
+    return recv.permute(1, 0, 2).reshape(R, N).contiguous()  # [c][i*R + r] = A^T[me*R + c][i*R + r]
 
 
 def fft2_slab(x_slab, plan, mode: str = "forward", comm: Comm = None, ops=None, k: int = 0,
@@ -262,9 +278,9 @@ def fft2_slab(x_slab, plan, mode: str = "forward", comm: Comm = None, ops=None, 
     for i, inv in enumerate(dirs):
         first, last = i == 0, i == len(dirs) - 1
         if i > 0:  # every later pass works on the rows of the previous result's transpose
-            y = _transpose_slabs(y, comm)
+            y = _transpose_slabs(y, comm, ops)
         y = ops.rows(y, plan, inv, exp_in=k if first else 0, exp_out=out_exp if last else 0)
-    return _transpose_slabs(y, comm) if restore else y
+    return _transpose_slabs(y, comm, ops) if restore else y
 
 
 def pipeline_slab(x_slab, plan, cfg: PrescaleConfig, roundtrip: bool, comm: Comm = None, ops=None):

@@ -58,5 +58,9 @@ class OracleOps:
         counts = (int(nz.sum()), int((nz & (k < np.float32(lo))).sum()), int(cm.sum()), int(tm.sum()), flags)
         return counts, torch.from_numpy(cand[:cand_cap].copy()), torch.from_numpy(topv[:top_cap].copy())
 
+    def block_transpose(self, a, g):
+        R = a.shape[0]
+        return torch.from_numpy(np.ascontiguousarray(a.numpy().reshape(R, g, R).transpose(1, 2, 0)))
+
     def cabs(self, z):
         return torch.from_numpy(O.cabs(z.numpy().astype(np.complex128)))

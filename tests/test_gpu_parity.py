@@ -650,3 +650,13 @@ def test_multicoil_pipelines_golden(mx):
         rt = mx.roundtrip_pipeline(mx.ComplexGrid(g[f"c{ci}_img"], "image"), p, cfg)
         assert_same(fwd.pixels, g[f"c{ci}_fwd"], f"{case} forward rss")
         assert_same(rt.pixels, g[f"c{ci}_rt"], f"{case} round-trip rss")
+
+
+def test_strided_block_transpose(mx, torch):
+    from paper_2512_04317_b200 import distributed as D
+
+    for R, G in ((64, 4), (128, 2), (96, 3)):
+        a = torch.randn(R, G * R, dtype=torch.complex64, device="cuda")
+        got = D.CudaOps().block_transpose(a, G)
+        want = a.reshape(R, G, R).permute(1, 2, 0).contiguous()
+        assert torch.equal(torch.view_as_real(got), torch.view_as_real(want))
