@@ -54,7 +54,7 @@ static inline int sample_size(int64_t npts) {
     return npts < 32768 ? 256 : (npts <= 262144 ? 1024 : SAMPLE_MAX);
 }
 
-constexpr int64_t FUSED_MAX = int64_t(1) << 17;
+constexpr int64_t FUSED_MAX = int64_t(1) << 18;
 #ifndef MXFFT_FUSED_MIN_SEG
 #define MXFFT_FUSED_MIN_SEG 32  // fewer segments: the grid-wide path
 #endif
@@ -894,6 +894,10 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
                 e = cudaFuncSetAttribute(k_ps_fused<512, 4096, 1, 4096, 2048, 1024>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sizeof(FusedShared<512, 4096, 4096, 2048, 1024>));
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(k_ps_fused<512, 8192, 1, 4096, 2048, 2048>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(FusedShared<512, 8192, 4096, 2048, 2048>));
             if (e != cudaSuccess) return e;
             attr = true;
         }
@@ -903,8 +907,11 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
         if (npts <= 32768) {
             k_ps_fused<256, 4096, 1, 4096, 2048, 1024><<<(unsigned)nseg, 256, sizeof(FusedShared<256, 4096, 4096, 2048, 1024>), st>>>(
                 x, npts, S, q, c, out, kvec, list, list_n);
-        } else {
+        } else if (npts <= (int64_t(1) << 17)) {
             k_ps_fused<512, 4096, 1, 4096, 2048, 1024><<<(unsigned)nseg, 512, sizeof(FusedShared<512, 4096, 4096, 2048, 1024>), st>>>(
+                x, npts, S, q, c, out, kvec, list, list_n);
+        } else {  // C3's 512^2 images: ~1.7 % of 2^18 points in the bracket
+            k_ps_fused<512, 8192, 1, 4096, 2048, 2048><<<(unsigned)nseg, 512, sizeof(FusedShared<512, 8192, 4096, 2048, 2048>), st>>>(
                 x, npts, S, q, c, out, kvec, list, list_n);
         }
         note_launch();
