@@ -55,6 +55,9 @@ static inline int sample_size(int64_t npts) {
 }
 
 constexpr int64_t FUSED_MAX = int64_t(1) << 18;
+#ifndef MXFFT_C3_CLUSTER
+#define MXFFT_C3_CLUSTER 1  // 2-CTA clusters when few large segments leave SMs idle
+#endif
 #ifndef MXFFT_FUSED_MIN_SEG
 #define MXFFT_FUSED_MIN_SEG 32  // fewer segments: the grid-wide path
 #endif
@@ -898,6 +901,10 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
                 e = cudaFuncSetAttribute(k_ps_fused<512, 8192, 1, 4096, 2048, 2048>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sizeof(FusedShared<512, 8192, 4096, 2048, 2048>));
+            if (e == cudaSuccess && MXFFT_C3_CLUSTER)
+                e = cudaFuncSetAttribute(k_ps_fused<512, 8192, 2, 4096, 2048, 2048>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(FusedShared<512, 8192, 4096, 2048, 2048>));
             if (e != cudaSuccess) return e;
             attr = true;
         }
@@ -910,6 +917,24 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
         } else if (npts <= (int64_t(1) << 17)) {
             k_ps_fused<512, 4096, 1, 4096, 2048, 1024><<<(unsigned)nseg, 512, sizeof(FusedShared<512, 4096, 4096, 2048, 1024>), st>>>(
                 x, npts, S, q, c, out, kvec, list, list_n);
+        } else if (nseg * 2 <= 148 * 2 && MXFFT_C3_CLUSTER) {
+            // few large segments (C3: 64 x 512^2): a 2-CTA cluster per segment
+            // so that twice as many SMs stream
+            auto k = k_ps_fused<512, 8192, 2, 4096, 2048, 2048>;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)(nseg * 2));
+            cfg.blockDim = dim3(512);
+            cfg.dynamicSmemBytes = sizeof(FusedShared<512, 8192, 4096, 2048, 2048>);
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            cudaError_t e2 = cudaLaunchKernelEx(&cfg, k, x, npts, S, q, c, out, kvec, list, list_n);
+            if (e2 != cudaSuccess) return e2;
         } else {  // C3's 512^2 images: ~1.7 % of 2^18 points in the bracket
             k_ps_fused<512, 8192, 1, 4096, 2048, 2048><<<(unsigned)nseg, 512, sizeof(FusedShared<512, 8192, 4096, 2048, 2048>), st>>>(
                 x, npts, S, q, c, out, kvec, list, list_n);

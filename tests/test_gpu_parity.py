@@ -660,3 +660,18 @@ def test_strided_block_transpose(mx, torch):
         got = D.CudaOps().block_transpose(a, G)
         want = a.reshape(R, G, R).permute(1, 2, 0).contiguous()
         assert torch.equal(torch.view_as_real(got), torch.view_as_real(want))
+
+
+@pytest.mark.parametrize("n,batch", [(512, 40), (256, 48), (128, 64)])
+def test_fused_stats_variants_vs_oracle(mx, torch, n, batch):
+    """Every fused statistics variant at batch sizes that select it (512^2: the
+    2-CTA cluster kernel; 256^2 / 128^2: the single-CTA kernels): per-image
+    a_max, p_tau and k equal the oracle's."""
+    from paper_2512_04317_b200.workloads import ellipse_kspace_batch
+
+    x = ellipse_kspace_batch(batch, n, seed=77, noise=0.02)
+    res, k = mx.prescale_stats_device(torch.from_numpy(x).cuda(), batch, n * n, mx.PrescaleConfig())
+    r = mx.prescale.decode_results(res)
+    for i in range(batch):
+        o = O.compute_prescale(x[i])
+        assert (int(r[i]["k"]), float(r[i]["a_max"]), float(r[i]["p_tau"])) == (o.k, o.a_max, o.p_tau), i
