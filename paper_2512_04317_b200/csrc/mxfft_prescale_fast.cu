@@ -890,7 +890,11 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
     if (npts <= FUSED_MAX && nseg >= MXFFT_FUSED_MIN_SEG) {
         static bool attr = false;
         if (!attr) {
-            cudaError_t e = cudaFuncSetAttribute(k_ps_fused<256, 4096, 1, 4096, 2048, 1024>,
+            cudaError_t e = cudaFuncSetAttribute(k_ps_fused<256, 4096, 1, 256, 1024, 1024>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)sizeof(FusedShared<256, 4096, 256, 1024, 1024>));
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(k_ps_fused<256, 4096, 1, 4096, 2048, 1024>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)sizeof(FusedShared<256, 4096, 4096, 2048, 1024>));
             if (e == cudaSuccess)
@@ -911,7 +915,10 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
         cudaError_t e = cudaMemsetAsync(list_n, 0, sizeof(int), st);
         if (e != cudaSuccess) return e;
         const int S = fused_sample_size(npts);
-        if (npts <= 32768) {
+        if (npts < 32768) {  // S = 256: small sample / window / peak buffers, 4 CTAs per SM
+            k_ps_fused<256, 4096, 1, 256, 1024, 1024><<<(unsigned)nseg, 256, sizeof(FusedShared<256, 4096, 256, 1024, 1024>), st>>>(
+                x, npts, S, q, c, out, kvec, list, list_n);
+        } else if (npts <= 32768) {
             k_ps_fused<256, 4096, 1, 4096, 2048, 1024><<<(unsigned)nseg, 256, sizeof(FusedShared<256, 4096, 4096, 2048, 1024>), st>>>(
                 x, npts, S, q, c, out, kvec, list, list_n);
         } else if (npts <= (int64_t(1) << 17)) {
