@@ -3,9 +3,11 @@
 Public surface of pkg/src/mxfft/fftcore.py:32-353 (ModeSpec, FftPlan,
 make_plan, butterfly_mx, fft_1d, fft_1d_fp16, fft_2d, plus the private
 _fft_batch / _encode_blocks_batch / _mx_multiply_batch the reference tests
-import).  The MX transform is the hand-written sm_100a kernel behind
-mxfft_fft_rows / mxfft_fft2 (csrc/mxfft_fft.cu); this module only validates
-arguments, builds plans and moves data.
+import).  Every ModeSpec kind runs in hand-written sm_100a kernels: MX behind
+mxfft_fft_rows / mxfft_fft2 (csrc/mxfft_lines.cuh, csrc/mxfft_fft.cu), fp16
+and reference behind mxfft_fft_rows_fp16 / mxfft_fft_rows_f64
+(csrc/mxfft_modes.cu).  This module validates arguments, builds plans and
+moves data.
 
 The device-resident batched entry points (fft2_device, fft_rows_device) take
 and return CUDA tensors without synchronizing; the numpy-facing functions are
@@ -204,7 +206,8 @@ def fast_path_supported(plan: FftPlan) -> bool:
 def _require_mx(plan: FftPlan):
     if plan.mode.kind != "mx":
         raise NotImplementedError(
-            f"{plan.mode.kind!r} mode has no GPU kernel in this build (MX mode only)")
+            f"the batched device entry points take MX plans; {plan.mode.kind!r} plans run through "
+            "_fft_batch / fft_1d / fft_2d (mxfft_fft_rows_fp16 / mxfft_fft_rows_f64)")
 
 
 def fft_rows_device(x, plan: FftPlan, inverse: bool = False, out=None):
