@@ -12,10 +12,12 @@ from paper_2512_04317_b200 import _native  # noqa: E402
 from paper_2512_04317_b200.workloads import ellipse_kspace_device  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
-x = ellipse_kspace_device(n, 7) * (2.0 ** -20)
+batch = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+x = torch.cat([ellipse_kspace_device(n, 7 + i) for i in range(batch)]) * (2.0 ** -20)
 plan = mx.make_plan(n, mx.ModeSpec.mx(mx.E4M3, 32))
 y = torch.empty_like(x)
-ws = torch.empty(int(_native.lib().mxfft_fft2_workspace_bytes(plan.handle, 1)), dtype=torch.uint8, device="cuda")
+ws = torch.empty(int(_native.lib().mxfft_fft2_workspace_bytes(plan.handle, batch)), dtype=torch.uint8,
+                 device="cuda")
 
 
 def t(fn, reps=5):
@@ -30,12 +32,13 @@ def t(fn, reps=5):
     return e0.elapsed_time(e1) / reps
 
 
-gb = n * n * 16 / 1e9
+gb = batch * n * n * 16 / 1e9
 for name, fn, npass in (("rows", lambda: mx.fft_rows_device(x, plan, False, out=y), 1),
-                        ("cols in place", lambda: mx.fftcore.fft_cols_device(x[None], plan, False, out=y[None]), 1),
-                        ("fft2 tstore", lambda: mx.fft2_device(x[None], plan, "forward", out=y[None], workspace=ws), 2),
-                        ("torch transpose", lambda: y.copy_(x.t()), 1),
+                        ("cols in place", lambda: mx.fftcore.fft_cols_device(x.view(batch, n, n), plan, False,
+                                                                            out=y.view(batch, n, n)), 1),
+                        ("fft2 (current)", lambda: mx.fft2_device(x.view(batch, n, n), plan, "forward",
+                                                                 out=y.view(batch, n, n), workspace=ws), 2),
                         ("mxfft transpose", lambda: _native.check(_native.lib().mxfft_transpose_c64(
-                            x.data_ptr(), y.data_ptr(), 1, n, _native.stream_handle())), 1)):
+                            x.data_ptr(), y.data_ptr(), batch, n, _native.stream_handle())), 1)):
     ms = t(fn) / npass
-    print(f"n={n} {name:16s} {ms:8.3f} ms/pass  {gb / ms * 1e3:7.0f} GB/s")
+    print(f"n={n} batch={batch} {name:16s} {ms:8.3f} ms/pass  {gb / ms * 1e3:7.0f} GB/s")
