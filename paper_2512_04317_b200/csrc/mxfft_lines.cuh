@@ -246,9 +246,11 @@ __device__ __forceinline__ void mxb(float2 (&u)[NB], float2 (&v)[NB], const unsi
     const float inv = exp2i(-ev);
     unsigned cv[NB];
     float pr[NB], pi[NB];
+    const float2 inv2 = make_float2(inv, inv);
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
-        cv[i] = q2h<ID>(v[i].x * inv, v[i].y * inv);
+        const float2 vs = __fmul2_rn(v[i], inv2);  // FMUL2: exact power-of-two scaling
+        cv[i] = q2h<ID>(vs.x, vs.y);
         cprod(w[i], cv[i], pr[i], pi[i]);
     }
     const float ap = pair_max<PAIR>(amax_2<NB>(pr, pi));
@@ -276,13 +278,17 @@ __device__ __forceinline__ void mxb(float2 (&u)[NB], float2 (&v)[NB], const unsi
     }
     const float fac = exp2i(-sh);
     const float sc = exp2i(E);
+    const float2 fac2 = make_float2(fac, fac), sc2 = make_float2(sc, sc);
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
-        const unsigned qp = q2h<ID>(pr[i] * fac, pi[i] * fac);
+        const float2 ps = __fmul2_rn(make_float2(pr[i], pi[i]), fac2);
+        const unsigned qp = q2h<ID>(ps.x, ps.y);
         const float qr = h_lo(qp), qi = h_hi(qp);
+        const float2 q = make_float2(qr, qi);
         const float2 uu = u[i];
-        u[i] = make_float2(__fmaf_rn(qr, sc, uu.x), __fmaf_rn(qi, sc, uu.y));
-        v[i] = make_float2(__fmaf_rn(-qr, sc, uu.x), __fmaf_rn(-qi, sc, uu.y));
+        // decode folded into the butterfly as two FFMA2: u +- q * 2^E
+        u[i] = __ffma2_rn(q, sc2, uu);
+        v[i] = __ffma2_rn(make_float2(-qr, -qi), sc2, uu);
         if (DBG) dbg_codes(*d, bfly0 + i, h_lo(cv[i]), h_hi(cv[i]), qr, qi);
     }
     if (DBG && ((bfly0 % d->cpb) == 0)) dbg_exps(*d, bfly0, ev, E, sh);
@@ -301,16 +307,18 @@ __device__ __forceinline__ bool trivial_block(float2 (&u)[NB], float2 (&v)[NB], 
     const int ev = am > 0.f ? floor_log2f(am) - F::EMAX : 0;
     if (!((ev >= -127) & (ev <= 126) & (ev >= Rg::ELO) & (ev <= Rg::EHI))) return false;
     const float inv = exp2i(-ev), sc = exp2i(ev);
+    const float2 inv2 = make_float2(inv, inv), sc2 = make_float2(sc, sc);
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
-        const unsigned cv = q2h<ID>(v[i].x * inv, v[i].y * inv);
+        const float2 vs = __fmul2_rn(v[i], inv2);
+        const unsigned cv = q2h<ID>(vs.x, vs.y);
         const float cr = h_lo(cv), ci = h_hi(cv);
         const bool rot = S == 1 && ((j0 + i) & 1);
         const float tr = rot ? sigma * ci : cr;
         const float ti = rot ? -sigma * cr : ci;
         const float2 uu = u[i];
-        u[i] = make_float2(__fmaf_rn(tr, sc, uu.x), __fmaf_rn(ti, sc, uu.y));
-        v[i] = make_float2(__fmaf_rn(-tr, sc, uu.x), __fmaf_rn(-ti, sc, uu.y));
+        u[i] = __ffma2_rn(make_float2(tr, ti), sc2, uu);
+        v[i] = __ffma2_rn(make_float2(-tr, -ti), sc2, uu);
         if (DBG) dbg_codes(*d, bfly0 + i, cr, ci, tr, ti);
     }
     if (DBG && ((bfly0 % d->cpb) == 0))
@@ -394,8 +402,9 @@ __device__ __forceinline__ void scale32(float2 (&x)[32], int e, bool& bad) {
     if (!DBG || (e >= -126 && e <= 127)) {
         bad |= !(e >= -126 && e <= 127);  // non-debug kernels replay the group
         const float f = exp2i(e);
+        const float2 f2 = make_float2(f, f);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) x[i] = make_float2(x[i].x * f, x[i].y * f);
+        for (int i = 0; i < 32; ++i) x[i] = __fmul2_rn(x[i], f2);
     } else {
         float2 t[32];
 #pragma unroll
