@@ -28,6 +28,12 @@
 #include "mxfft_generic.cuh"
 #include "mxfft_internal.h"
 
+#ifndef MXFFT_BATCH_STORE
+#define MXFFT_BATCH_STORE 0  // transposed stores: read the whole column run from shared memory first
+#endif
+#ifndef MXFFT_UNROLL_SMEM
+#define MXFFT_UNROLL_SMEM 0  // unroll the shared-memory stages of the n-specialised kernels
+#endif
 #ifndef MXFFT_LOCAL_STAGES
 #define MXFFT_LOCAL_STAGES 5  // unrolled register stages before the shared-memory loop
 #endif
@@ -113,6 +119,24 @@ __device__ __forceinline__ float h_lo(unsigned h) {
 }
 __device__ __forceinline__ float h_hi(unsigned h) {
     return __high2float(*reinterpret_cast<const __half2*>(&h));
+}
+
+// f16x2 -> two FP32 values (exact).  MXFFT_FHFMA_CVT=1 converts on the FMA pipe
+// as fma.rn.f32.f16(h, 1.0, -0.0) (FHFMA, full rate) instead of HADD2.F32 on the
+// half-rate ALU pipe, which the F2FP packs/unpacks and FMNMX3 already load.
+#ifndef MXFFT_FHFMA_CVT
+#define MXFFT_FHFMA_CVT 1
+#endif
+__device__ __forceinline__ void h2f2(unsigned h, float& lo, float& hi) {
+#if MXFFT_FHFMA_CVT
+    asm("{\n\t.reg .f16 l, u, one;\n\tmov.b32 {l, u}, %2;\n\tmov.b16 one, 0x3C00;\n\t"
+        "fma.rn.f32.f16 %0, l, one, 0f80000000;\n\tfma.rn.f32.f16 %1, u, one, 0f80000000;\n\t}"
+        : "=f"(lo), "=f"(hi)
+        : "r"(h));
+#else
+    lo = h_lo(h);
+    hi = h_hi(h);
+#endif
 }
 
 // exact mantissa-space complex product of packed f16 codes W = (wr, wi) and
@@ -283,7 +307,8 @@ __device__ __forceinline__ void mxb(float2 (&u)[NB], float2 (&v)[NB], const unsi
     for (int i = 0; i < NB; ++i) {
         const float2 ps = __fmul2_rn(make_float2(pr[i], pi[i]), fac2);
         const unsigned qp = q2h<ID>(ps.x, ps.y);
-        const float qr = h_lo(qp), qi = h_hi(qp);
+        float qr, qi;
+        h2f2(qp, qr, qi);
         const float2 q = make_float2(qr, qi);
         const float2 uu = u[i];
         // decode folded into the butterfly as two FFMA2: u +- q * 2^E
@@ -312,7 +337,8 @@ __device__ __forceinline__ bool trivial_block(float2 (&u)[NB], float2 (&v)[NB], 
     for (int i = 0; i < NB; ++i) {
         const float2 vs = __fmul2_rn(v[i], inv2);
         const unsigned cv = q2h<ID>(vs.x, vs.y);
-        const float cr = h_lo(cv), ci = h_hi(cv);
+        float cr, ci;
+        h2f2(cv, cr, ci);
         const bool rot = S == 1 && ((j0 + i) & 1);
         const float tr = rot ? sigma * ci : cr;
         const float ti = rot ? -sigma * cr : ci;
@@ -556,6 +582,14 @@ __device__ __forceinline__ void run_stages(float2 (&x)[32], int& U, int& V, cons
     // kept rolled: one copy of the stage body keeps the kernel inside the
     // instruction cache (unrolling measured slower)
     const int last = L.slim < lt + 5 ? L.slim : lt + 5;
+#if MXFFT_UNROLL_SMEM
+    if constexpr (LT >= 0 && !DBG) {
+#pragma unroll
+        for (int s = LOCAL; s < LT + 5; ++s)
+            if (s < last) smem_stage<ID, CPB, DBG>(x, U, V, L, rb, ebase, s, LT > 5, dbg, bad);
+        return;
+    }
+#endif
 #pragma unroll 1
     for (int s = LOCAL; s < last; ++s) smem_stage<ID, CPB, DBG>(x, U, V, L, rb, ebase, s, big, dbg, bad);
 }
@@ -794,9 +828,18 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
             if (gl < a.total_lines) {
                 const int64_t img = gl >> LN;
                 float2* dst = a.out + img * (int64_t)N * N + (int64_t)tq0 * N + (gl & (N - 1));
+#if MXFFT_BATCH_STORE
+                // all shared-memory reads first: each store then finds its data ready
+                float2 o[32];
+#pragma unroll
+                for (int k = 0; k < 32; ++k) o[k] = lds64(caddr(bcur, tch ^ dsw((T * k) >> 1), th ^ ((T * k) & 1)));
+#pragma unroll
+                for (int k = 0; k < 32; ++k) dst[(int64_t)k * T * N] = o[k];
+#else
 #pragma unroll
                 for (int k = 0; k < 32; ++k)
                     dst[(int64_t)k * T * N] = lds64(caddr(bcur, tch ^ dsw((T * k) >> 1), th ^ ((T * k) & 1)));
+#endif
             }
         }
     }

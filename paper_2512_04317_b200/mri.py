@@ -108,15 +108,93 @@ def pipeline_device(x, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, coil
     return y, k, res
 
 
-_HOST_PIPE = {}  # per device: (streams, events) of pipeline_host
+_HOST_PIPE = {}  # per device: the three streams of pipeline_host
+
+# device staging budget of pipeline_host: batches up to this size get whole-batch
+# device buffers (no ring back-pressure between the copy streams and compute)
+HOST_PIPE_DEVICE_BYTES = 16 << 30
+
+
+def host_slices(nstack: int, chunks: int):
+    """Slice sizes (in coil stacks) for pipeline_host: `chunks` slices with
+    weights 1, 2, 4, 4, ..., 4.  Nothing overlaps the first H2D, so it is short;
+    after it, H2D and D2H run at the same rate, so a slice no larger than the
+    lead the D2H stream starts with is ready (copied in and transformed) by the
+    time the D2H stream reaches it.  Sizes sum to nstack; none is empty."""
+    chunks = max(1, min(chunks, nstack))
+    w = [min(4, 2 ** i) for i in range(chunks)]
+    tot = float(sum(w))
+    sizes = [max(1, int(nstack * wi / tot)) for wi in w]
+    # hand the rounding remainder to the largest (middle) slices
+    d = nstack - sum(sizes)
+    order = sorted(range(chunks), key=lambda j: -w[j])
+    j = 0
+    while d != 0:
+        k = order[j % chunks]
+        if d > 0:
+            sizes[k] += 1
+            d -= 1
+        elif sizes[k] > 1:
+            sizes[k] -= 1
+            d += 1
+        j += 1
+    return sizes
+
+
+_HOST_GRAPHS = {}  # (device, buffers, shape, plan, cfg, ...) -> captured pipeline_host step
+_HOST_GRAPHS_MAX = 4
 
 
 def pipeline_host(x_host, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, out_host=None,
-                  coils: int = 1, chunks: int = 8):
-    """pipeline_device for a batch that lives in (pinned) host memory: the batch
-    is cut into `chunks` slices of whole coil stacks; slice i+1 is copied in on
-    one stream while slice i is transformed on another and slice i-1 is copied
-    out on a third (PCIe is full duplex).  Two device buffers ping-pong.
+                  coils: int = 1, chunks: int = 8, graph: bool = True):
+    """pipeline_device for a batch in (pinned) host memory -- see
+    _pipeline_host_eager for the slicing and stream overlap.
+
+    With graph=True and pinned buffers, the whole step (every H2D slice, the
+    kernels, every D2H slice, on three streams) is captured once per
+    (buffers, shape, plan, cfg, roundtrip, coils, chunks) as a CUDA graph and
+    replayed on later calls: the copies still run every call (the graph's
+    memcpy nodes read and write the caller's host buffers at replay time), but
+    the host no longer spends ~0.1 ms of Python per slice enqueueing them."""
+    import torch
+
+    if x_host.is_cuda or x_host.dtype != torch.complex64:
+        raise TypeError("pipeline_host takes a host complex64 tensor")
+    if out_host is None:
+        out_host = torch.empty(x_host.shape, dtype=x_host.dtype).pin_memory()
+    if not (graph and x_host.is_pinned() and out_host.is_pinned() and x_host.shape[0] > 0
+            and x_host.is_contiguous() and out_host.is_contiguous()):
+        return _pipeline_host_eager(x_host, plan, cfg, roundtrip, out_host, coils, chunks)
+    dev = torch.cuda.current_device()
+    key = (dev, x_host.data_ptr(), out_host.data_ptr(), tuple(x_host.shape), id(plan), plan.n,
+           repr(cfg), bool(roundtrip), int(coils), int(chunks))
+    ent = _HOST_GRAPHS.get(key)
+    if ent is None or ent[1] is not plan:
+        _pipeline_host_eager(x_host, plan, cfg, roundtrip, out_host, coils, chunks)  # warm-up
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(g, stream=cs):
+            _pipeline_host_eager(x_host, plan, cfg, roundtrip, out_host, coils, chunks, capture=True)
+        if len(_HOST_GRAPHS) >= _HOST_GRAPHS_MAX:
+            _HOST_GRAPHS.pop(next(iter(_HOST_GRAPHS)))
+        ent = (g, plan)
+        _HOST_GRAPHS[key] = ent
+    ent[0].replay()
+    torch.cuda.current_stream().synchronize()
+    return out_host
+
+
+def _pipeline_host_eager(x_host, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, out_host=None,
+                         coils: int = 1, chunks: int = 8, capture: bool = False):
+    """pipeline_device for a batch that lives in (pinned) host memory.
+
+    The batch is cut into `chunks` slices of whole coil stacks (host_slices:
+    a short first slice, then equal ones).  Three streams: slice i+1
+    is copied in while slice i is transformed and slice i-1 is copied out (PCIe
+    is full duplex).  Batches up to HOST_PIPE_DEVICE_BYTES are staged in
+    whole-batch device buffers, so the H2D stream never waits for compute or
+    D2H; larger batches cycle through two slice-sized buffers.
     x_host: CPU complex64 (B*coils, N, N), pinned for overlap.  Returns
     out_host (allocated pinned if None) once every copy has finished."""
     import torch
@@ -125,47 +203,66 @@ def pipeline_host(x_host, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, o
         raise TypeError("pipeline_host takes a host complex64 tensor")
     n = plan.n
     nstack = x_host.shape[0] // coils
-    chunks = max(1, min(chunks, nstack))
-    per = (nstack + chunks - 1) // chunks * coils  # images per slice
     if out_host is None:
         out_host = torch.empty(x_host.shape, dtype=x_host.dtype).pin_memory()
+    if nstack == 0:
+        return out_host
+    sizes = host_slices(nstack, chunks)
     dev = torch.device("cuda", torch.cuda.current_device())
     key = str(dev)
     if key not in _HOST_PIPE:
         _HOST_PIPE[key] = [torch.cuda.Stream(dev) for _ in range(3)]
     s_in, s_cmp, s_out = _HOST_PIPE[key]
     cur = torch.cuda.current_stream(dev)
-    xb = [torch.empty((per, n, n), dtype=torch.complex64, device=dev) for _ in range(2)]
-    yb = [torch.empty((per, n, n), dtype=torch.complex64, device=dev) for _ in range(2)]
-    kb = [torch.empty(per // coils, dtype=torch.int32, device=dev) for _ in range(2)]
-    ev_in = [torch.cuda.Event() for _ in range(2)]
-    ev_cmp = [torch.cuda.Event() for _ in range(2)]
-    ev_out = [torch.cuda.Event() for _ in range(2)]
+    whole = 2 * x_host.numel() * 8 <= HOST_PIPE_DEVICE_BYTES
+    if whole:
+        xb = [torch.empty(x_host.shape, dtype=torch.complex64, device=dev)]
+        yb = [torch.empty(x_host.shape, dtype=torch.complex64, device=dev)]
+        kb = [torch.empty(nstack, dtype=torch.int32, device=dev)]
+    else:
+        per = max(sizes) * coils
+        xb = [torch.empty((per, n, n), dtype=torch.complex64, device=dev) for _ in range(2)]
+        yb = [torch.empty((per, n, n), dtype=torch.complex64, device=dev) for _ in range(2)]
+        kb = [torch.empty(per // coils, dtype=torch.int32, device=dev) for _ in range(2)]
+    nb = len(xb)
+    ev_cmp = [None] * nb
+    ev_out = [None] * nb
     for s in (s_in, s_cmp, s_out):
         s.wait_stream(cur)  # buffers were allocated on the current stream
-    for i, start in enumerate(range(0, x_host.shape[0], per)):
-        b = i & 1
-        m = min(per, x_host.shape[0] - start)
-        if i >= 2:
-            s_in.wait_event(ev_cmp[b])  # slice i-2 no longer reads xb[b]
+    start = 0
+    for i, sz in enumerate(sizes):
+        b = i % nb
+        m = sz * coils
+        if whole:
+            xs, ys, ks = xb[0][start:start + m], yb[0][start:start + m], kb[0][start // coils:start // coils + sz]
+        else:
+            xs, ys, ks = xb[b][:m], yb[b][:m], kb[b][:sz]
+            if ev_cmp[b] is not None:
+                s_in.wait_event(ev_cmp[b])  # slice i-2 no longer reads xb[b]
         with torch.cuda.stream(s_in):
-            xb[b][:m].copy_(x_host[start:start + m], non_blocking=True)
-            ev_in[b].record(s_in)
-        s_cmp.wait_event(ev_in[b])
-        if i >= 2:
+            xs.copy_(x_host[start:start + m], non_blocking=True)
+            e_in = torch.cuda.Event()
+            e_in.record(s_in)
+        s_cmp.wait_event(e_in)
+        if not whole and ev_out[b] is not None:
             s_cmp.wait_event(ev_out[b])  # slice i-2 has left yb[b]
         with torch.cuda.stream(s_cmp):
-            pipeline_device(xb[b][:m], plan, cfg, roundtrip, coils=coils, out=yb[b][:m], k=kb[b][:m // coils])
+            pipeline_device(xs, plan, cfg, roundtrip, coils=coils, out=ys, k=ks)
+            ev_cmp[b] = torch.cuda.Event()
             ev_cmp[b].record(s_cmp)
         s_out.wait_event(ev_cmp[b])
         with torch.cuda.stream(s_out):
-            out_host[start:start + m].copy_(yb[b][:m], non_blocking=True)
+            out_host[start:start + m].copy_(ys, non_blocking=True)
+            ev_out[b] = torch.cuda.Event()
             ev_out[b].record(s_out)
+        start += m
     for t in xb + yb + kb:
         for s in (s_in, s_cmp, s_out):
             t.record_stream(s)
-    cur.wait_stream(s_out)
-    s_out.synchronize()
+    for s in (s_in, s_cmp, s_out):
+        cur.wait_stream(s)
+    if not capture:
+        s_out.synchronize()
     return out_host
 
 
