@@ -28,6 +28,9 @@
 #include "mxfft_generic.cuh"
 #include "mxfft_internal.h"
 
+#ifndef MXFFT_PAIR_STORE
+#define MXFFT_PAIR_STORE 1  // strided copy-out: two adjacent lines per thread, 16-byte stores
+#endif
 #ifndef MXFFT_BATCH_STORE
 #define MXFFT_BATCH_STORE 0  // transposed stores: read the whole column run from shared memory first
 #endif
@@ -724,6 +727,12 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
     const int te0 = belem(tj, tq0);
     const int tch = dsw(te0 >> 1);
     const int th = te0 & 1;
+#if MXFFT_PAIR_STORE
+    // paired strided stores: lines 2 pa, 2 pa + 1 of the group, positions pq0 + 2 T k
+    const int pa = tid & ((LPC >> 1) - 1), pq0 = tid >> (LLPC > 0 ? LLPC - 1 : 0);
+    const int pe0 = belem(2 * pa, pq0), pe1 = belem(2 * pa + 1, pq0);
+    const int pch0 = dsw(pe0 >> 1), ph0 = pe0 & 1, pch1 = dsw(pe1 >> 1), ph1 = pe1 & 1;
+#endif
     // contiguous access: chunk tid + NT k
     const int rch = dsw(tid);
     const bool strided_out = a.col_mode || a.tstore;
@@ -823,6 +832,20 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
                     dst[NT * k] = make_float4(p0.x, p0.y, p1.x, p1.y);
                 }
             }
+#if MXFFT_PAIR_STORE
+        } else if (LT >= 0 && LT <= 3 && (grp + 1) * LPC <= a.total_lines) {  // n <= 256 (n = 512: slower)
+            // two adjacent output columns per thread: one 16-byte store per position
+            const int64_t gl = grp * LPC + 2 * pa;
+            const int64_t img = gl >> LN;
+            float4* dst = reinterpret_cast<float4*>(a.out + img * (int64_t)N * N + (int64_t)pq0 * N + (gl & (N - 1)));
+            const int64_t rs = (int64_t)T * N;  // 2 T rows, in float4 units
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const float2 v0 = lds64(caddr(bcur, pch0 ^ dsw(T * k), ph0));
+                const float2 v1 = lds64(caddr(bcur, pch1 ^ dsw(T * k), ph1));
+                dst[k * rs] = make_float4(v0.x, v0.y, v1.x, v1.y);
+            }
+#endif
         } else {  // columns, or rows stored transposed: line gl -> column (gl mod n) of image gl/n
             const int64_t gl = grp * LPC + tj;
             if (gl < a.total_lines) {
