@@ -58,6 +58,12 @@ constexpr int64_t FUSED_MAX = int64_t(1) << 18;
 #ifndef MXFFT_C3_CLUSTER
 #define MXFFT_C3_CLUSTER 1  // 2-CTA clusters when few large segments leave SMs idle
 #endif
+#ifndef MXFFT_PS_PREFETCH
+#define MXFFT_PS_PREFETCH 4  // lean statistics: stream rounds prefetched into L2 ahead of the loads
+#endif
+#ifndef MXFFT_PS_LEAN
+#define MXFFT_PS_LEAN 1  // k_ps_lean for segments of 2^13 .. 2^17 points
+#endif
 #ifndef MXFFT_FUSED_MIN_SEG
 #define MXFFT_FUSED_MIN_SEG 32  // fewer segments: the grid-wide path
 #endif
@@ -874,6 +880,456 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_ps_fused(const float2* __rest
     if (tid == 0) finish_result(c, a_max, p_tau, nnz, out, kvec, seg);
 }
 
+// ---------------------------------------------------------------------------
+// Lean fused statistics, one CTA per segment (C2 / C4 image sizes).  Same
+// result contract and exactness argument as k_ps_fused; three changes make it
+// issue-light:
+//  * bracket: a 2048-bin histogram of the sample keys (bin = key bits >> 20,
+//    1/8 binade of the key) instead of sorting the sample: lo / hi are the
+//    edges of the bins holding sample ranks ilo / ihi (so the bracket only
+//    widens), lo never drops below the sample minimum's bin edge / 2^8;
+//  * stream: per point a squared-magnitude key, an exact zero test, an
+//    integer "below lo" count and one "rare" test (bracket or peak); rare
+//    points go to a per-thread shared-memory list with a predicated store --
+//    no branch, no atomic on the hot loop;
+//  * select: candidate bins span [min candidate key, hi], so the exact
+//    window (np.abs in FP64) is a few dozen points and counted ranks pick
+//    the order statistics.
+// Anything that does not settle (list overflow, ranks outside the bracket,
+// selected values within key rounding of a window edge, extreme / non-finite
+// keys) sends the segment to the exact fallback list, as before.
+// ---------------------------------------------------------------------------
+constexpr int LB_BINS = 2048;  // sample histogram: key >> 20
+
+template <int NT, int K, int WC, int OV>
+struct LeanShared {
+    union {
+        struct {
+            unsigned hist[LB_BINS];
+        } s;  // sample phase
+        struct {
+            unsigned hist[NBIN];
+            double w[WC];
+        } q;  // select phase
+    } u;
+    float2 buf[(K + 8) * NT];  // per-thread rare lists, entry k of thread t at k * NT + t; rows >= K: sink
+    float2 ovf[OV];      // shared spill for threads whose list is full
+    unsigned warp_a[NT / 32], warp_b[NT / 32], warp_c[NT / 32];
+    unsigned long long amax_b;
+    unsigned snz, smax, wn, flags, kmin, novf;
+    int bsel[3];
+    double wsel[3];
+    float lo, hi, top;
+    int bt, bt1;
+    unsigned woff, wend;
+};
+
+// block-wide sum of three counters (all threads get the totals)
+template <int NT>
+__device__ __forceinline__ void block_sum3(unsigned& a, unsigned& b, unsigned& c, unsigned* wa, unsigned* wb,
+                                           unsigned* wc) {
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    for (int o = 16; o; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    __syncthreads();
+    if (lane == 0) {
+        wa[wp] = a;
+        wb[wp] = b;
+        wc[wp] = c;
+    }
+    __syncthreads();
+    a = b = c = 0;
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) {
+        a += wa[i];
+        b += wb[i];
+        c += wc[i];
+    }
+}
+
+template <int NT, int K, int WC, int OV>
+__global__ void __launch_bounds__(NT, 1024 / NT)
+    k_ps_lean(const float2* __restrict__ xall, int64_t npts, int S, double q, mxfft_prescale_cfg c,
+              mxfft_prescale_result* out, int32_t* kvec, int* list, int* list_n) {
+#ifdef PS_TIMING
+    long long T0 = clock64(), TL[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define PL_T(i) if (threadIdx.x == 0) TL[i] = clock64() - T0;
+#else
+#define PL_T(i)
+#endif
+    using Shared = LeanShared<NT, K, WC, OV>;
+    extern __shared__ unsigned long long lean_smem[];
+    Shared& F = *reinterpret_cast<Shared*>(lean_smem);
+    const int seg = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+    const float2* x = xall + (int64_t)seg * npts;
+    constexpr unsigned HUGEB = 0x7e800000u;  // key 2^126: beyond it the segment goes to the exact kernel
+
+    // the stream's first rounds head for L2 while the sample is drawn
+    constexpr int PF = MXFFT_PS_PREFETCH;  // rounds of look-ahead (bulk L2 prefetch, one thread)
+    constexpr unsigned RB = NT * 4 * 16;   // bytes per stream round
+    const int nrounds_pf = (int)(npts * 8 / RB);
+    if (tid == 0)
+        for (int r = 0; r < PF && r < nrounds_pf; ++r)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(x) + (size_t)r * RB),
+                         "n"(RB)
+                         : "memory");
+    // ---- sample -> histogram bracket ----
+    for (int i = tid; i < LB_BINS; i += NT) F.u.s.hist[i] = 0;
+    if (tid == 0) {
+        F.snz = 0;
+        F.smax = 0;
+        F.wn = 0;
+        F.flags = 0;
+        F.kmin = 0xffffffffu;
+        F.novf = 0;
+        F.amax_b = 0;
+        F.bsel[0] = F.bsel[1] = F.bsel[2] = -1;
+    }
+    __syncthreads();
+    {
+        const int64_t nsec = npts / 4;
+        unsigned cnt = 0, mx = 0, mn = 0xffffffffu;
+        // all of this thread's sample sectors are requested before any is used
+        constexpr int SPT = 4;  // sectors per thread per batch (S <= 4 * 4 * NT)
+        for (int j0 = tid; j0 < S / 4; j0 += SPT * NT) {
+            float4 sa[SPT], sb[SPT];
+#pragma unroll
+            for (int u = 0; u < SPT; ++u) {
+                const int j = j0 + u * NT;
+                const uint64_t h = (uint64_t)j * 2654435761ull;
+                const uint64_t sec = (nsec & (nsec - 1)) == 0 ? (h & (uint64_t)(nsec - 1)) : h % (uint64_t)nsec;
+                const float4* p = reinterpret_cast<const float4*>(x + sec * 4);
+                if (j < S / 4) {
+                    sa[u] = __ldg(p);
+                    sb[u] = __ldg(p + 1);
+                } else {
+                    sa[u] = sb[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+#pragma unroll
+          for (int u = 0; u < SPT; ++u) {
+            const float4 a = sa[u], b = sb[u];
+            const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int hh = 0; hh < 4; ++hh) {
+                const float re = v[2 * hh], im = v[2 * hh + 1];
+                const float m = fmaxf(fabsf(re), fabsf(im));
+                if (m > 0.f) {
+                    const float sk = (m >= 0x1p-60f && m <= 0x1p60f) ? skey(re, im) : (m < 1.f ? 0.f : 0x1p125f);
+                    const unsigned k = __float_as_uint(sk);
+                    atomicAdd(&F.u.s.hist[k >> 20], 1u);
+                    mx = max(mx, k);
+                    mn = min(mn, k);
+                    ++cnt;
+                }
+            }
+          }
+        }
+        for (int o = 16; o; o >>= 1) {
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        }
+        if (lane == 0) {
+            atomicAdd(&F.snz, cnt);
+            atomicMax(&F.smax, mx);
+            atomicMin(&F.kmin, mn);  // (reused: sample minimum here)
+        }
+    }
+    __syncthreads();
+    PL_T(0)
+    {
+        const int n = (int)F.snz;
+        const double rs = (double)(n - 1) * q;
+        const int d = 8 + (int)(4.0 * sqrt(rs + 1.0));
+        const int ilo = (int)floor(rs) - d, ihi = (int)ceil(rs) + 1 + d;
+        // exclusive scan of the 2048 bins, B consecutive bins per thread
+        constexpr int B = LB_BINS / NT;
+        unsigned hv[B], tot = 0;
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            hv[i] = F.u.s.hist[tid * B + i];
+            tot += hv[i];
+        }
+        unsigned incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) F.warp_a[tid >> 5] = incl;
+        __syncthreads();
+        unsigned base = incl - tot;
+        for (int w = 0; w < (tid >> 5); ++w) base += F.warp_a[w];
+        const int want[2] = {ilo, ihi};
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int rk = want[r];
+            if (rk >= 0 && rk < n && (unsigned)rk >= base && (unsigned)rk < base + tot) {
+                unsigned e = base;
+#pragma unroll
+                for (int i = 0; i < B; ++i) {
+                    if ((unsigned)rk >= e && (unsigned)rk < e + hv[i]) F.bsel[r] = tid * B + i;
+                    e += hv[i];
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            if (n == 0) {
+                F.lo = 0x1p-126f;  // no nonzero sample: everything nonzero is a candidate (-> fallback)
+                F.hi = __int_as_float(0x7f800000);
+                F.top = __int_as_float(0x7f800000);
+            } else {
+                // lo > 0 always (zeros, key 0, are then never rare)
+                unsigned lob;
+                if (ilo > 0) {
+                    lob = (unsigned)F.bsel[0] << 20;
+                } else {
+                    const unsigned e = (F.kmin >> 20) << 20;
+                    lob = e > (8u << 23) ? e - (8u << 23) : 0u;
+                }
+                F.lo = __uint_as_float(lob > 1u ? lob : 1u);
+                F.hi = ihi < n ? __uint_as_float((((unsigned)F.bsel[1] + 1u) << 20) - 1u) : __int_as_float(0x7f800000);
+                F.top = __uint_as_float(F.smax) * (1.f - 0x1p-20f);
+            }
+            F.kmin = 0xffffffffu;
+        }
+        __syncthreads();
+    }
+    const unsigned lob = __float_as_uint(F.lo), hib = __float_as_uint(F.hi), topb = __float_as_uint(F.top);
+    const unsigned rng = hib - lob;
+    PL_T(1)
+
+    // ---- stream: counts + per-thread rare lists ----
+    // npts is a multiple of 2 * NT * U (dispatch), so rounds need no bounds checks.
+    // A thread's list has K rows plus 2U sink rows: a round appends at most 2U
+    // entries, and a round that crosses row K spills its late entries.
+    unsigned nzero = 0, below_all = 0;
+    constexpr int U = 4;
+    const unsigned row0 = (unsigned)__cvta_generic_to_shared(&F.buf[tid]);
+    unsigned wa = row0;  // next free row of this thread's list
+    {
+        const int nrounds = (int)(npts / (2 * NT * U));
+        const float4* x4 = reinterpret_cast<const float4*>(x) + tid;
+        float4 vn[U];
+#pragma unroll
+        for (int it = 0; it < U; ++it) vn[it] = __ldg(x4 + it * NT);
+        for (int r = 0; r < nrounds; ++r) {
+            if (tid == 0 && r + PF < nrounds)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                 reinterpret_cast<const char*>(x) + (size_t)(r + PF) * RB),
+                             "n"(RB)
+                             : "memory");
+            float4 v[U];
+#pragma unroll
+            for (int it = 0; it < U; ++it) v[it] = vn[it];
+            if (r + 1 < nrounds) {
+#pragma unroll
+                for (int it = 0; it < U; ++it) vn[it] = __ldg(x4 + (r + 1) * (NT * U) + it * NT);
+            }
+            const unsigned wa0 = wa;
+#pragma unroll
+            for (int it = 0; it < U; ++it) {
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const float re = hh ? v[it].z : v[it].x, im = hh ? v[it].w : v[it].y;
+                    const unsigned kb = __float_as_uint(skey(re, im));
+                    const unsigned z = (__float_as_uint(re) | __float_as_uint(im)) & 0x7fffffffu;
+                    const unsigned d = kb - lob;
+                    nzero += (z - 1u) >> 31;   // z == 0
+                    below_all += d >> 31;      // kb < lob (keys and lob are < 2^31; NaN keys are flagged)
+                    asm volatile(
+                        "{\n\t.reg .pred p, q;\n\t"
+                        "setp.le.u32 p, %1, %2;\n\t"
+                        "setp.ge.u32 q, %3, %4;\n\t"
+                        "or.pred p, p, q;\n\t"
+                        "@p st.shared.v2.f32 [%0], {%5, %6};\n\t"
+                        "@p add.u32 %0, %0, %7;\n\t}"
+                        : "+r"(wa)
+                        : "r"(d), "r"(rng), "r"(kb), "r"(topb), "f"(re), "f"(im), "n"(NT * 8)
+                        : "memory");
+                }
+            }
+            if (wa >= row0 + (unsigned)(K * NT * 8)) {  // list full: spill this round's entries past row K
+                unsigned w2 = wa0;
+#pragma unroll
+                for (int it = 0; it < U; ++it) {
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const float re = hh ? v[it].z : v[it].x, im = hh ? v[it].w : v[it].y;
+                        const unsigned kb = __float_as_uint(skey(re, im));
+                        if ((kb - lob <= rng) | (kb >= topb)) {
+                            if (w2 >= row0 + (unsigned)(K * NT * 8)) {
+                                const unsigned o = atomicAdd(&F.novf, 1u);
+                                if (o < (unsigned)OV) F.ovf[o] = make_float2(re, im);
+                            }
+                            w2 += NT * 8;
+                        }
+                    }
+                }
+                wa = row0 + (unsigned)(K * NT * 8);  // later rounds spill everything
+            }
+        }
+    }
+    const unsigned nr = (wa - row0) / (unsigned)(NT * 8);
+
+    // ---- select ----
+    __syncthreads();
+    PL_T(2)
+    const unsigned nsp = F.novf < (unsigned)OV ? F.novf : (unsigned)OV;
+    const unsigned nmine = nr < (unsigned)K ? nr : (unsigned)K;  // (nr <= K: later entries were spilled)
+    const unsigned nall = nmine + (nsp > (unsigned)tid ? (nsp - 1 - tid) / NT + 1 : 0u);
+    // entry e of this thread: its own list, then a strided share of the spill
+    auto entry = [&](unsigned e) { return e < nmine ? F.buf[e * NT + tid] : F.ovf[tid + (e - nmine) * NT]; };
+    // classify: candidates, peak, extreme
+    unsigned ncand = 0, flg = F.novf > (unsigned)OV ? 1u : 0u, kmn = 0xffffffffu;
+    unsigned long long am = 0;
+    for (unsigned e = 0; e < nall; ++e) {
+        const float2 v = entry(e);
+        const unsigned kb = __float_as_uint(skey(v.x, v.y));
+        if (kb >= HUGEB) flg = 1;
+        if (kb - lob <= rng) {
+            ++ncand;
+            kmn = min(kmn, kb);
+        }
+        if (kb >= topb) am = max(am, (unsigned long long)__double_as_longlong(np_cabs_f((double)v.x, (double)v.y)));
+    }
+    for (int o = 16; o; o >>= 1) {
+        am = max(am, __shfl_xor_sync(0xffffffffu, am, o));
+        kmn = min(kmn, __shfl_xor_sync(0xffffffffu, kmn, o));
+    }
+    if (lane == 0) {
+        atomicMax(&F.amax_b, am);
+        atomicMin(&F.kmin, kmn);
+    }
+    unsigned ntop_any = am != 0 ? 1u : 0u;
+    block_sum3<NT>(nzero, below_all, ncand, F.warp_a, F.warp_b, F.warp_c);
+    unsigned fl = flg, tp = ntop_any, dummy = 0;
+    block_sum3<NT>(fl, tp, dummy, F.warp_a, F.warp_b, F.warp_c);
+    PL_T(3)
+    const unsigned long long nnz = (unsigned long long)npts - nzero;
+    const unsigned below = below_all - nzero;  // lo > 0: every zero counted below
+    if (fl) {
+        if (tid == 0) fail_seg(list, list_n, seg);
+        return;
+    }
+    double a_max = 0.0, p_tau = 0.0;
+    if (nnz > 0) {
+        const double virt = __dmul_rn((double)(nnz - 1), q);
+        unsigned long long r_lo, r_hi;
+        double gamma;
+        if (virt >= (double)(nnz - 1)) {
+            r_lo = r_hi = nnz - 1;
+            gamma = __dadd_rn(virt, 1.0);
+        } else {
+            r_lo = (unsigned long long)floor(virt);
+            r_hi = r_lo + 1;
+            gamma = __dsub_rn(virt, (double)r_lo);
+        }
+        const unsigned nc = ncand;
+        if (!(tp >= 1 && below <= r_lo && r_hi < below + nc)) {
+            if (tid == 0) fail_seg(list, list_n, seg);
+            return;
+        }
+        const unsigned t = (unsigned)(r_lo - below), t1 = (unsigned)(r_hi - below);
+        const unsigned klo = F.kmin;  // smallest candidate key
+        const float inv = (float)NBIN / ((float)(hib - klo) + 1.f);
+        for (int i = tid; i < NBIN; i += NT) F.u.q.hist[i] = 0;
+        __syncthreads();
+        for (unsigned e = 0; e < nall; ++e) {
+            const float2 v = entry(e);
+            const unsigned kb = __float_as_uint(skey(v.x, v.y));
+            if (kb - lob <= rng) atomicAdd(&F.u.q.hist[kbin(kb, klo, inv)], 1u);
+        }
+        __syncthreads();
+        {  // exclusive scan of the candidate histogram
+            constexpr int B = NBIN / NT > 0 ? NBIN / NT : 1;
+            const bool has = tid * B < NBIN;
+            unsigned hv[B], tot = 0;
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                hv[i] = has ? F.u.q.hist[tid * B + i] : 0u;
+                tot += hv[i];
+            }
+            unsigned incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) F.warp_a[tid >> 5] = incl;
+            __syncthreads();
+            unsigned e = incl - tot;
+            for (int w = 0; w < (tid >> 5); ++w) e += F.warp_a[w];
+            if (has) {
+#pragma unroll
+                for (int i = 0; i < B; ++i) {
+                    if (e <= t && t < e + hv[i]) F.bt = tid * B + i;
+                    if (e <= t1 && t1 < e + hv[i]) F.bt1 = tid * B + i;
+                    e += hv[i];
+                }
+            }
+            __syncthreads();
+            const int wlo = F.bt > 0 ? F.bt - 1 : 0, whi = F.bt1 < NBIN - 1 ? F.bt1 + 1 : NBIN - 1;
+            e = incl - tot;
+            for (int w = 0; w < (tid >> 5); ++w) e += F.warp_a[w];
+            if (has) {
+#pragma unroll
+                for (int i = 0; i < B; ++i) {
+                    if (tid * B + i == wlo) F.woff = e;
+                    if (tid * B + i == whi) F.wend = e + hv[i];
+                    e += hv[i];
+                }
+            }
+        }
+        __syncthreads();
+        const int wlo = F.bt > 0 ? F.bt - 1 : 0, whi = F.bt1 < NBIN - 1 ? F.bt1 + 1 : NBIN - 1;
+        const unsigned woff = F.woff, wcount = F.wend - F.woff;
+        if (wcount > (unsigned)WC) {
+            if (tid == 0) fail_seg(list, list_n, seg);
+            return;
+        }
+        PL_T(4)
+        for (unsigned e = 0; e < nall; ++e) {
+            const float2 v = entry(e);
+            const unsigned kb = __float_as_uint(skey(v.x, v.y));
+            if (kb - lob <= rng) {
+                const int b = kbin(kb, klo, inv);
+                if (b >= wlo && b <= whi) F.u.q.w[atomicAdd(&F.wn, 1u)] = np_cabs_f((double)v.x, (double)v.y);
+            }
+        }
+        __syncthreads();
+        PL_T(5)
+        pick_two<double, NT, WC / NT>(F.u.q.w, (int)wcount, (int)(t - woff), (int)(t1 - woff), F.wsel);
+        PL_T(6)
+#ifdef PS_TIMING
+        if (tid == 0 && (seg == 0 || seg == 100))
+            printf("lean seg %d nc=%u wcount=%u spill=%u | bracket %lld stream0 %lld streamed %lld classified %lld hist %lld window %lld picked %lld\n",
+                   seg, nc, wcount, F.novf, TL[0], TL[1], TL[2], TL[3], TL[4], TL[5], TL[6]);
+#endif
+        const double vlo = F.wsel[0], vhi = F.wsel[1];
+        const float glo = __uint_as_float(lob), ghi = __uint_as_float(hib);
+        const float elo = wlo > 0 ? __uint_as_float(bin_lo(wlo, klo, inv)) : glo;
+        const float ehi = whi < NBIN - 1 ? __uint_as_float(bin_lo(whi + 1, klo, inv)) : ghi;
+        bool good = true;
+        if (elo > 0.f && !(elo >= 0x1p-100f && vlo * vlo > (double)elo * (1.0 + 0x1p-18))) good = false;
+        if (ehi <= FLT_MAX && !(vhi * vhi < (double)ehi * (1.0 - 0x1p-18))) good = false;
+        if (!good) {
+            if (tid == 0) fail_seg(list, list_n, seg);
+            return;
+        }
+        a_max = __longlong_as_double((long long)F.amax_b);
+        const double diff = __dsub_rn(vhi, vlo);
+        p_tau = gamma >= 0.5 ? __dsub_rn(vhi, __dmul_rn(diff, __dsub_rn(1.0, gamma)))
+                             : __dadd_rn(vlo, __dmul_rn(diff, gamma));
+    }
+    if (tid == 0) finish_result(c, a_max, p_tau, nnz, out, kvec, seg);
+}
+
 cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, double q,
                                  const mxfft_prescale_cfg& c, mxfft_prescale_result* out,
                                  int32_t* kvec, void* ws, int** list_out, int** list_n_out, cudaStream_t st) {
@@ -914,6 +1370,30 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
         }
         cudaError_t e = cudaMemsetAsync(list_n, 0, sizeof(int), st);
         if (e != cudaSuccess) return e;
+#if MXFFT_PS_LEAN
+        if (npts >= 8192 && npts <= (int64_t(1) << 17) && npts % (npts > 32768 ? 4096 : 2048) == 0) {
+            static bool lattr = false;
+            using L512 = LeanShared<512, 12, 1024, 1024>;
+            using L256 = LeanShared<256, 12, 1024, 1024>;
+            if (!lattr) {
+                e = cudaFuncSetAttribute(k_ps_lean<512, 12, 1024, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(L512));
+                if (e == cudaSuccess)
+                    e = cudaFuncSetAttribute(k_ps_lean<256, 12, 1024, 1024>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(L256));
+                if (e != cudaSuccess) return e;
+                lattr = true;
+            }
+            if (npts > 32768)
+                k_ps_lean<512, 12, 1024, 1024><<<(unsigned)nseg, 512, sizeof(L512), st>>>(x, npts, 4096, q, c, out, kvec,
+                                                                                     list, list_n);
+            else
+                k_ps_lean<256, 12, 1024, 1024><<<(unsigned)nseg, 256, sizeof(L256), st>>>(x, npts, 1024, q, c, out, kvec,
+                                                                                     list, list_n);
+            note_launch();
+            return cudaGetLastError();
+        }
+#endif
         const int S = fused_sample_size(npts);
         if (npts < 32768) {  // S = 256: small sample / window / peak buffers, 4 CTAs per SM
             k_ps_fused<256, 4096, 1, 256, 1024, 1024><<<(unsigned)nseg, 256, sizeof(FusedShared<256, 4096, 256, 1024, 1024>), st>>>(
