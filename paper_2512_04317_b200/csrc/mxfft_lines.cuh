@@ -333,7 +333,8 @@ __device__ __forceinline__ bool trivial_block(float2 (&u)[NB], float2 (&v)[NB], 
     using Rg = DecodeRange<F>;
     const float am = pair_max<PAIR>(amax_c<NB>(v));
     const int ev = am > 0.f ? floor_log2f(am) - F::EMAX : 0;
-    if (!((ev >= -127) & (ev <= 126) & (ev >= Rg::ELO) & (ev <= Rg::EHI))) return false;
+    const bool ok = (ev >= -127) & (ev <= 126) & (ev >= Rg::ELO) & (ev <= Rg::EHI);
+    if (DBG && !ok) return false;  // non-debug kernels finish branch-free and replay
     const float inv = exp2i(-ev), sc = exp2i(ev);
     const float2 inv2 = make_float2(inv, inv), sc2 = make_float2(sc, sc);
 #pragma unroll
@@ -352,7 +353,7 @@ __device__ __forceinline__ bool trivial_block(float2 (&u)[NB], float2 (&v)[NB], 
     }
     if (DBG && ((bfly0 % d->cpb) == 0))
         dbg_exps(*d, bfly0, ev, am > 0.f ? ev : -F::EMAX, am > 0.f ? F::EMAX : 0);
-    return true;
+    return ok;
 }
 
 // One register-resident stage S (half = 2^S <= 16) over the thread's 32 values.
@@ -378,10 +379,12 @@ __device__ __forceinline__ void local_stage(float2 (&x)[32], const unsigned* tw,
         const int j0 = (k * NB) & (half - 1);
         const int bfly0 = c * 16 + k * NB;
         if (S <= 1) {
-            bool done = trivial && trivial_block<ID, NB, PAIR, S, DBG>(ub, vb, j0, sigma, d, bfly0);
             if constexpr (!DBG) {
-                bad |= !done;
-            } else if (!done) {
+                // computed unconditionally (no join to merge registers at); a
+                // non-trivial plan or an out-of-range block replays the group
+                const bool done = trivial_block<ID, NB, PAIR, S, DBG>(ub, vb, j0, sigma, d, bfly0);
+                bad |= !(done & trivial);
+            } else if (!(trivial && trivial_block<ID, NB, PAIR, S, DBG>(ub, vb, j0, sigma, d, bfly0))) {
                 // exact out-of-line path (also covers plans whose stage-0/1
                 // twiddles are not exactly 1 / -i)
                 float2 tu[NB], tv[NB];
@@ -573,7 +576,11 @@ __device__ __forceinline__ void run_stages(float2 (&x)[32], int& U, int& V, cons
     const int lt = LT >= 0 ? LT : L.lt;
     const bool big = lt > 5;  // a line spans several warps
     constexpr int LOCAL = MXFFT_LOCAL_STAGES;  // unrolled register stages (4 or 5)
-    const int lim_loc = L.slim < LOCAL ? L.slim : LOCAL;
+    // n-specialised kernels always run every stage (stage-limited launches go to
+    // the LT = -1 variant): unconditional register stages leave the compiler no
+    // join points at which to shuffle the 32 values back into fixed registers
+    constexpr bool FULL = LT >= 0 && !DBG;
+    const int lim_loc = FULL ? LOCAL : (L.slim < LOCAL ? L.slim : LOCAL);
     if (lim_loc > 0) local_stage<ID, CPB, 0, DBG>(x, L.tw, L.twe, L.c, L.trivial, L.sigma, dbg, bad);
     if (lim_loc > 1) local_stage<ID, CPB, 1, DBG>(x, L.tw, L.twe, L.c, L.trivial, L.sigma, dbg, bad);
     if (lim_loc > 2) local_stage<ID, CPB, 2, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg, bad);
@@ -584,7 +591,7 @@ __device__ __forceinline__ void run_stages(float2 (&x)[32], int& U, int& V, cons
     V = U + 16;
     // kept rolled: one copy of the stage body keeps the kernel inside the
     // instruction cache (unrolling measured slower)
-    const int last = L.slim < lt + 5 ? L.slim : lt + 5;
+    const int last = FULL ? lt + 5 : (L.slim < lt + 5 ? L.slim : lt + 5);
 #if MXFFT_UNROLL_SMEM
     if constexpr (LT >= 0 && !DBG) {
 #pragma unroll
@@ -1013,7 +1020,7 @@ static cudaError_t disp_lt(const MxLinesArgs& a, size_t smem, cudaStream_t st) {
         return cudaErrorInvalidValue;
     }
     if constexpr (!DBG && CPB >= 8) {
-        if (a.col_mode) return launch_t<ID, CPB, DBG, -1, false>(a, smem, st);
+        if (a.col_mode || a.stage_limit < a.log2n) return launch_t<ID, CPB, DBG, -1, false>(a, smem, st);
         switch (a.log2T) {
             case 0: return launch_t<ID, CPB, DBG, 0, false>(a, smem, st);
             case 1: return launch_t<ID, CPB, DBG, 1, false>(a, smem, st);
