@@ -31,6 +31,9 @@
 #ifndef MXFFT_PAIR_STORE
 #define MXFFT_PAIR_STORE 1  // strided copy-out: two adjacent lines per thread, 16-byte stores
 #endif
+#ifndef MXFFT_PAIR_BATCH
+#define MXFFT_PAIR_BATCH 1  // paired strided copy-out: positions read from shared memory per batch of stores
+#endif
 #ifndef MXFFT_BATCH_STORE
 #define MXFFT_BATCH_STORE 0  // transposed stores: read the whole column run from shared memory first
 #endif
@@ -263,13 +266,22 @@ __device__ __forceinline__ float amax_2(const float (&a)[NB], const float (&b)[N
     return fmaxf(fmax3(m[0], m[1], m[2 % L]), m[3 % L]);
 }
 
+// floor(log2 am) for the block exponent.  Non-debug kernels read the biased
+// exponent field only: a subnormal am then yields -127, which puts ev below
+// the fast range, so the group is replayed exactly (replay_lines).
+template <bool DBG>
+__device__ __forceinline__ int flog2_hot(float am) {
+    if constexpr (DBG) return floor_log2f(am);
+    return (int)(__float_as_uint(am) >> 23) - 127;  // am >= 0
+}
+
 template <int ID, int NB, bool PAIR, bool DBG>
 __device__ __forceinline__ void mxb(float2 (&u)[NB], float2 (&v)[NB], const unsigned (&w)[NB],
                                     int ew, const LDbg* d, int bfly0, bool& bad) {
     using F = HwFmt<ID>;
     using Rg = DecodeRange<F>;
     const float am = pair_max<PAIR>(amax_c<NB>(v));
-    const int ev = am > 0.f ? floor_log2f(am) - F::EMAX : 0;
+    const int ev = am > 0.f ? flog2_hot<DBG>(am) - F::EMAX : 0;
     const float inv = exp2i(-ev);
     unsigned cv[NB];
     float pr[NB], pi[NB];
@@ -332,7 +344,7 @@ __device__ __forceinline__ bool trivial_block(float2 (&u)[NB], float2 (&v)[NB], 
     using F = HwFmt<ID>;
     using Rg = DecodeRange<F>;
     const float am = pair_max<PAIR>(amax_c<NB>(v));
-    const int ev = am > 0.f ? floor_log2f(am) - F::EMAX : 0;
+    const int ev = am > 0.f ? flog2_hot<DBG>(am) - F::EMAX : 0;
     const bool ok = (ev >= -127) & (ev <= 126) & (ev >= Rg::ELO) & (ev <= Rg::EHI);
     if (DBG && !ok) return false;  // non-debug kernels finish branch-free and replay
     const float inv = exp2i(-ev), sc = exp2i(ev);
@@ -846,11 +858,20 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
             const int64_t img = gl >> LN;
             float4* dst = reinterpret_cast<float4*>(a.out + img * (int64_t)N * N + (int64_t)pq0 * N + (gl & (N - 1)));
             const int64_t rs = (int64_t)T * N;  // 2 T rows, in float4 units
+            // shared-memory reads in batches of PB positions ahead of their stores,
+            // so that no store waits on the load just before it
+            constexpr int PB = MXFFT_PAIR_BATCH;
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                const float2 v0 = lds64(caddr(bcur, pch0 ^ dsw(T * k), ph0));
-                const float2 v1 = lds64(caddr(bcur, pch1 ^ dsw(T * k), ph1));
-                dst[k * rs] = make_float4(v0.x, v0.y, v1.x, v1.y);
+            for (int k0 = 0; k0 < 16; k0 += PB) {
+                float4 o[PB];
+#pragma unroll
+                for (int k = 0; k < PB; ++k) {
+                    const float2 v0 = lds64(caddr(bcur, pch0 ^ dsw(T * (k0 + k)), ph0));
+                    const float2 v1 = lds64(caddr(bcur, pch1 ^ dsw(T * (k0 + k)), ph1));
+                    o[k] = make_float4(v0.x, v0.y, v1.x, v1.y);
+                }
+#pragma unroll
+                for (int k = 0; k < PB; ++k) dst[(k0 + k) * rs] = o[k];
             }
 #endif
         } else {  // columns, or rows stored transposed: line gl -> column (gl mod n) of image gl/n
