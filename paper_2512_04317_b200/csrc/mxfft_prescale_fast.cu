@@ -58,6 +58,9 @@ constexpr int64_t FUSED_MAX = int64_t(1) << 18;
 #ifndef MXFFT_C3_CLUSTER
 #define MXFFT_C3_CLUSTER 1  // 2-CTA clusters when few large segments leave SMs idle
 #endif
+#ifndef MXFFT_PS_SAMPLE_FIRST
+#define MXFFT_PS_SAMPLE_FIRST 1  // lean statistics: issue the sample loads before the L2 prefetch
+#endif
 #ifndef MXFFT_PS_PREFETCH
 #define MXFFT_PS_PREFETCH 4  // lean statistics: stream rounds prefetched into L2 ahead of the loads
 #endif
@@ -971,11 +974,17 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
     constexpr int PF = MXFFT_PS_PREFETCH;  // rounds of look-ahead (bulk L2 prefetch, one thread)
     constexpr unsigned RB = NT * 4 * 16;   // bytes per stream round
     const int nrounds_pf = (int)(npts * 8 / RB);
-    if (tid == 0)
-        for (int r = 0; r < PF && r < nrounds_pf; ++r)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(x) + (size_t)r * RB),
-                         "n"(RB)
-                         : "memory");
+    auto prefetch_head = [&]() {
+        if (tid == 0)
+            for (int r = 0; r < PF && r < nrounds_pf; ++r)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                 reinterpret_cast<const char*>(x) + (size_t)r * RB),
+                             "n"(RB)
+                             : "memory");
+    };
+#if !MXFFT_PS_SAMPLE_FIRST
+    prefetch_head();
+#endif
     // ---- sample -> histogram bracket ----
     for (int i = tid; i < LB_BINS; i += NT) F.u.s.hist[i] = 0;
     if (tid == 0) {
@@ -1009,6 +1018,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
                     sa[u] = sb[u] = make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
+#if MXFFT_PS_SAMPLE_FIRST
+            // the sample's sector loads go out ahead of the stream's bulk L2
+            // prefetch, so they do not queue behind it
+            if (j0 == tid) prefetch_head();
+#endif
 #pragma unroll
           for (int u = 0; u < SPT; ++u) {
             const float4 a = sa[u], b = sb[u];

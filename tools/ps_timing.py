@@ -1,0 +1,8 @@
+import os,sys,torch
+sys.path.insert(0,'.')
+os.environ['MXFFT_B200_LIB']=os.path.abspath('paper_2512_04317_b200/_lib_pst/libmxfft_b200.so')
+import paper_2512_04317_b200 as mx
+from paper_2512_04317_b200.workloads import ellipse_kspace_batch
+x=torch.from_numpy(ellipse_kspace_batch(256,256,seed=0)).cuda()
+for i in range(3):
+    mx.prescale_stats_device(x,256,256*256,mx.PrescaleConfig()); torch.cuda.synchronize()
