@@ -349,19 +349,22 @@ __device__ __forceinline__ bool trivial_block(float2 (&u)[NB], float2 (&v)[NB], 
     if (DBG && !ok) return false;  // non-debug kernels finish branch-free and replay
     const float inv = exp2i(-ev), sc = exp2i(ev);
     const float2 inv2 = make_float2(inv, inv), sc2 = make_float2(sc, sc);
+    // rotated butterflies: (tr, ti) = (sigma ci, -sigma cr), folded into the
+    // scale pair (exact: sigma = +-1) so that no multiply by sigma is issued
+    const float2 scr = make_float2(sigma * sc, -sigma * sc);
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
         const float2 vs = __fmul2_rn(v[i], inv2);
         const unsigned cv = q2h<ID>(vs.x, vs.y);
         float cr, ci;
         h2f2(cv, cr, ci);
-        const bool rot = S == 1 && ((j0 + i) & 1);
-        const float tr = rot ? sigma * ci : cr;
-        const float ti = rot ? -sigma * cr : ci;
+        const bool rot = S == 1 && ((j0 + i) & 1);  // compile-time
+        const float2 c = rot ? make_float2(ci, cr) : make_float2(cr, ci);
+        const float2 f = rot ? scr : sc2;
         const float2 uu = u[i];
-        u[i] = __ffma2_rn(make_float2(tr, ti), sc2, uu);
-        v[i] = __ffma2_rn(make_float2(-tr, -ti), sc2, uu);
-        if (DBG) dbg_codes(*d, bfly0 + i, cr, ci, tr, ti);
+        u[i] = __ffma2_rn(c, f, uu);
+        v[i] = __ffma2_rn(make_float2(-c.x, -c.y), f, uu);
+        if (DBG) dbg_codes(*d, bfly0 + i, cr, ci, rot ? sigma * ci : cr, rot ? -sigma * cr : ci);
     }
     if (DBG && ((bfly0 % d->cpb) == 0))
         dbg_exps(*d, bfly0, ev, am > 0.f ? ev : -F::EMAX, am > 0.f ? F::EMAX : 0);
@@ -768,10 +771,16 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
             const int64_t base = grp * LPC * (int64_t)N;
             const float4* src = reinterpret_cast<const float4*>(a.in + base) + tid;
             const int64_t lim = (a.total_lines * (int64_t)N - base) / 2;  // chunks left
+            if (lim >= NT * 16) {  // whole tile: no per-chunk bounds checks
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                const bool ok = tid + NT * k < lim;
-                cp_async16(caddr(buf, rch ^ dsw(NT * k), 0), ok ? (const void*)(src + NT * k) : (const void*)a.in, ok);
+                for (int k = 0; k < 16; ++k) cp_async16(caddr(buf, rch ^ dsw(NT * k), 0), src + NT * k, true);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const bool ok = tid + NT * k < lim;
+                    cp_async16(caddr(buf, rch ^ dsw(NT * k), 0), ok ? (const void*)(src + NT * k) : (const void*)a.in,
+                               ok);
+                }
             }
         } else {
             const int64_t gl = grp * LPC + tj;
