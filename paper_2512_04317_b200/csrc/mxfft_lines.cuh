@@ -738,6 +738,11 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
     char* const tile_g = reinterpret_cast<char*>(smem4 + a.tw_chunks);  // generic view (replay)
     constexpr unsigned BUFSZ = (unsigned)GEL * 8u;
     if (buf0 & 127u) __trap();  // radr() ORs chunk offsets into 128-byte-aligned run bases
+    // n = 64 .. 512: the host places both tile buffers on 4 KB boundaries, so a
+    // swizzled address (thread base) ^ (constant chunk offset < 256 chunks) is one
+    // LOP3 instead of an XOR plus an add
+    constexpr bool AX = LT >= 1 && LT <= 4;
+    if (AX && (buf0 & 4095u)) __trap();
     // this thread's line inside the buffer (tile element belem(j, q) = line j, position q)
     auto belem = [&](int j, int q) { return (j >> (lt > 5 ? 0 : 5 - lt)) * (W * 32) + (j & (LPR - 1)) * N + q; };
     const int ebase = belem(tid >> lt, 0);
@@ -823,7 +828,8 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
         bool bad = false;
 #pragma unroll
         for (int m = 0; m < 32; ++m)
-            x[rev_c<5>(m)] = lds64(caddr(bcur, gch ^ dsw((m * T) >> 1), lt ? gh : (m & 1)));
+            x[rev_c<5>(m)] = AX ? lds64(caddr(bcur, gch, gh) ^ (16u * (unsigned)dsw((m * T) >> 1)))
+                                : lds64(caddr(bcur, gch ^ dsw((m * T) >> 1), lt ? gh : (m & 1)));
         if (a.prof_flags & 1) {  // profiling without loads: synthetic in-range data
 #pragma unroll
             for (int m = 0; m < 32; ++m)
@@ -875,8 +881,9 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
                 float4 o[PB];
 #pragma unroll
                 for (int k = 0; k < PB; ++k) {
-                    const float2 v0 = lds64(caddr(bcur, pch0 ^ dsw(T * (k0 + k)), ph0));
-                    const float2 v1 = lds64(caddr(bcur, pch1 ^ dsw(T * (k0 + k)), ph1));
+                    const unsigned c16 = 16u * (unsigned)dsw(T * (k0 + k));
+                    const float2 v0 = AX ? lds64(caddr(bcur, pch0, ph0) ^ c16) : lds64(caddr(bcur, pch0 ^ dsw(T * (k0 + k)), ph0));
+                    const float2 v1 = AX ? lds64(caddr(bcur, pch1, ph1) ^ c16) : lds64(caddr(bcur, pch1 ^ dsw(T * (k0 + k)), ph1));
                     o[k] = make_float4(v0.x, v0.y, v1.x, v1.y);
                 }
 #pragma unroll
@@ -1046,7 +1053,16 @@ static cudaError_t launch_t(const MxLinesArgs& a, size_t smem, cudaStream_t st) 
 template <int ID, int CPB, bool DBG>
 static cudaError_t disp_lt(const MxLinesArgs& a, size_t smem, cudaStream_t st) {
     if (a.log2T > 7) {
-        if constexpr (!DBG) return launch_t<ID, CPB, false, -1, true>(a, smem, st);
+        if constexpr (!DBG) {
+            // n = 8192 / 16384 specialised (every stage, unconditional register stages)
+            if constexpr (CPB >= 8) {
+                if (!a.col_mode && a.stage_limit >= a.log2n) {
+                    if (a.log2T == 8) return launch_t<ID, CPB, false, 8, true>(a, smem, st);
+                    if (a.log2T == 9) return launch_t<ID, CPB, false, 9, true>(a, smem, st);
+                }
+            }
+            return launch_t<ID, CPB, false, -1, true>(a, smem, st);
+        }
         return cudaErrorInvalidValue;
     }
     if constexpr (!DBG && CPB >= 8) {
