@@ -31,6 +31,9 @@
 #ifndef MXFFT_PAIR_STORE
 #define MXFFT_PAIR_STORE 1  // strided copy-out: two adjacent lines per thread, 16-byte stores
 #endif
+#ifndef MXFFT_BIG_PREFETCH
+#define MXFFT_BIG_PREFETCH 1  // n = 8192/16384: bulk L2 prefetch of the next row during this one
+#endif
 #ifndef MXFFT_PAIR_BATCH
 #define MXFFT_PAIR_BATCH 1  // paired strided copy-out: positions read from shared memory per batch of stores
 #endif
@@ -974,6 +977,16 @@ __device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
             for (int m = 0; m < 32; ++m) x[rev_c<5>(m)] = __ldg(src + m * stride);
             if (kin) scale32<DBG>(x, kin, bad);
         }
+#if MXFFT_BIG_PREFETCH
+        // while this line computes, its successor (a contiguous row) streams into
+        // L2, so the next load phase hits L2 instead of waiting on HBM
+        if (!a.col_mode && tid < 4 && grp + gridDim.x < ngroups) {
+            const char* nx = reinterpret_cast<const char*>(a.in + (grp + gridDim.x) * (int64_t)N);
+            const unsigned part = (unsigned)N * 2u;  // bytes per prefetching thread (N * 8 / 4)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx + (size_t)tid * part), "r"(part)
+                         : "memory");
+        }
+#endif
         int U, V;
         run_stages<ID, CPB, DBG, LT>(x, U, V, L, rb, ebase, &dbg, bad);
         if (kout) scale32<DBG>(x, kout, bad);
