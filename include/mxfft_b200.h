@@ -237,6 +237,9 @@ void mxfft_profile_stage_limit(int32_t limit);
 /* Profiling knob for the line kernel: bit 0 skips the tile loads, bit 1 the
  * stores (outputs are then NOT valid); 0 restores normal passes. */
 void mxfft_profile_flags(int32_t flags);
+/* Scheduling knob for the line kernels: cap the persistent grid at n CTAs per
+ * SM (n <= 0: as many as fit).  Results are unchanged. */
+void mxfft_lines_ctas_per_sm(int32_t n);
 
 /* Total number of kernels this library has launched in the process
  * (bookkeeping for the benchmark's gpu_launches count). */

@@ -45,6 +45,7 @@ SIGNATURES = {
     "mxfft_launch_count": ([], _i64),
     "mxfft_profile_stage_limit": ([_i32], None),
     "mxfft_profile_flags": ([_i32], None),
+    "mxfft_lines_ctas_per_sm": ([_i32], None),
     "mxfft_quantize_f64": ([_vp, _vp, _i64, _fp, _vp, _u], _i32),
     "mxfft_mx_encode_f64": ([_vp, _i64, _i32, _fp, _vp, _vp, _vp, _u], _i32),
     "mxfft_mx_decode_f64": ([_vp, _vp, _i64, _i32, _vp, _u], _i32),

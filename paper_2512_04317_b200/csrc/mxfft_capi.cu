@@ -87,6 +87,7 @@ int64_t mxfft_launch_count(void) { return g_launches.load(); }
 
 void mxfft_profile_stage_limit(int32_t limit) { mxfft::g_profile_stage_limit = limit; }
 void mxfft_profile_flags(int32_t flags) { mxfft::g_profile_flags = flags; }
+void mxfft_lines_ctas_per_sm(int32_t n) { mxfft::g_lines_ctas_per_sm = n < 0 ? 0 : n; }
 
 int32_t mxfft_quantize_f64(const double* x, double* out, int64_t n, const mxfft_format* fmt,
                            int32_t* d_nonfinite, uintptr_t stream) {

@@ -89,6 +89,7 @@ struct GenericArgs {
 };
 
 extern int g_profile_stage_limit;
+extern int g_lines_ctas_per_sm;
 extern int g_profile_flags;  // < 0: off (see mxfft_profile_stage_limit)
 bool mx_lines_ok(const Plan& p);
 cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st);

@@ -37,6 +37,7 @@ static cudaError_t disp_fmt(const MxLinesArgs& a, int id, int cpb, size_t smem, 
 
 int g_profile_stage_limit = -1;
 int g_profile_flags = 0;
+int g_lines_ctas_per_sm = 0;  // 0: occupancy (see mxfft_lines_ctas_per_sm)
 
 bool mx_lines_ok(const Plan& p) {
     if (p.fmt.id == F_GENERIC) return false;

@@ -1052,7 +1052,8 @@ static cudaError_t launch_t(const MxLinesArgs& a, size_t smem, cudaStream_t st) 
     }
     const int lines_per_cta = nt >> a.log2T;
     const int64_t groups = (a.total_lines + lines_per_cta - 1) / lines_per_cta;
-    const int64_t cap = (int64_t)sms * occ;
+    const int per_sm = g_lines_ctas_per_sm > 0 && g_lines_ctas_per_sm < occ ? g_lines_ctas_per_sm : occ;
+    const int64_t cap = (int64_t)sms * per_sm;
     const int grid = (int)(groups < cap ? groups : cap);
     k<<<grid, nt, smem, st>>>(a);
     note_launch();
