@@ -57,6 +57,7 @@ struct MxLinesArgs {
     int trivial01, inverse;
     const int32_t* kvec;
     int k_group, kin_sign, kout_sign, kout_const, kin_const, stage_limit;
+    int lpi_shift;  // log2(lines_per_image) when it is a power of two, else -1
     int prof_flags;  // profiling only: bit 0 skip tile loads, bit 1 skip stores
     int tw_chunks;
     // exact replay (replay_lines): reference-literal tables of the plan

@@ -65,6 +65,10 @@ cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
     a.inverse = lp.inverse;
     a.kvec = lp.kvec;
     a.k_group = lp.k_group > 0 ? lp.k_group : 1;
+    a.lpi_shift = -1;
+    if (a.lines_per_image > 0 && (a.lines_per_image & (a.lines_per_image - 1)) == 0)
+        for (a.lpi_shift = 0; (1 << a.lpi_shift) < a.lines_per_image; ++a.lpi_shift) {
+        }
     a.kin_sign = lp.kin_sign;
     a.kout_sign = lp.kout_sign;
     a.kout_const = lp.kout_const;

@@ -34,6 +34,12 @@
 #ifndef MXFFT_BIG_PREFETCH
 #define MXFFT_BIG_PREFETCH 1  // n = 8192/16384: bulk L2 prefetch of the next row during this one
 #endif
+#ifndef MXFFT_KPREF
+#define MXFFT_KPREF 1  // load the next group's prescale exponent a group ahead
+#endif
+#ifndef MXFFT_SHCHAIN
+#define MXFFT_SHCHAIN 0  // renormalisation shift by exponent-field carry (non-debug kernels)
+#endif
 #ifndef MXFFT_PAIR_BATCH
 #define MXFFT_PAIR_BATCH 1  // paired strided copy-out: positions read from shared memory per batch of stores
 #endif
@@ -296,9 +302,13 @@ __device__ __forceinline__ void mxb(float2 (&u)[NB], float2 (&v)[NB], const unsi
         cprod(w[i], cv[i], pr[i], pi[i]);
     }
     const float ap = pair_max<PAIR>(amax_2<NB>(pr, pi));
-    const int sh = ap > F::MAXF ? shift_for<F>(ap) : 0;
+    // ceil(log2(ap / max_finite)) for ap > max_finite, else 0: the mantissa
+    // excess over max_finite's carries into the exponent field (exact; NaN and
+    // inf give a huge shift, which replays the group)
+    const int sh = (DBG || !MXFFT_SHCHAIN) ? (ap > F::MAXF ? shift_for<F>(ap) : 0)
+                       : max(0, (int)((__float_as_uint(ap) + (0x7fffffu - F::MM)) >> 23) - 127 - F::EM);
     const int E = ew + ev + sh;
-    const bool fast = (ev >= -127) & (ev <= 126) & (E >= Rg::ELO) & (E <= Rg::EHI);
+    const bool fast = ((unsigned)(ev + 127) <= 253u) & ((unsigned)(E - Rg::ELO) <= (unsigned)(Rg::EHI - Rg::ELO));
     if constexpr (!DBG) {
         bad |= !fast;  // the group is replayed exactly (replay_lines); keep going
     } else if (__builtin_expect(!fast, 0)) {
@@ -501,6 +511,13 @@ __device__ __forceinline__ Run mkrun(unsigned rb, int e) {
     return {rb + (unsigned)C0 * 16u, (unsigned)(dsw(C0) ^ C0) << 4};
 }
 __device__ __forceinline__ unsigned radr(const Run& r, int k) { return r.a0 | (r.f ^ (unsigned)(k << 4)); }
+
+// prescale-exponent entry of a line: kvec[(line / lines_per_image) / k_group]
+// (a shift and no division in the common power-of-two / one-image-per-k case)
+__device__ __forceinline__ int64_t k_index(const MxLinesArgs& a, int64_t line) {
+    const int64_t img = a.lpi_shift >= 0 ? line >> a.lpi_shift : line / a.lines_per_image;
+    return a.k_group == 1 ? img : img / a.k_group;
+}
 
 // ---------------------------------------------------------------------------
 // kernel body.  The hot variants are specialised on LT = log2(T) (n = 32 T):
@@ -804,6 +821,7 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
 
     // iteration "grp - gridDim.x" only issues the first tile (one issue site)
     int cur = 1;
+    int kk_nxt = 0;  // kvec entry of this thread's line in the next group, loaded a group ahead
     for (int64_t grp = (int64_t)blockIdx.x - gridDim.x; grp < ngroups; grp += gridDim.x) {
         const int64_t nxt = grp + gridDim.x;
         const unsigned bcur = buf0 + (unsigned)cur * BUFSZ, bnxt = buf0 + (unsigned)(cur ^ 1) * BUFSZ;
@@ -811,19 +829,22 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
         __syncthreads();  // the other buffer's previous readers are done
         if (nxt < ngroups) issue_tile(nxt, bnxt);
         cp_commit();
+#if MXFFT_KPREF
+        const int kk = kk_nxt;
+        if (a.kvec && nxt < ngroups) {
+            const int64_t nl = nxt * LPC + (tid >> lt);
+            kk_nxt = nl < a.total_lines ? __ldg(a.kvec + k_index(a, nl)) : 0;
+        }
+#endif
         if (grp < 0) continue;
         cp_wait<1>();     // this thread's copies of group grp have landed
         __syncthreads();  // ... and everybody's
 
         const int64_t line = grp * LPC + (tid >> lt);
-        int kin = a.kin_const, kout = a.kout_const;
-        if (a.kvec) {
-            const bool active = line < a.total_lines;
-            const int64_t img = line / a.lines_per_image;
-            const int kk = active ? a.kvec[img / a.k_group] : 0;
-            kin += a.kin_sign * kk;
-            kout += a.kout_sign * kk;
-        }
+#if !MXFFT_KPREF
+        const int kk = a.kvec && line < a.total_lines ? a.kvec[k_index(a, line)] : 0;
+#endif
+        const int kin = a.kin_const + a.kin_sign * kk, kout = a.kout_const + a.kout_sign * kk;
         if (DBG) dbg.row = line;
 
         // bit-reversed gather (fftcore.py:262): x[rev5(m)] <- line element m*T + rev_T(c)
