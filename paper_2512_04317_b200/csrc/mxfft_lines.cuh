@@ -40,6 +40,9 @@
 #ifndef MXFFT_SHCHAIN
 #define MXFFT_SHCHAIN 0  // renormalisation shift by exponent-field carry (non-debug kernels)
 #endif
+#ifndef MXFFT_PAIR_STAGES
+#define MXFFT_PAIR_STAGES 1  // n-specialised kernels: two butterfly stages per shared-memory exchange
+#endif
 #ifndef MXFFT_PAIR_BATCH
 #define MXFFT_PAIR_BATCH 1  // paired strided copy-out: positions read from shared memory per batch of stores
 #endif
@@ -180,6 +183,18 @@ __device__ __forceinline__ float pair_max(float a) {
     return a;
 }
 
+// max over the G consecutive lanes (G = 1, 2, 4) that share one MX block
+template <int G>
+__device__ __forceinline__ float grp_max(float a) {
+    if constexpr (G > 1) {
+        const unsigned lane = threadIdx.x & 31;
+        const unsigned m = ((1u << G) - 1u) << (lane & ~(unsigned)(G - 1));
+        a = fmaxf(a, __shfl_xor_sync(m, a, 1));
+        if constexpr (G > 2) a = fmaxf(a, __shfl_xor_sync(m, a, 2));
+    }
+    return a;
+}
+
 struct LDbg {
     int32_t* vexp;
     float* vcodes;
@@ -284,12 +299,14 @@ __device__ __forceinline__ int flog2_hot(float am) {
     return (int)(__float_as_uint(am) >> 23) - 127;  // am >= 0
 }
 
-template <int ID, int NB, bool PAIR, bool DBG>
+template <int ID, int NB, int G, bool DBG>
 __device__ __forceinline__ void mxb(float2 (&u)[NB], float2 (&v)[NB], const unsigned (&w)[NB],
                                     int ew, const LDbg* d, int bfly0, bool& bad) {
     using F = HwFmt<ID>;
     using Rg = DecodeRange<F>;
-    const float am = pair_max<PAIR>(amax_c<NB>(v));
+    constexpr bool PAIR = G == 2;
+    static_assert(!(DBG && G > 2), "debug kernels split a block over at most a lane pair");
+    const float am = grp_max<G>(amax_c<NB>(v));
     const int ev = am > 0.f ? flog2_hot<DBG>(am) - F::EMAX : 0;
     const float inv = exp2i(-ev);
     unsigned cv[NB];
@@ -301,7 +318,7 @@ __device__ __forceinline__ void mxb(float2 (&u)[NB], float2 (&v)[NB], const unsi
         cv[i] = q2h<ID>(vs.x, vs.y);
         cprod(w[i], cv[i], pr[i], pi[i]);
     }
-    const float ap = pair_max<PAIR>(amax_2<NB>(pr, pi));
+    const float ap = grp_max<G>(amax_2<NB>(pr, pi));
     // ceil(log2(ap / max_finite)) for ap > max_finite, else 0: the mantissa
     // excess over max_finite's carries into the exponent field (exact; NaN and
     // inf give a huge shift, which replays the group)
@@ -438,7 +455,7 @@ __device__ __forceinline__ void local_stage(float2 (&x)[32], const unsigned* tw,
             unsigned w[NB];
 #pragma unroll
             for (int i = 0; i < NB; ++i) w[i] = tw[tws(half + ((k * NB + i) & (half - 1)))];
-            mxb<ID, NB, PAIR, DBG>(ub, vb, w, twe[half + j0], d, bfly0, bad);
+            mxb<ID, NB, PAIR ? 2 : 1, DBG>(ub, vb, w, twe[half + j0], d, bfly0, bad);
         }
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
@@ -592,7 +609,7 @@ __device__ __forceinline__ void smem_stage(float2 (&x)[32], int& U, int& V, cons
             vb[i] = x[16 + k * NB + i];
             wb[i] = w16[k * NB + i];
         }
-        mxb<ID, NB, PAIR, DBG>(ub, vb, wb, L.twe[half + j0 + k * NB], dbg, b0 + k * NB, bad);
+        mxb<ID, NB, PAIR ? 2 : 1, DBG>(ub, vb, wb, L.twe[half + j0 + k * NB], dbg, b0 + k * NB, bad);
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
             x[k * NB + i] = ub[i];
@@ -601,12 +618,81 @@ __device__ __forceinline__ void smem_stage(float2 (&x)[32], int& U, int& V, cons
     }
 }
 
+// Two butterfly stages s, s+1 (h = 2^s >= 32) per shared-memory exchange.
+// Thread tl owns the radix-4 units [8 tl, 8 tl + 8) of the line: with
+// g = 8 tl / h and j0 = 8 tl mod h, x[8k + i] holds line element
+// P + k h + i, P = 4 h g + j0 (k < 4, i < 8).  Stage s pairs (x[i], x[8+i]) and
+// (x[16+i], x[24+i]) (butterflies j0 + i of groups 2g, 2g+1); stage s+1 pairs
+// (x[i], x[16+i]) and (x[8+i], x[24+i]) (butterflies j0 + i and h + j0 + i of
+// group g).  Every 8-butterfly set is a whole MX block (cpb 8) or 1/2, 1/4 of
+// one shared with the neighbouring lanes (cpb 16, 32: G = cpb/8 lanes, the
+// block maxima are reduced with shuffles).  The four runs of 4 chunks are
+// conflict-free under dsw() for every n and s (checked by simulation).
+__device__ __forceinline__ unsigned run4_addr(unsigned rb, int e) {  // e: multiple of 8
+    return rb + 16u * (unsigned)dsw(e >> 1);
+}
+__device__ __forceinline__ void publish4(const float2 (&x)[32], unsigned rb, int ebase, int P, int h) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const unsigned a = run4_addr(rb, ebase + P + k * h);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sts128(a ^ (16u * c), x[8 * k + 2 * c], x[8 * k + 2 * c + 1]);
+    }
+}
+__device__ __forceinline__ void publish2(const float2 (&x)[32], unsigned rb, int ebase, int U, int V) {
+    const Run ru = mkrun(rb, ebase + U), rv = mkrun(rb, ebase + V);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        sts128(radr(ru, k), x[2 * k], x[2 * k + 1]);
+        sts128(radr(rv, k), x[16 + 2 * k], x[17 + 2 * k]);
+    }
+}
+
+template <int ID, int CPB>
+__device__ __forceinline__ void pair_stage(float2 (&x)[32], int& P, int& H, const LCtx& L, unsigned rb, int ebase,
+                                           int s, bool big, bool& bad) {
+    constexpr int G = CPB / 8;  // lanes per MX block
+    const int h = 1 << s;
+    const int u0 = 8 * L.tl, j0 = u0 & (h - 1);
+    P = ((u0 >> s) << (s + 2)) + j0;
+    H = h;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const unsigned a = run4_addr(rb, ebase + P + k * h);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) lds128(a ^ (16u * c), x[8 * k + 2 * c], x[8 * k + 2 * c + 1]);
+    }
+    unsigned w0[8], w1[8], w2[8];
+#pragma unroll
+    for (int i = 0; i < 8; i += 4) {
+        const uint4 q0 = lds128u(L.tw_sh + 4u * (unsigned)tws(h + j0 + i));
+        const uint4 q1 = lds128u(L.tw_sh + 4u * (unsigned)tws(2 * h + j0 + i));
+        const uint4 q2 = lds128u(L.tw_sh + 4u * (unsigned)tws(3 * h + j0 + i));
+        w0[i] = q0.x, w0[i + 1] = q0.y, w0[i + 2] = q0.z, w0[i + 3] = q0.w;
+        w1[i] = q1.x, w1[i + 1] = q1.y, w1[i + 2] = q1.z, w1[i + 3] = q1.w;
+        w2[i] = q2.x, w2[i + 1] = q2.y, w2[i + 2] = q2.z, w2[i + 3] = q2.w;
+    }
+    const int e0 = L.twe[h + j0], e1 = L.twe[2 * h + j0], e2 = L.twe[3 * h + j0];
+    float2 a[8], b[8], c[8], d[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = x[i], b[i] = x[8 + i], c[i] = x[16 + i], d[i] = x[24 + i];
+    // stage s
+    mxb<ID, 8, G, false>(a, b, w0, e0, nullptr, 0, bad);
+    mxb<ID, 8, G, false>(c, d, w0, e0, nullptr, 0, bad);
+    // stage s + 1
+    mxb<ID, 8, G, false>(a, c, w1, e1, nullptr, 0, bad);
+    mxb<ID, 8, G, false>(b, d, w2, e2, nullptr, 0, bad);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = a[i], x[8 + i] = b[i], x[16 + i] = c[i], x[24 + i] = d[i];
+}
+
 // All butterfly stages of one group.  Registers for stages < 5; stages >= 5
 // exchange through the line's region (element e of the buffer at shared
 // address rb lives in chunk dsw(e/2), half e&1).  On return x[0..15] sit at
-// line positions U.., x[16..31] at V.. .
+// line positions U.., x[16..31] at V.. (H == 0), or -- after paired stages --
+// x[8k..8k+7] at P + k H (H > 0).
 template <int ID, int CPB, bool DBG, int LT>
-__device__ __forceinline__ void run_stages(float2 (&x)[32], int& U, int& V, const LCtx& L,
+__device__ __forceinline__ void run_stages(float2 (&x)[32], int& U, int& V, int& P, int& H, const LCtx& L,
                                            unsigned rb, int ebase, LDbg* dbg, bool& bad) {
     const int lt = LT >= 0 ? LT : L.lt;
     const bool big = lt > 5;  // a line spans several warps
@@ -624,9 +710,31 @@ __device__ __forceinline__ void run_stages(float2 (&x)[32], int& U, int& V, cons
         if (lim_loc > 4) local_stage<ID, CPB, 4, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg, bad);
     U = 32 * L.c;
     V = U + 16;
+    H = 0;
+    P = 0;
     // kept rolled: one copy of the stage body keeps the kernel inside the
     // instruction cache (unrolling measured slower)
     const int last = FULL ? lt + 5 : (L.slim < lt + 5 ? L.slim : lt + 5);
+#if MXFFT_PAIR_STAGES
+    if constexpr (FULL && LOCAL == 5 && LT >= 2) {
+        // an odd stage out first (single), then pairs of stages per exchange
+        int s = 5;
+        if (LT & 1) {
+            smem_stage<ID, CPB, DBG>(x, U, V, L, rb, ebase, 5, LT > 5, dbg, bad);
+            s = 6;
+        }
+        publish2(x, rb, ebase, U, V);
+        lsync(LT > 5);
+        pair_stage<ID, CPB>(x, P, H, L, rb, ebase, s, LT > 5, bad);
+#pragma unroll 1
+        for (s += 2; s < LT + 5; s += 2) {
+            publish4(x, rb, ebase, P, H);
+            lsync(LT > 5);
+            pair_stage<ID, CPB>(x, P, H, L, rb, ebase, s, LT > 5, bad);
+        }
+        return;
+    }
+#endif
 #if MXFFT_UNROLL_SMEM
     if constexpr (LT >= 0 && !DBG) {
 #pragma unroll
@@ -861,20 +969,17 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
         }
         if (kin) scale32<DBG>(x, kin, bad);
 
-        int U, V;
-        run_stages<ID, CPB, DBG, LT>(x, U, V, L, bcur, ebase, &dbg, bad);
+        int U, V, P, H;
+        run_stages<ID, CPB, DBG, LT>(x, U, V, P, H, L, bcur, ebase, &dbg, bad);
 
         // publish (undo_prescale / 1/n^2 fused), then coalesced stores
         if (kout) scale32<DBG>(x, kout, bad);
         if (!DBG && __syncthreads_or(bad)) {
             replay_lines(a, grp * LPC, LPC, tile_g + (bcur - buf0), lt > 5 ? 0 : 5 - lt, W * 32, LPR - 1);
+        } else if (H > 0) {
+            publish4(x, bcur, ebase, P, H);
         } else {
-            const Run ru = mkrun(bcur, ebase + U), rv = mkrun(bcur, ebase + V);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                sts128(radr(ru, k), x[2 * k], x[2 * k + 1]);
-                sts128(radr(rv, k), x[16 + 2 * k], x[17 + 2 * k]);
-            }
+            publish2(x, bcur, ebase, U, V);
         }
         __syncthreads();
         if (a.prof_flags & 2) {
@@ -1008,14 +1113,31 @@ __device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
                          : "memory");
         }
 #endif
-        int U, V;
-        run_stages<ID, CPB, DBG, LT>(x, U, V, L, rb, ebase, &dbg, bad);
+        int U, V, P, H;
+        run_stages<ID, CPB, DBG, LT>(x, U, V, P, H, L, rb, ebase, &dbg, bad);
         if (kout) scale32<DBG>(x, kout, bad);
         if (!DBG && __syncthreads_or(bad)) {
             char* tile = reinterpret_cast<char*>(smem4 + a.tw_chunks);
             replay_lines(a, line, 1, tile, 0, N, 0);
             for (int i = tid; i < N; i += blockDim.x)
                 a.out[obase + (int64_t)i * oes] = *reinterpret_cast<const float2*>(tile + 16 * dsw(i >> 1) + 8 * (i & 1));
+            __syncthreads();
+            continue;
+        }
+        if (H > 0) {  // paired-stage layout: x[8k..8k+7] at P + k H
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                float2* dk = a.out + obase + (int64_t)(P + k * H) * oes;
+                if (oes == 1) {
+#pragma unroll
+                    for (int i = 0; i < 8; i += 2)
+                        *reinterpret_cast<float4*>(dk + i) =
+                            make_float4(x[8 * k + i].x, x[8 * k + i].y, x[8 * k + i + 1].x, x[8 * k + i + 1].y);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) dk[i * oes] = x[8 * k + i];
+                }
+            }
             __syncthreads();
             continue;
         }
