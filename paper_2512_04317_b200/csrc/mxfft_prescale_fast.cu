@@ -56,7 +56,7 @@ static inline int sample_size(int64_t npts) {
 
 constexpr int64_t FUSED_MAX = int64_t(1) << 18;
 #ifndef MXFFT_C3_CLUSTER
-#define MXFFT_C3_CLUSTER 1  // 2-CTA clusters when few large segments leave SMs idle
+#define MXFFT_C3_CLUSTER 2  // CTAs per cluster (2 or 4; 0: off) when few large segments leave SMs idle (4 measured slower: 109 vs 80 us on C3)
 #endif
 #ifndef MXFFT_PS_SAMPLE_FIRST
 #define MXFFT_PS_SAMPLE_FIRST 1  // lean statistics: issue the sample loads before the L2 prefetch
@@ -753,19 +753,30 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_ps_fused(const float2* __rest
         cg::cluster_group cluster = cg::this_cluster();
         cluster.sync();
         if (crank == 0) {
-            const Shared& R = *cluster.map_shared_rank(&F, 1);
-            const unsigned nc0 = F.ncand, nc1 = R.ncand, nt0 = F.ntop, nt1 = R.ntop;
-            for (unsigned i = tid; i < nc1; i += F_THREADS)
-                if (nc0 + i < F_CCAP && i < F_CCAP) F.cand[nc0 + i] = R.cand[i];
-            for (unsigned i = tid; i < nt1; i += F_THREADS)
-                if (nt0 + i < F_TOPCAP && i < F_TOPCAP) F.topb[nt0 + i] = R.topb[i];
+            // append ranks 1 .. CL-1 in order (counts may exceed the capacity:
+            // the select phase then fails the segment over to the exact kernel)
+            unsigned nc = F.ncand, nt = F.ntop, flags = F.flags;
+            unsigned nnz = F.nnz, below = F.below;
+            for (int r = 1; r < CL; ++r) {
+                const Shared& R = *cluster.map_shared_rank(&F, r);
+                const unsigned nc1 = R.ncand, nt1 = R.ntop;
+                for (unsigned i = tid; i < nc1; i += F_THREADS)
+                    if (nc + i < F_CCAP && i < F_CCAP) F.cand[nc + i] = R.cand[i];
+                for (unsigned i = tid; i < nt1; i += F_THREADS)
+                    if (nt + i < F_TOPCAP && i < F_TOPCAP) F.topb[nt + i] = R.topb[i];
+                nc += nc1;
+                nt += nt1;
+                nnz += R.nnz;
+                below += R.below;
+                flags |= R.flags;
+            }
             __syncthreads();
             if (tid == 0) {
-                F.ncand = nc0 + nc1;
-                F.ntop = nt0 + nt1;
-                F.nnz += R.nnz;
-                F.below += R.below;
-                F.flags |= R.flags;
+                F.ncand = nc;
+                F.ntop = nt;
+                F.nnz = nnz;
+                F.below = below;
+                F.flags = flags;
             }
         }
         cluster.sync();  // CTA 1's shared memory stays alive until CTA 0 has read it
@@ -1376,7 +1387,7 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sizeof(FusedShared<512, 8192, 4096, 2048, 2048>));
             if (e == cudaSuccess && MXFFT_C3_CLUSTER)
-                e = cudaFuncSetAttribute(k_ps_fused<512, 8192, 2, 4096, 2048, 2048>,
+                e = cudaFuncSetAttribute(k_ps_fused<512, 8192, (MXFFT_C3_CLUSTER > 1 ? MXFFT_C3_CLUSTER : 2), 4096, 2048, 2048>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sizeof(FusedShared<512, 8192, 4096, 2048, 2048>));
             if (e != cudaSuccess) return e;
@@ -1419,17 +1430,18 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
             k_ps_fused<512, 4096, 1, 4096, 2048, 1024><<<(unsigned)nseg, 512, sizeof(FusedShared<512, 4096, 4096, 2048, 1024>), st>>>(
                 x, npts, S, q, c, out, kvec, list, list_n);
         } else if (nseg * 2 <= 148 * 2 && MXFFT_C3_CLUSTER) {
-            // few large segments (C3: 64 x 512^2): a 2-CTA cluster per segment
-            // so that twice as many SMs stream
-            auto k = k_ps_fused<512, 8192, 2, 4096, 2048, 2048>;
+            // few large segments (C3: 64 x 512^2): a CL-CTA cluster per segment
+            // so that CL times as many SMs stream
+            constexpr int CLN = MXFFT_C3_CLUSTER > 1 ? MXFFT_C3_CLUSTER : 2;
+            auto k = k_ps_fused<512, 8192, CLN, 4096, 2048, 2048>;
             cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3((unsigned)(nseg * 2));
+            cfg.gridDim = dim3((unsigned)(nseg * CLN));
             cfg.blockDim = dim3(512);
             cfg.dynamicSmemBytes = sizeof(FusedShared<512, 8192, 4096, 2048, 2048>);
             cfg.stream = st;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.x = CLN;
             attr[0].val.clusterDim.y = 1;
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
