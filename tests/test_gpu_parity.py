@@ -160,7 +160,9 @@ def test_stage_capture_golden(mx, torch):
 def test_rows_vs_oracle_all_formats_blocks(mx, torch, rng):
     for name in FMTS:
         for bsz in (2, 4, 8, 16, 32, 64):
-            for n in (32, 128, 512, 2048):
+            # even and odd numbers of shared-memory stages (paired-stage
+            # exchange with and without a single stage first)
+            for n in (32, 128, 256, 512, 1024, 2048, 4096):
                 x = (rng.standard_normal((6, n)) + 1j * rng.standard_normal((6, n))) \
                     * 10.0 ** rng.uniform(-4, 4, (6, 1))
                 x = x.astype(np.complex64)
@@ -169,6 +171,21 @@ def test_rows_vs_oracle_all_formats_blocks(mx, torch, rng):
                 for inv in (False, True):
                     got = mx.fftcore.fft_rows_device(torch.from_numpy(x).cuda(), p, inv)
                     assert_same(got.cpu().numpy(), O.fft_batch(x, op, inv), f"{name}:{bsz}:{n}:{inv}")
+
+
+def test_rows_8192_blocks(mx, torch, rng):
+    """n = 8192 (one line per CTA, paired stages; MX blocks over 1, 2 and 4
+    lanes for B = 16, 32, 64) against the oracle, forward and inverse."""
+    n = 8192
+    x = ((rng.standard_normal((2, n)) + 1j * rng.standard_normal((2, n))) * 10.0 ** rng.uniform(-3, 3, (2, 1)))
+    x = x.astype(np.complex64)
+    for name in ("e4m3", "e2m1"):
+        for bsz in (16, 32, 64):
+            p = mx.make_plan(n, mx.ModeSpec.mx(mx.get_mx_format(name), bsz))
+            op = O.make_plan(n, O.ALL_MX[name], bsz)
+            for inv in (False, True):
+                got = mx.fftcore.fft_rows_device(torch.from_numpy(x).cuda(), p, inv).cpu().numpy()
+                assert_same(got, O.fft_batch(x, op, inv), f"{name}:{bsz}:8192:{inv}")
 
 
 def test_rows_16384(mx, torch):
