@@ -465,7 +465,7 @@ def main():
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get(dom)
+            traffic = (json.load(open(tr_path)).get(a.config) or {}).get(dom)
         except Exception:
             traffic = None
 
