@@ -873,7 +873,12 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
     if (AX && (buf0 & 4095u)) __trap();
     // this thread's line inside the buffer (tile element belem(j, q) = line j, position q)
     auto belem = [&](int j, int q) { return (j >> (lt > 5 ? 0 : 5 - lt)) * (W * 32) + (j & (LPR - 1)) * N + q; };
-    const int ebase = belem(tid >> lt, 0);
+    // the line this thread computes.  n = 256: the two line bits within a warp
+    // are swapped so that each half-warp's 64-bit gather loads (two lines)
+    // cover all 32 banks (2 wavefronts instead of 4, by simulation and ncu); the
+    // 128-bit exchange accesses are one line per quarter-warp either way
+    const int lj = (LT == 3) ? (((tid >> 3) & ~3) | (((tid >> 3) & 1) << 1) | (((tid >> 4) & 1))) : (tid >> lt);
+    const int ebase = belem(lj, 0);
     // gather: element ebase + m T + rcol -> chunk dsw(ebase/2) ^ dsw(rcol/2) ^ dsw(m T/2)
     const int gch = dsw(ebase >> 1) ^ dsw(rcol >> 1);
     const int gh = rcol & 1;
@@ -940,7 +945,7 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
 #if MXFFT_KPREF
         const int kk = kk_nxt;
         if (a.kvec && nxt < ngroups) {
-            const int64_t nl = nxt * LPC + (tid >> lt);
+            const int64_t nl = nxt * LPC + lj;
             kk_nxt = nl < a.total_lines ? __ldg(a.kvec + k_index(a, nl)) : 0;
         }
 #endif
@@ -948,7 +953,7 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
         cp_wait<1>();     // this thread's copies of group grp have landed
         __syncthreads();  // ... and everybody's
 
-        const int64_t line = grp * LPC + (tid >> lt);
+        const int64_t line = grp * LPC + lj;
 #if !MXFFT_KPREF
         const int kk = a.kvec && line < a.total_lines ? a.kvec[k_index(a, line)] : 0;
 #endif
