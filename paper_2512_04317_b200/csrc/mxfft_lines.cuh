@@ -889,7 +889,15 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
     const int th = te0 & 1;
 #if MXFFT_PAIR_STORE
     // paired strided stores: lines 2 pa, 2 pa + 1 of the group, positions pq0 + 2 T k
-    const int pa = tid & ((LPC >> 1) - 1), pq0 = tid >> (LLPC > 0 ? LLPC - 1 : 0);
+    // n <= 256: pa bits 0-2 <- tid bits 0-2, pq0 bit 0 <- tid bit 3, then the
+    // remaining pa bits, then pq0: every half-warp reads two positions (both
+    // halves of the 16-byte chunks), so its 64-bit reads hit 32 distinct banks
+    // (tools/sim_copyout_banks.py); a warp still writes whole 128-byte row segments
+    const int phb = 3 - lt > 0 ? 3 - lt : 0;  // pa bits above bit 2 (n <= 256)
+    const int pa = LT >= 0 && LT <= 3 ? ((tid & 7) | (((tid >> 4) & ((1 << phb) - 1)) << 3))
+                                      : tid & ((LPC >> 1) - 1);
+    const int pq0 = LT >= 0 && LT <= 3 ? (((tid >> 3) & 1) | ((tid >> (4 + phb)) << 1))
+                                       : tid >> (LLPC > 0 ? LLPC - 1 : 0);
     const int pe0 = belem(2 * pa, pq0), pe1 = belem(2 * pa + 1, pq0);
     const int pch0 = dsw(pe0 >> 1), ph0 = pe0 & 1, pch1 = dsw(pe1 >> 1), ph1 = pe1 & 1;
 #endif
