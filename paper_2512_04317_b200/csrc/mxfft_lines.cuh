@@ -43,6 +43,9 @@
 #ifndef MXFFT_PAIR_STAGES
 #define MXFFT_PAIR_STAGES 1  // n-specialised kernels: two butterfly stages per shared-memory exchange
 #endif
+#ifndef MXFFT_PAIR_STORE_MAXLT
+#define MXFFT_PAIR_STORE_MAXLT 3  // paired strided copy-out up to n = 32 * 2^LT (n = 512 measured 13 % slower)
+#endif
 #ifndef MXFFT_PAIR_BATCH
 #define MXFFT_PAIR_BATCH 1  // paired strided copy-out: positions read from shared memory per batch of stores
 #endif
@@ -894,9 +897,13 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
     // halves of the 16-byte chunks), so its 64-bit reads hit 32 distinct banks
     // (tools/sim_copyout_banks.py); a warp still writes whole 128-byte row segments
     const int phb = 3 - lt > 0 ? 3 - lt : 0;  // pa bits above bit 2 (n <= 256)
+    // n = 512 (4 pairs): pa <- tid bits 4-5, pq0 <- tid bits 0-3, 6 (simulated
+    // conflict-free; a warp writes 32-byte row segments of 16 rows)
     const int pa = LT >= 0 && LT <= 3 ? ((tid & 7) | (((tid >> 4) & ((1 << phb) - 1)) << 3))
+                   : LT == 4          ? ((tid >> 4) & 3)
                                       : tid & ((LPC >> 1) - 1);
     const int pq0 = LT >= 0 && LT <= 3 ? (((tid >> 3) & 1) | ((tid >> (4 + phb)) << 1))
+                    : LT == 4          ? ((tid & 15) | ((tid >> 6) << 4))
                                        : tid >> (LLPC > 0 ? LLPC - 1 : 0);
     const int pe0 = belem(2 * pa, pq0), pe1 = belem(2 * pa + 1, pq0);
     const int pch0 = dsw(pe0 >> 1), ph0 = pe0 & 1, pch1 = dsw(pe1 >> 1), ph1 = pe1 & 1;
@@ -1009,7 +1016,7 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
                 }
             }
 #if MXFFT_PAIR_STORE
-        } else if (LT >= 0 && LT <= 3 && (grp + 1) * LPC <= a.total_lines) {  // n <= 256 (n = 512: slower)
+        } else if (LT >= 0 && LT <= MXFFT_PAIR_STORE_MAXLT && (grp + 1) * LPC <= a.total_lines) {
             // two adjacent output columns per thread: one 16-byte store per position
             const int64_t gl = grp * LPC + 2 * pa;
             const int64_t img = gl >> LN;
