@@ -46,6 +46,9 @@
 #ifndef MXFFT_PAIR_STORE_MAXLT
 #define MXFFT_PAIR_STORE_MAXLT 3  // paired strided copy-out up to n = 32 * 2^LT (n = 512 measured 13 % slower)
 #endif
+#ifndef MXFFT_DEFER_COPYOUT
+#define MXFFT_DEFER_COPYOUT 0  // n <= 256 transposed stores: copy group g out during group g+1 (measured +1.5 % C2, +3 % C4: ptxas does not interleave it with the math)
+#endif
 #ifndef MXFFT_PAIR_BATCH
 #define MXFFT_PAIR_BATCH 1  // paired strided copy-out: positions read from shared memory per batch of stores
 #endif
@@ -694,9 +697,13 @@ __device__ __forceinline__ void pair_stage(float2 (&x)[32], int& P, int& H, cons
 // address rb lives in chunk dsw(e/2), half e&1).  On return x[0..15] sit at
 // line positions U.., x[16..31] at V.. (H == 0), or -- after paired stages --
 // x[8k..8k+7] at P + k H (H > 0).
-template <int ID, int CPB, bool DBG, int LT>
+struct NoHook {
+    __device__ __forceinline__ void operator()() const {}
+};
+
+template <int ID, int CPB, bool DBG, int LT, class Mid = NoHook>
 __device__ __forceinline__ void run_stages(float2 (&x)[32], int& U, int& V, int& P, int& H, const LCtx& L,
-                                           unsigned rb, int ebase, LDbg* dbg, bool& bad) {
+                                           unsigned rb, int ebase, LDbg* dbg, bool& bad, const Mid& mid = Mid()) {
     const int lt = LT >= 0 ? LT : L.lt;
     const bool big = lt > 5;  // a line spans several warps
     constexpr int LOCAL = MXFFT_LOCAL_STAGES;  // unrolled register stages (4 or 5)
@@ -707,6 +714,7 @@ __device__ __forceinline__ void run_stages(float2 (&x)[32], int& U, int& V, int&
     const int lim_loc = FULL ? LOCAL : (L.slim < LOCAL ? L.slim : LOCAL);
     if (lim_loc > 0) local_stage<ID, CPB, 0, DBG>(x, L.tw, L.twe, L.c, L.trivial, L.sigma, dbg, bad);
     if (lim_loc > 1) local_stage<ID, CPB, 1, DBG>(x, L.tw, L.twe, L.c, L.trivial, L.sigma, dbg, bad);
+    mid();  // (deferred copy-out: the previous group's buffer is free from here on)
     if (lim_loc > 2) local_stage<ID, CPB, 2, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg, bad);
     if (lim_loc > 3) local_stage<ID, CPB, 3, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg, bad);
     if constexpr (LOCAL > 4)
@@ -947,6 +955,84 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
         }
     };
 
+#if MXFFT_DEFER_COPYOUT
+    // n <= 256 transposed-store passes: group g's results stay in its buffer and
+    // leave while group g+1's first two (register) stages compute -- the copy-out
+    // is branch-free (predicated stores) so the compiler can interleave its
+    // shared-memory reads and global stores with that arithmetic.  Group g+2's
+    // tile is then issued into the freed buffer after stage 1.
+    if constexpr (LT >= 0 && LT <= MXFFT_PAIR_STORE_MAXLT && !DBG && MXFFT_PAIR_STORE) {
+        if (a.tstore && !a.col_mode && !(a.prof_flags & 3)) {
+            auto copy_out = [&](int64_t g, unsigned bsrc) {
+                const int64_t gl = g * LPC + 2 * pa;
+                const bool v2 = g >= 0 && gl + 1 < a.total_lines;         // both lines of the pair
+                const bool v1 = g >= 0 && gl < a.total_lines && !v2;      // only the first
+                const int64_t glc = g >= 0 ? gl : 0;
+                const int64_t img = glc >> LN;
+                float4* dst = reinterpret_cast<float4*>(a.out + img * (int64_t)N * N + (int64_t)pq0 * N + (glc & (N - 1)));
+                const int64_t rs = (int64_t)T * N;
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const unsigned c16 = 16u * (unsigned)dsw(T * k);
+                    const float2 v0 = AX ? lds64(caddr(bsrc, pch0, ph0) ^ c16) : lds64(caddr(bsrc, pch0 ^ dsw(T * k), ph0));
+                    const float2 v1v = AX ? lds64(caddr(bsrc, pch1, ph1) ^ c16) : lds64(caddr(bsrc, pch1 ^ dsw(T * k), ph1));
+                    if (v2) dst[k * rs] = make_float4(v0.x, v0.y, v1v.x, v1v.y);
+                    if (v1) *reinterpret_cast<float2*>(dst + k * rs) = v0;
+                }
+            };
+            int cur = 0;
+            int kk = 0, kk_nxt = 0;
+            if ((int64_t)blockIdx.x < ngroups) {
+                issue_tile(blockIdx.x, buf0);
+                const int64_t nl = (int64_t)blockIdx.x * LPC + lj;
+                if (a.kvec && nl < a.total_lines) kk = __ldg(a.kvec + k_index(a, nl));
+            }
+            cp_commit();
+            int64_t prev = -1;
+            for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+                const unsigned bcur = buf0 + (unsigned)cur * BUFSZ, both = buf0 + (unsigned)(cur ^ 1) * BUFSZ;
+                cp_wait<0>();     // this thread's copies of group grp have landed
+                __syncthreads();  // ... everybody's, and group prev's results are published
+                const int kin = a.kin_const + a.kin_sign * kk, kout = a.kout_const + a.kout_sign * kk;
+                float2 x[32];
+                bool bad = false;
+#pragma unroll
+                for (int m = 0; m < 32; ++m)
+                    x[rev_c<5>(m)] = AX ? lds64(caddr(bcur, gch, gh) ^ (16u * (unsigned)dsw((m * T) >> 1)))
+                                        : lds64(caddr(bcur, gch ^ dsw((m * T) >> 1), lt ? gh : (m & 1)));
+                if (kin) scale32<DBG>(x, kin, bad);
+                copy_out(prev, both);  // group prev leaves while stages 0-1 of grp compute
+                const int64_t nxt = grp + gridDim.x;
+                auto mid = [&]() {
+                    __syncthreads();  // everybody has read group prev out of 'both'
+                    if (nxt < ngroups) {
+                        issue_tile(nxt, both);
+                        const int64_t nl = nxt * LPC + lj;
+                        kk_nxt = a.kvec && nl < a.total_lines ? __ldg(a.kvec + k_index(a, nl)) : 0;
+                    }
+                    cp_commit();
+                };
+                int U, V, P, H;
+                run_stages<ID, CPB, DBG, LT>(x, U, V, P, H, L, bcur, ebase, &dbg, bad, mid);
+                if (kout) scale32<DBG>(x, kout, bad);
+                if (__syncthreads_or(bad)) {
+                    replay_lines(a, grp * LPC, LPC, tile_g + (bcur - buf0), lt > 5 ? 0 : 5 - lt, W * 32, LPR - 1);
+                } else if (H > 0) {
+                    publish4(x, bcur, ebase, P, H);
+                } else {
+                    publish2(x, bcur, ebase, U, V);
+                }
+                prev = grp;
+                cur ^= 1;
+                kk = kk_nxt;
+            }
+            __syncthreads();
+            copy_out(prev, buf0 + (unsigned)(cur ^ 1) * BUFSZ);
+            cp_wait<0>();
+            return;
+        }
+    }
+#endif
     // iteration "grp - gridDim.x" only issues the first tile (one issue site)
     int cur = 1;
     int kk_nxt = 0;  // kvec entry of this thread's line in the next group, loaded a group ahead
