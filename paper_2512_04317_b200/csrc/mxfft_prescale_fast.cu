@@ -61,6 +61,12 @@ constexpr int64_t FUSED_MAX = int64_t(1) << 18;
 #ifndef MXFFT_PS_SAMPLE_FIRST
 #define MXFFT_PS_SAMPLE_FIRST 1  // lean statistics: issue the sample loads before the L2 prefetch
 #endif
+#ifndef MXFFT_PS_FPREFETCH
+#define MXFFT_PS_FPREFETCH 4  // fused statistics (segments > 2^17 points): rounds prefetched into L2
+#endif
+#ifndef MXFFT_PS_HISTSEL
+#define MXFFT_PS_HISTSEL 1  // fused statistics: sample order statistics by histogram + exact in-bin rank (no sort)
+#endif
 #ifndef MXFFT_PS_PREFETCH
 #define MXFFT_PS_PREFETCH 4  // lean statistics: stream rounds prefetched into L2 ahead of the loads
 #endif
@@ -646,6 +652,81 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_ps_fused(const float2* __rest
         const int ilo = (int)floor(rs) - d, ihi = (int)ceil(rs) + 1 + d;
         if (S <= F_THREADS) {
             rank_select<unsigned, F_THREADS>(F.u.keys, S, ilo > 0 ? ilo : -1, ihi < n ? ihi : -1, n - 1, F.sel);
+        } else if (MXFFT_PS_HISTSEL) {
+            // the same three order statistics without sorting: a 512-bin
+            // histogram of key >> 22 finds the bins holding ranks ilo and ihi,
+            // then ranks are counted exactly among those bins' keys (the sort of
+            // 4096 keys took ~47k cycles on C3)
+            unsigned* l0 = reinterpret_cast<unsigned*>(F.cand);  // free until the stream
+            unsigned* l1 = l0 + SAMPLE_MAX;
+            unsigned kmax = 0;
+            for (int i = tid; i < S; i += F_THREADS) {
+                const unsigned k = F.u.keys[i];
+                if (k != 0xffffffffu) {
+                    atomicAdd(&F.hist[k >> 22], 1u);
+                    kmax = max(kmax, k);
+                }
+            }
+            for (int o = 16; o; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+            if (tid == 0) {
+                F.sel[2] = 0;
+                F.bt = F.bt1 = -1;
+                F.woff = F.wend = 0;  // (reused here: list lengths)
+            }
+            __syncthreads();
+            if (lane == 0) atomicMax(&F.sel[2], kmax);
+            {  // exclusive scan, one bin per thread (NBIN == 512 <= F_THREADS)
+                const unsigned h = tid < NBIN ? F.hist[tid] : 0u;
+                unsigned incl = h;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                if (lane == 31) F.warp_sums[tid >> 5] = incl;
+                __syncthreads();
+                unsigned base = incl - h;
+                for (int w = 0; w < (tid >> 5); ++w) base += F.warp_sums[w];
+                if (h && ilo > 0 && (unsigned)ilo >= base && (unsigned)ilo < base + h) {
+                    F.bt = tid;
+                    F.wn = (unsigned)ilo - base;  // rank within the bin
+                }
+                if (h && ihi < n && (unsigned)ihi >= base && (unsigned)ihi < base + h) {
+                    F.bt1 = tid;
+                    F.nnz = (unsigned)ihi - base;  // (reused: rank within the bin)
+                }
+            }
+            __syncthreads();
+            const int b0 = F.bt, b1 = F.bt1;
+            for (int i = tid; i < S; i += F_THREADS) {
+                const unsigned k = F.u.keys[i];
+                if (k == 0xffffffffu) continue;
+                if ((int)(k >> 22) == b0) l0[atomicAdd(&F.woff, 1u)] = k;
+                if ((int)(k >> 22) == b1) l1[atomicAdd(&F.wend, 1u)] = k;
+            }
+            __syncthreads();
+            const unsigned c0 = F.woff, c1 = F.wend, r0 = F.wn, r1 = F.nnz;
+            for (unsigned i = tid; i < c0; i += F_THREADS) {  // exact rank among the bin's keys
+                const unsigned e = l0[i];
+                unsigned lt = 0, eq = 0;
+                for (unsigned j = 0; j < c0; ++j) {
+                    lt += l0[j] < e;
+                    eq += l0[j] == e;
+                }
+                if (lt <= r0 && r0 < lt + eq) F.sel[0] = e;
+            }
+            for (unsigned i = tid; i < c1; i += F_THREADS) {
+                const unsigned e = l1[i];
+                unsigned lt = 0, eq = 0;
+                for (unsigned j = 0; j < c1; ++j) {
+                    lt += l1[j] < e;
+                    eq += l1[j] == e;
+                }
+                if (lt <= r1 && r1 < lt + eq) F.sel[1] = e;
+            }
+            for (int i = tid; i < NBIN; i += F_THREADS) F.hist[i] = 0;  // the select phase reuses it
+            if (tid == 0) F.wn = F.nnz = F.woff = F.wend = 0;
+            __syncthreads();
         } else {
             sort_block<unsigned, F_THREADS, SAMPLE_MAX / F_THREADS>(F.u.keys, S);
             if (tid == 0) {
@@ -681,6 +762,17 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_ps_fused(const float2* __rest
         const int64_t npairs = (npts / 2 - p_begin) < part ? (npts / 2 - p_begin) : part;
         const float4* x4 = reinterpret_cast<const float4*>(x) + p_begin;
         constexpr int64_t STEP = (int64_t)F_THREADS * F_UNR;
+        // bulk L2 prefetch MXFFT_PS_FPREFETCH rounds ahead (one thread): a lone CTA
+        // per SM (C3's few large segments) is otherwise bound by its loads in flight
+        constexpr int FPF = MXFFT_PS_FPREFETCH;
+        auto fprefetch = [&](int64_t b) {
+            if (FPF > 0 && tid == 0 && b < npairs) {
+                const int64_t cnt = npairs - b < STEP ? npairs - b : STEP;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x4 + b), "r"((unsigned)(cnt * 16))
+                             : "memory");
+            }
+        };
+        for (int r = 0; r < FPF; ++r) fprefetch((int64_t)r * STEP);
         float4 vn[F_UNR];  // next round's loads are in flight while this one is classified
 #pragma unroll
         for (int it = 0; it < F_UNR; ++it) {
@@ -688,6 +780,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_ps_fused(const float2* __rest
             vn[it] = pi < npairs ? __ldg(x4 + pi) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
         for (int64_t base = 0; base < npairs; base += STEP) {
+            fprefetch(base + (int64_t)FPF * STEP);
             float4 v[F_UNR];
 #pragma unroll
             for (int it = 0; it < F_UNR; ++it) {
