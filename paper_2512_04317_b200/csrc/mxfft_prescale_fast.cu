@@ -67,6 +67,9 @@ constexpr int64_t FUSED_MAX = int64_t(1) << 18;
 #ifndef MXFFT_PS_HISTSEL
 #define MXFFT_PS_HISTSEL 1  // fused statistics: sample order statistics by histogram + exact in-bin rank (no sort)
 #endif
+#ifndef MXFFT_PS_LEAN_S512
+#define MXFFT_PS_LEAN_S512 4096  // lean statistics, 512-thread variant: sample size
+#endif
 #ifndef MXFFT_PS_PREFETCH
 #define MXFFT_PS_PREFETCH 4  // lean statistics: stream rounds prefetched into L2 ahead of the loads
 #endif
@@ -1503,7 +1506,7 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
                 lattr = true;
             }
             if (npts > 32768)
-                k_ps_lean<512, 12, 1024, 1024><<<(unsigned)nseg, 512, sizeof(L512), st>>>(x, npts, 4096, q, c, out, kvec,
+                k_ps_lean<512, 12, 1024, 1024><<<(unsigned)nseg, 512, sizeof(L512), st>>>(x, npts, MXFFT_PS_LEAN_S512, q, c, out, kvec,
                                                                                      list, list_n);
             else
                 k_ps_lean<256, 12, 1024, 1024><<<(unsigned)nseg, 256, sizeof(L256), st>>>(x, npts, 1024, q, c, out, kvec,
