@@ -27,6 +27,7 @@
 #include "mxfft_common.cuh"
 #include "mxfft_generic.cuh"
 #include "mxfft_internal.h"
+#include <cooperative_groups.h>
 
 #ifndef MXFFT_PAIR_STORE
 #define MXFFT_PAIR_STORE 1  // strided copy-out: two adjacent lines per thread, 16-byte stores
@@ -48,6 +49,9 @@
 #endif
 #ifndef MXFFT_DEFER_COPYOUT
 #define MXFFT_DEFER_COPYOUT 0  // n <= 256 transposed stores: copy group g out during group g+1 (measured +1.5 % C2, +3 % C4: ptxas does not interleave it with the math)
+#endif
+#ifndef MXFFT_CL2
+#define MXFFT_CL2 0  // n = 8192/16384 plain row passes: a 2-CTA cluster per line (measured 3.52 vs 2.55 ms: off)
 #endif
 #ifndef MXFFT_PAIR_BATCH
 #define MXFFT_PAIR_BATCH 1  // paired strided copy-out: positions read from shared memory per batch of stores
@@ -1267,6 +1271,189 @@ __device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// n = 8192 / 16384 plain row passes on a 2-CTA cluster per line.  The first
+// L-1 stages of a radix-2 DIT transform on bit-reversed input act on the two
+// contiguous halves independently, and half r of the bit-reversed line is the
+// (n/2)-point transform of the decimated sequence x[2m + r] (the MX block and
+// twiddle structure of stages < L-1 do not depend on n: blocks never straddle
+// the halves, and the stage tables are the plan's own prefix).  So CTA r runs
+// the n/2-point kernel on x[r::2] with 256 (or 128) threads, both CTAs publish
+// their halves to shared memory, and the last stage (butterflies j and
+// n/2 + j) reads u from CTA 0 and v from CTA 1 through distributed shared
+// memory; CTA r takes j in [r n/4, (r+1) n/4).  Half a line plus the n/2
+// twiddle entries fit twice per SM, so one CTA's loads and stores overlap the
+// other's arithmetic (the one-CTA-per-line kernel cannot).  A line with any
+// block outside the fast exponent range is recomputed by both CTAs with the
+// reference-literal stages over the cluster's shared memory.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float2 lds64_cluster(unsigned addr) {
+    float2 v;
+    asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void lds128_cluster(unsigned addr, float2& a, float2& b) {
+    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(a.x), "=f"(a.y), "=f"(b.x), "=f"(b.y)
+                 : "r"(addr)
+                 : "memory");
+}
+__device__ __forceinline__ unsigned map_cluster(unsigned addr, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// exact recomputation of one line over the cluster's two regions (rare path)
+static __device__ __noinline__ void replay_line_cl2(const MxLinesArgs& a, int64_t line, char* reg0, char* reg1,
+                                                    int rank, int kin, int kout) {
+    const int n = a.n, m = n / 2, nthr = 2 * blockDim.x, tid = rank * blockDim.x + threadIdx.x;
+    auto acc = [reg0, reg1, m](int i) {
+        const int e = i < m ? i : i - m;
+        char* r = i < m ? reg0 : reg1;
+        return reinterpret_cast<float2*>(r + 16 * dsw(e >> 1) + 8 * (e & 1));
+    };
+    const int64_t base = line * n;
+    cluster_sync_all();  // both CTAs are done with their regions' normal contents
+    for (int i = tid; i < n; i += nthr) {
+        const int r = (int)(__brev((unsigned)i) >> (32 - a.log2n));
+        *acc(i) = gscale(a.in[base + r], kin);
+    }
+    cluster_sync_all();
+    for (int st = 0; st < a.log2n; ++st) {
+        generic_stage(acc, st, m, a.cpb, a.fmt, a.wcr, a.wci, a.wsexp, a.inverse != 0, tid, nthr);
+        cluster_sync_all();
+    }
+    for (int i = tid; i < n; i += nthr) a.out[base + i] = gscale(*acc(i), kout);
+    cluster_sync_all();
+}
+
+template <int ID, int CPB, int LT>  // LT: log2 of the threads per CTA (n / 64)
+__device__ __forceinline__ void lines_body_cl2(const MxLinesArgs& a) {
+    constexpr int T = 1 << LT, NH = 32 * T;  // threads per CTA, points per half line
+    constexpr int NB = CPB < 16 ? CPB : 16;
+    constexpr bool PAIR = CPB == 32;
+    const int n = 2 * NH;
+    extern __shared__ float4 smem4[];
+    unsigned* tw = reinterpret_cast<unsigned*>(smem4);
+    signed char* twe = reinterpret_cast<signed char*>(tw + NH);
+    const int tid = threadIdx.x;
+    const unsigned rank = cooperative_groups::this_cluster().block_rank();
+    load_twiddles<ID, CPB, false>(tw, twe, a, NH);  // stages < L-1: the plan table's prefix
+    LCtx L;
+    L.tw = tw;
+    L.twe = twe;
+    L.tw_sh = (unsigned)__cvta_generic_to_shared(tw);
+    L.lt = LT;
+    L.tl = tid;
+    L.c = (int)(__brev((unsigned)tid) >> (32 - LT));
+    L.trivial = a.trivial01;
+    L.sigma = a.inverse ? -1.f : 1.f;
+    L.slim = a.stage_limit;
+    const unsigned rb = (unsigned)__cvta_generic_to_shared(smem4 + a.tw_chunks);
+    if (rb & 127u) __trap();
+    char* const reg_mine = reinterpret_cast<char*>(smem4 + a.tw_chunks);
+    char* const reg_other = static_cast<char*>(cooperative_groups::this_cluster().map_shared_rank(
+        static_cast<void*>(reg_mine), rank ^ 1u));
+    char* const reg0 = rank ? reg_other : reg_mine;
+    char* const reg1 = rank ? reg_mine : reg_other;
+    const unsigned rb_u = map_cluster(rb, 0);  // CTA 0's region (u of the last stage)
+    const unsigned rb_v = map_cluster(rb, 1);  // CTA 1's region (v)
+    int& bad_flag = *reinterpret_cast<int*>(reg_mine + NH * 8);  // just past the region
+    const int64_t nclusters = gridDim.x / 2, cl = blockIdx.x / 2;
+    const int j0 = (int)rank * (NH / 2) + 16 * tid;  // last-stage butterflies of this thread
+    LDbg dbg;
+    __syncthreads();
+    for (int64_t line = cl; line < a.total_lines; line += nclusters) {
+        const int kk = a.kvec ? a.kvec[k_index(a, line)] : 0;
+        const int kin = a.kin_sign * kk + a.kin_const, kout = a.kout_sign * kk + a.kout_const;
+        float2 x[32];
+        bool bad = false;
+        {
+            // decimated half: sub-index m T + tid <- natural element 2 (m T + tid) + rank
+            const float2* src = a.in + line * n + rank + 2 * tid;
+#pragma unroll
+            for (int m = 0; m < 32; ++m) x[rev_c<5>(m)] = __ldg(src + (int64_t)m * 2 * T);
+            if (kin) scale32<false>(x, kin, bad);
+        }
+#if MXFFT_BIG_PREFETCH
+        if (tid < 2 && line + nclusters < a.total_lines) {  // this CTA's half of the next row into L2
+            const char* nx = reinterpret_cast<const char*>(a.in + (line + nclusters) * n);
+            const unsigned part = (unsigned)n * 2u;  // n * 8 bytes / 4 parts
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx + (size_t)(2 * rank + tid) * part),
+                         "r"(part)
+                         : "memory");
+        }
+#endif
+        int U, V, P, H;
+        run_stages<ID, CPB, false, LT>(x, U, V, P, H, L, rb, 0, &dbg, bad);
+        if (H > 0) publish4(x, rb, 0, P, H);
+        else publish2(x, rb, 0, U, V);
+        cluster_sync_all();  // both halves published
+        // last stage: butterflies j0 .. j0+15, u from CTA 0's half, v from CTA 1's
+        float2 u[16], v[16];
+        {
+            const Run ru = mkrun(rb_u, j0), rv = mkrun(rb_v, j0);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                lds128_cluster(ru.a0 + (ru.f ^ (unsigned)(k << 4)), u[2 * k], u[2 * k + 1]);
+                lds128_cluster(rv.a0 + (rv.f ^ (unsigned)(k << 4)), v[2 * k], v[2 * k + 1]);
+            }
+        }
+        unsigned w16[16];
+        {
+            const uint4* wp = reinterpret_cast<const uint4*>(a.tw16 + NH + j0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint4 q = __ldg(wp + i);
+                w16[4 * i] = q.x, w16[4 * i + 1] = q.y, w16[4 * i + 2] = q.z, w16[4 * i + 3] = q.w;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 16 / NB; ++k) {
+            float2 ub[NB], vb[NB];
+            unsigned wb[NB];
+#pragma unroll
+            for (int i = 0; i < NB; ++i) ub[i] = u[k * NB + i], vb[i] = v[k * NB + i], wb[i] = w16[k * NB + i];
+            mxb<ID, NB, PAIR ? 2 : 1, false>(ub, vb, wb, __ldg(a.twe + NH + j0 + k * NB), nullptr, 0, bad);
+#pragma unroll
+            for (int i = 0; i < NB; ++i) u[k * NB + i] = ub[i], v[k * NB + i] = vb[i];
+        }
+        if (kout) {  // undo_prescale / 1/n^2 (a power of two; non-normal factors replay)
+            bad |= !(kout >= -126 && kout <= 127);
+            const float f = exp2i(kout);
+            const float2 f2 = make_float2(f, f);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) u[i] = __fmul2_rn(u[i], f2), v[i] = __fmul2_rn(v[i], f2);
+        }
+        const int mine = __syncthreads_or(bad);
+        if (tid == 0) bad_flag = mine;
+        cluster_sync_all();  // last-stage reads of both regions done; flags visible
+        const int other = *static_cast<volatile int*>(
+            cooperative_groups::this_cluster().map_shared_rank(&bad_flag, rank ^ 1u));
+        if (mine | other) {
+            replay_line_cl2(a, line, reg0, reg1, (int)rank, kin, kout);
+            continue;
+        }
+        float2* du = a.out + line * n + j0;
+        float2* dv = du + NH;
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+            *reinterpret_cast<float4*>(du + i) = make_float4(u[i].x, u[i].y, u[i + 1].x, u[i + 1].y);
+            *reinterpret_cast<float4*>(dv + i) = make_float4(v[i].x, v[i].y, v[i + 1].x, v[i + 1].y);
+        }
+    }
+    cluster_sync_all();  // no CTA leaves while its partner may still read its region
+}
+
+template <int ID, int CPB, int LT>
+__global__ void __launch_bounds__(1 << LT, 2) k_mx_lines_cl2(MxLinesArgs a) {
+    lines_body_cl2<ID, CPB, LT>(a);
+}
+
 template <int ID, int CPB, bool DBG, int LT>
 __global__ void __launch_bounds__(128, MXFFT_LINES_MINB) k_mx_lines(MxLinesArgs a) {
     lines_body_pipe<ID, CPB, DBG, LT>(a);
@@ -1309,6 +1496,40 @@ static cudaError_t launch_t(const MxLinesArgs& a, size_t smem, cudaStream_t st) 
     return cudaGetLastError();
 }
 
+template <int ID, int CPB, int LT>
+static cudaError_t launch_cl2(const MxLinesArgs& a0, cudaStream_t st) {
+    static bool attr = false;
+    MxLinesArgs a = a0;
+    constexpr int NH = 32 << LT;
+    a.tw_chunks = ((NH * 5 + 1023) / 1024) * 64;
+    const size_t smem = (size_t)a.tw_chunks * 16 + (size_t)NH * 8 + 128;
+    auto k = k_mx_lines_cl2<ID, CPB, LT>;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t nclusters = a.total_lines < sms ? a.total_lines : sms;  // two CTAs per SM
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * nclusters));
+    cfg.blockDim = dim3(1u << LT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k, a);
+    note_launch();
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 // Specialised (compile-time n) variants: block sizes 16/32/64 (cpb 8..32),
 // n <= 4096.  Everything else -- smaller blocks, n = 8192/16384 and the
 // debug-capture kernels (test instrumentation, n <= 4096 only) -- runs the
@@ -1319,6 +1540,12 @@ static cudaError_t disp_lt(const MxLinesArgs& a, size_t smem, cudaStream_t st) {
         if constexpr (!DBG) {
             // n = 8192 / 16384 specialised (every stage, unconditional register stages)
             if constexpr (CPB >= 8) {
+#if MXFFT_CL2
+                if (!a.col_mode && !a.tstore && a.stage_limit >= a.log2n && a.prof_flags == 0) {
+                    if (a.log2T == 8) return launch_cl2<ID, CPB, 7>(a, st);
+                    if (a.log2T == 9) return launch_cl2<ID, CPB, 8>(a, st);
+                }
+#endif
                 if (!a.col_mode && a.stage_limit >= a.log2n) {
                     if (a.log2T == 8) return launch_t<ID, CPB, false, 8, true>(a, smem, st);
                     if (a.log2T == 9) return launch_t<ID, CPB, false, 9, true>(a, smem, st);
