@@ -53,6 +53,9 @@
 #ifndef MXFFT_CL2
 #define MXFFT_CL2 0  // n = 8192/16384 plain row passes: a 2-CTA cluster per line (measured 3.52 vs 2.55 ms: off)
 #endif
+#ifndef MXFFT_UNROLL_PAIRS
+#define MXFFT_UNROLL_PAIRS 0  // unroll the paired-stage loop for LT <= this (compile-time stage indices)
+#endif
 #ifndef MXFFT_PAIR_BATCH
 #define MXFFT_PAIR_BATCH 1  // paired strided copy-out: positions read from shared memory per batch of stores
 #endif
@@ -741,6 +744,15 @@ __device__ __forceinline__ void run_stages(float2 (&x)[32], int& U, int& V, int&
         publish2(x, rb, ebase, U, V);
         lsync(LT > 5);
         pair_stage<ID, CPB>(x, P, H, L, rb, ebase, s, LT > 5, bad);
+        if constexpr (LT <= MXFFT_UNROLL_PAIRS) {
+#pragma unroll
+            for (int s2 = (LT & 1) ? 8 : 7; s2 < LT + 5; s2 += 2) {
+                publish4(x, rb, ebase, P, H);
+                lsync(LT > 5);
+                pair_stage<ID, CPB>(x, P, H, L, rb, ebase, s2, LT > 5, bad);
+            }
+            return;
+        }
 #pragma unroll 1
         for (s += 2; s < LT + 5; s += 2) {
             publish4(x, rb, ebase, P, H);
