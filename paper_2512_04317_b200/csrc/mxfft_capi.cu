@@ -294,6 +294,7 @@ int32_t mxfft_fft2(mxfft_plan plan, const void* x, void* y, int64_t batch, int32
         lp.total_lines = batch * p.n;
         lp.batch = batch;
         lp.inverse = mode == 1 || (mode == 2 && pass >= 2);
+        lp.reverse = !split_t && (pass & 1);  // read the previous pass's output newest first
         lp.kvec = d_k;
         lp.k_group = k_group > 0 ? k_group : 1;
         if (pass == 0 && d_k) lp.kin_sign = 1;

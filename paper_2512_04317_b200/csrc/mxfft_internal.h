@@ -38,6 +38,7 @@ struct LinePass {
     int k_group = 1;
     int kin_sign = 0, kout_sign = 0, kout_const = 0, kin_const = 0;
     int stage_limit = -1;
+    int reverse = 0;  // walk the groups last to first (the previous pass's latest output is still in L2)
     int32_t* d_vexp = nullptr;
     float* d_vcodes = nullptr;
     int32_t* d_pexp = nullptr;
@@ -58,6 +59,7 @@ struct MxLinesArgs {
     const int32_t* kvec;
     int k_group, kin_sign, kout_sign, kout_const, kin_const, stage_limit;
     int lpi_shift;  // log2(lines_per_image) when it is a power of two, else -1
+    int reverse;    // group order last to first
     int prof_flags;  // profiling only: bit 0 skip tile loads, bit 1 skip stores
     int tw_chunks;
     // exact replay (replay_lines): reference-literal tables of the plan

@@ -3,6 +3,10 @@
 #include "mxfft_common.cuh"
 #include "mxfft_internal.h"
 
+#ifndef MXFFT_REVERSE_PASSES
+#define MXFFT_REVERSE_PASSES 1  // fft2: every second pass walks its groups backwards (L2 reuse)
+#endif
+
 namespace mxfft {
 
 cudaError_t run_mx_lines_e4m3(const MxLinesArgs&, int, size_t, cudaStream_t);
@@ -65,6 +69,7 @@ cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
     a.inverse = lp.inverse;
     a.kvec = lp.kvec;
     a.k_group = lp.k_group > 0 ? lp.k_group : 1;
+    a.reverse = lp.reverse && MXFFT_REVERSE_PASSES;
     a.lpi_shift = -1;
     if (a.lines_per_image > 0 && (a.lines_per_image & (a.lines_per_image - 1)) == 0)
         for (a.lpi_shift = 0; (1 << a.lpi_shift) < a.lines_per_image; ++a.lpi_shift) {

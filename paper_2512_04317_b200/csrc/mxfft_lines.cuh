@@ -942,8 +942,9 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
     // column-mode loads (mxfft_fft_cols / fft2 without workspace) only in the
     // run-time-n variant: the specialised kernels stay small
     const bool col_in = LT < 0 && a.col_mode;
-    auto issue_tile = [&](int64_t grp, unsigned buf) {
+    auto issue_tile = [&](int64_t grp_, unsigned buf) {
         if (a.prof_flags & 1) return;
+        const int64_t grp = a.reverse ? ngroups - 1 - grp_ : grp_;
         if (!col_in) {
             const int64_t base = grp * LPC * (int64_t)N;
             const float4* src = reinterpret_cast<const float4*>(a.in + base) + tid;
@@ -978,7 +979,7 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
     // shared-memory reads and global stores with that arithmetic.  Group g+2's
     // tile is then issued into the freed buffer after stage 1.
     if constexpr (LT >= 0 && LT <= MXFFT_PAIR_STORE_MAXLT && !DBG && MXFFT_PAIR_STORE) {
-        if (a.tstore && !a.col_mode && !(a.prof_flags & 3)) {
+        if (a.tstore && !a.col_mode && !(a.prof_flags & 3) && !a.reverse) {
             auto copy_out = [&](int64_t g, unsigned bsrc) {
                 const int64_t gl = g * LPC + 2 * pa;
                 const bool v2 = g >= 0 && gl + 1 < a.total_lines;         // both lines of the pair
@@ -1052,8 +1053,8 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
     // iteration "grp - gridDim.x" only issues the first tile (one issue site)
     int cur = 1;
     int kk_nxt = 0;  // kvec entry of this thread's line in the next group, loaded a group ahead
-    for (int64_t grp = (int64_t)blockIdx.x - gridDim.x; grp < ngroups; grp += gridDim.x) {
-        const int64_t nxt = grp + gridDim.x;
+    for (int64_t grp_it = (int64_t)blockIdx.x - gridDim.x; grp_it < ngroups; grp_it += gridDim.x) {
+        const int64_t nxt = grp_it + gridDim.x;
         const unsigned bcur = buf0 + (unsigned)cur * BUFSZ, bnxt = buf0 + (unsigned)(cur ^ 1) * BUFSZ;
         cur ^= 1;
         __syncthreads();  // the other buffer's previous readers are done
@@ -1062,11 +1063,12 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
 #if MXFFT_KPREF
         const int kk = kk_nxt;
         if (a.kvec && nxt < ngroups) {
-            const int64_t nl = nxt * LPC + lj;
+            const int64_t nl = (a.reverse ? ngroups - 1 - nxt : nxt) * LPC + lj;
             kk_nxt = nl < a.total_lines ? __ldg(a.kvec + k_index(a, nl)) : 0;
         }
 #endif
-        if (grp < 0) continue;
+        if (grp_it < 0) continue;
+        const int64_t grp = a.reverse ? ngroups - 1 - grp_it : grp_it;
         cp_wait<1>();     // this thread's copies of group grp have landed
         __syncthreads();  // ... and everybody's
 
