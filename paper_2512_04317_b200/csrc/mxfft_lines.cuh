@@ -56,6 +56,9 @@
 #ifndef MXFFT_UNROLL_PAIRS
 #define MXFFT_UNROLL_PAIRS 0  // unroll the paired-stage loop for LT <= this (compile-time stage indices)
 #endif
+#ifndef MXFFT_SINGLE_BUF
+#define MXFFT_SINGLE_BUF 0  // one tile buffer per CTA + L2 prefetch of the next tile (build with MXFFT_NBUF=1)
+#endif
 #ifndef MXFFT_PAIR_BATCH
 #define MXFFT_PAIR_BATCH 1  // paired strided copy-out: positions read from shared memory per batch of stores
 #endif
@@ -1050,32 +1053,8 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
         }
     }
 #endif
-    // iteration "grp - gridDim.x" only issues the first tile (one issue site)
-    int cur = 1;
-    int kk_nxt = 0;  // kvec entry of this thread's line in the next group, loaded a group ahead
-    for (int64_t grp_it = (int64_t)blockIdx.x - gridDim.x; grp_it < ngroups; grp_it += gridDim.x) {
-        const int64_t nxt = grp_it + gridDim.x;
-        const unsigned bcur = buf0 + (unsigned)cur * BUFSZ, bnxt = buf0 + (unsigned)(cur ^ 1) * BUFSZ;
-        cur ^= 1;
-        __syncthreads();  // the other buffer's previous readers are done
-        if (nxt < ngroups) issue_tile(nxt, bnxt);
-        cp_commit();
-#if MXFFT_KPREF
-        const int kk = kk_nxt;
-        if (a.kvec && nxt < ngroups) {
-            const int64_t nl = (a.reverse ? ngroups - 1 - nxt : nxt) * LPC + lj;
-            kk_nxt = nl < a.total_lines ? __ldg(a.kvec + k_index(a, nl)) : 0;
-        }
-#endif
-        if (grp_it < 0) continue;
-        const int64_t grp = a.reverse ? ngroups - 1 - grp_it : grp_it;
-        cp_wait<1>();     // this thread's copies of group grp have landed
-        __syncthreads();  // ... and everybody's
-
+    auto body = [&](const int64_t grp, const unsigned bcur, const int kk) {
         const int64_t line = grp * LPC + lj;
-#if !MXFFT_KPREF
-        const int kk = a.kvec && line < a.total_lines ? a.kvec[k_index(a, line)] : 0;
-#endif
         const int kin = a.kin_const + a.kin_sign * kk, kout = a.kout_const + a.kout_sign * kk;
         if (DBG) dbg.row = line;
 
@@ -1162,6 +1141,59 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
 #endif
             }
         }
+    };
+#if MXFFT_SINGLE_BUF
+    // one tile buffer per CTA (more CTAs per SM); the next tile is prefetched
+    // into L2 only, so its load into shared memory is short
+    for (int64_t grp_it = blockIdx.x; grp_it < ngroups; grp_it += gridDim.x) {
+        const int64_t grp = a.reverse ? ngroups - 1 - grp_it : grp_it;
+        __syncthreads();  // the previous group's copy-out reads are done
+        issue_tile(grp_it, buf0);
+        cp_commit();
+        const int64_t nx = grp_it + gridDim.x;
+        if (tid == 0 && nx < ngroups && !col_in) {
+            const int64_t g2 = a.reverse ? ngroups - 1 - nx : nx;
+            const int64_t b2 = g2 * LPC * (int64_t)N;
+            const int64_t left = a.total_lines * (int64_t)N - b2;
+            const int64_t cnt = left < (int64_t)GEL ? left : (int64_t)GEL;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.in + b2), "r"((unsigned)(cnt * 8))
+                         : "memory");
+        }
+        const int64_t l0 = grp * LPC + lj;
+        const int kk = a.kvec && l0 < a.total_lines ? __ldg(a.kvec + k_index(a, l0)) : 0;
+        cp_wait<0>();
+        __syncthreads();
+        body(grp, buf0, kk);
+    }
+    cp_wait<0>();
+    return;
+#endif
+    // iteration "grp - gridDim.x" only issues the first tile (one issue site)
+    int cur = 1;
+    int kk_nxt = 0;  // kvec entry of this thread's line in the next group, loaded a group ahead
+    for (int64_t grp_it = (int64_t)blockIdx.x - gridDim.x; grp_it < ngroups; grp_it += gridDim.x) {
+        const int64_t nxt = grp_it + gridDim.x;
+        const unsigned bcur = buf0 + (unsigned)cur * BUFSZ, bnxt = buf0 + (unsigned)(cur ^ 1) * BUFSZ;
+        cur ^= 1;
+        __syncthreads();  // the other buffer's previous readers are done
+        if (nxt < ngroups) issue_tile(nxt, bnxt);
+        cp_commit();
+#if MXFFT_KPREF
+        const int kk = kk_nxt;
+        if (a.kvec && nxt < ngroups) {
+            const int64_t nl = (a.reverse ? ngroups - 1 - nxt : nxt) * LPC + lj;
+            kk_nxt = nl < a.total_lines ? __ldg(a.kvec + k_index(a, nl)) : 0;
+        }
+#endif
+        if (grp_it < 0) continue;
+        const int64_t grp = a.reverse ? ngroups - 1 - grp_it : grp_it;
+        cp_wait<1>();     // this thread's copies of group grp have landed
+        __syncthreads();  // ... and everybody's
+#if !MXFFT_KPREF
+        const int64_t l0 = grp * LPC + lj;
+        const int kk = a.kvec && l0 < a.total_lines ? a.kvec[k_index(a, l0)] : 0;
+#endif
+        body(grp, bcur, kk);
     }
     cp_wait<0>();
 }
