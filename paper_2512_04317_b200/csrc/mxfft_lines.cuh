@@ -59,6 +59,9 @@
 #ifndef MXFFT_SINGLE_BUF
 #define MXFFT_SINGLE_BUF 0  // one tile buffer per CTA + L2 prefetch of the next tile (build with MXFFT_NBUF=1)
 #endif
+#ifndef MXFFT_INTERLEAVE_GATHER
+#define MXFFT_INTERLEAVE_GATHER 0  // n <= 256 transposed stores: copy-out of g interleaved with the gather of g+G (measured neutral: off)
+#endif
 #ifndef MXFFT_PAIR_BATCH
 #define MXFFT_PAIR_BATCH 1  // paired strided copy-out: positions read from shared memory per batch of stores
 #endif
@@ -975,6 +978,82 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
         }
     };
 
+#if MXFFT_INTERLEAVE_GATHER
+    // n <= 256 transposed-store passes: the copy-out of group g and the gather
+    // of group g+G (already in the other buffer) are written interleaved, so the
+    // gather's shared-memory loads issue while the copy-out's stores wait on
+    // their data
+    if constexpr (LT >= 0 && LT <= MXFFT_PAIR_STORE_MAXLT && !DBG && MXFFT_PAIR_STORE) {
+        if (a.tstore && !a.col_mode && !(a.prof_flags & 3)) {
+            auto gidx = [&](int64_t it) { return a.reverse ? ngroups - 1 - it : it; };
+            int cur = 0;
+            int kk = 0;
+            float2 x[32];
+            const int64_t g0 = blockIdx.x;
+            if (g0 < ngroups) {
+                issue_tile(g0, buf0);
+                const int64_t nl = gidx(g0) * LPC + lj;
+                if (a.kvec && nl < a.total_lines) kk = __ldg(a.kvec + k_index(a, nl));
+            }
+            cp_commit();
+            cp_wait<0>();
+            __syncthreads();
+#pragma unroll
+            for (int m = 0; m < 32; ++m)
+                x[rev_c<5>(m)] = AX ? lds64(caddr(buf0, gch, gh) ^ (16u * (unsigned)dsw((m * T) >> 1)))
+                                    : lds64(caddr(buf0, gch ^ dsw((m * T) >> 1), lt ? gh : (m & 1)));
+            for (int64_t it = g0; it < ngroups; it += gridDim.x) {
+                const int64_t grp = gidx(it), nxt = it + gridDim.x;
+                const unsigned bcur = buf0 + (unsigned)cur * BUFSZ, bnxt = buf0 + (unsigned)(cur ^ 1) * BUFSZ;
+                __syncthreads();  // the copy-out of the group before last has left bnxt
+                int kk_nxt = 0;
+                if (nxt < ngroups) {
+                    issue_tile(nxt, bnxt);
+                    const int64_t nl = gidx(nxt) * LPC + lj;
+                    if (a.kvec && nl < a.total_lines) kk_nxt = __ldg(a.kvec + k_index(a, nl));
+                }
+                cp_commit();
+                const int kin = a.kin_const + a.kin_sign * kk, kout = a.kout_const + a.kout_sign * kk;
+                bool bad = false;
+                if (kin) scale32<DBG>(x, kin, bad);
+                int U, V, P, H;
+                run_stages<ID, CPB, DBG, LT>(x, U, V, P, H, L, bcur, ebase, &dbg, bad);
+                if (kout) scale32<DBG>(x, kout, bad);
+                if (__syncthreads_or(bad)) {
+                    replay_lines(a, grp * LPC, LPC, tile_g + (bcur - buf0), lt > 5 ? 0 : 5 - lt, W * 32, LPR - 1);
+                } else if (H > 0) {
+                    publish4(x, bcur, ebase, P, H);
+                } else {
+                    publish2(x, bcur, ebase, U, V);
+                }
+                cp_wait<0>();     // tile nxt has landed (this thread's copies) ...
+                __syncthreads();  // ... everybody's, and the results of grp are published
+                // copy-out of grp, interleaved with the gather of nxt
+                const int64_t gl = grp * LPC + 2 * pa;
+                const bool v2 = gl + 1 < a.total_lines, v1 = gl < a.total_lines && !v2;
+                const int64_t img = gl >> LN;
+                float4* dst = reinterpret_cast<float4*>(a.out + img * (int64_t)N * N + (int64_t)pq0 * N + (gl & (N - 1)));
+                const int64_t rs = (int64_t)T * N;
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const unsigned c16 = 16u * (unsigned)dsw(T * k);
+                    const float2 v0 = AX ? lds64(caddr(bcur, pch0, ph0) ^ c16) : lds64(caddr(bcur, pch0 ^ dsw(T * k), ph0));
+                    const float2 w0 = AX ? lds64(caddr(bcur, pch1, ph1) ^ c16) : lds64(caddr(bcur, pch1 ^ dsw(T * k), ph1));
+#pragma unroll
+                    for (int m = 2 * k; m < 2 * k + 2; ++m)  // (after the last group: unused reads)
+                        x[rev_c<5>(m)] = AX ? lds64(caddr(bnxt, gch, gh) ^ (16u * (unsigned)dsw((m * T) >> 1)))
+                                            : lds64(caddr(bnxt, gch ^ dsw((m * T) >> 1), lt ? gh : (m & 1)));
+                    if (v2) dst[k * rs] = make_float4(v0.x, v0.y, w0.x, w0.y);
+                    if (v1) *reinterpret_cast<float2*>(dst + k * rs) = v0;
+                }
+                cur ^= 1;
+                kk = kk_nxt;
+            }
+            cp_wait<0>();
+            return;
+        }
+    }
+#endif
 #if MXFFT_DEFER_COPYOUT
     // n <= 256 transposed-store passes: group g's results stay in its buffer and
     // leave while group g+1's first two (register) stages compute -- the copy-out
