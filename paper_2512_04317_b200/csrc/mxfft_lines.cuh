@@ -47,20 +47,11 @@
 #ifndef MXFFT_PAIR_STORE_MAXLT
 #define MXFFT_PAIR_STORE_MAXLT 3  // paired strided copy-out up to n = 32 * 2^LT (n = 512 measured 13 % slower)
 #endif
-#ifndef MXFFT_DEFER_COPYOUT
-#define MXFFT_DEFER_COPYOUT 0  // n <= 256 transposed stores: copy group g out during group g+1 (measured +1.5 % C2, +3 % C4: ptxas does not interleave it with the math)
-#endif
 #ifndef MXFFT_CL2
 #define MXFFT_CL2 0  // n = 8192/16384 plain row passes: a 2-CTA cluster per line (measured 3.52 vs 2.55 ms: off)
 #endif
 #ifndef MXFFT_UNROLL_PAIRS
 #define MXFFT_UNROLL_PAIRS 0  // unroll the paired-stage loop for LT <= this (compile-time stage indices)
-#endif
-#ifndef MXFFT_SINGLE_BUF
-#define MXFFT_SINGLE_BUF 0  // one tile buffer per CTA + L2 prefetch of the next tile (build with MXFFT_NBUF=1)
-#endif
-#ifndef MXFFT_INTERLEAVE_GATHER
-#define MXFFT_INTERLEAVE_GATHER 0  // n <= 256 transposed stores: copy-out of g interleaved with the gather of g+G (measured neutral: off)
 #endif
 #ifndef MXFFT_PAIR_BATCH
 #define MXFFT_PAIR_BATCH 1  // paired strided copy-out: positions read from shared memory per batch of stores
@@ -710,13 +701,9 @@ __device__ __forceinline__ void pair_stage(float2 (&x)[32], int& P, int& H, cons
 // address rb lives in chunk dsw(e/2), half e&1).  On return x[0..15] sit at
 // line positions U.., x[16..31] at V.. (H == 0), or -- after paired stages --
 // x[8k..8k+7] at P + k H (H > 0).
-struct NoHook {
-    __device__ __forceinline__ void operator()() const {}
-};
-
-template <int ID, int CPB, bool DBG, int LT, class Mid = NoHook>
+template <int ID, int CPB, bool DBG, int LT>
 __device__ __forceinline__ void run_stages(float2 (&x)[32], int& U, int& V, int& P, int& H, const LCtx& L,
-                                           unsigned rb, int ebase, LDbg* dbg, bool& bad, const Mid& mid = Mid()) {
+                                           unsigned rb, int ebase, LDbg* dbg, bool& bad) {
     const int lt = LT >= 0 ? LT : L.lt;
     const bool big = lt > 5;  // a line spans several warps
     constexpr int LOCAL = MXFFT_LOCAL_STAGES;  // unrolled register stages (4 or 5)
@@ -727,7 +714,6 @@ __device__ __forceinline__ void run_stages(float2 (&x)[32], int& U, int& V, int&
     const int lim_loc = FULL ? LOCAL : (L.slim < LOCAL ? L.slim : LOCAL);
     if (lim_loc > 0) local_stage<ID, CPB, 0, DBG>(x, L.tw, L.twe, L.c, L.trivial, L.sigma, dbg, bad);
     if (lim_loc > 1) local_stage<ID, CPB, 1, DBG>(x, L.tw, L.twe, L.c, L.trivial, L.sigma, dbg, bad);
-    mid();  // (deferred copy-out: the previous group's buffer is free from here on)
     if (lim_loc > 2) local_stage<ID, CPB, 2, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg, bad);
     if (lim_loc > 3) local_stage<ID, CPB, 3, DBG>(x, L.tw, L.twe, L.c, false, L.sigma, dbg, bad);
     if constexpr (LOCAL > 4)
@@ -978,160 +964,6 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
         }
     };
 
-#if MXFFT_INTERLEAVE_GATHER
-    // n <= 256 transposed-store passes: the copy-out of group g and the gather
-    // of group g+G (already in the other buffer) are written interleaved, so the
-    // gather's shared-memory loads issue while the copy-out's stores wait on
-    // their data
-    if constexpr (LT >= 0 && LT <= MXFFT_PAIR_STORE_MAXLT && !DBG && MXFFT_PAIR_STORE) {
-        if (a.tstore && !a.col_mode && !(a.prof_flags & 3)) {
-            auto gidx = [&](int64_t it) { return a.reverse ? ngroups - 1 - it : it; };
-            int cur = 0;
-            int kk = 0;
-            float2 x[32];
-            const int64_t g0 = blockIdx.x;
-            if (g0 < ngroups) {
-                issue_tile(g0, buf0);
-                const int64_t nl = gidx(g0) * LPC + lj;
-                if (a.kvec && nl < a.total_lines) kk = __ldg(a.kvec + k_index(a, nl));
-            }
-            cp_commit();
-            cp_wait<0>();
-            __syncthreads();
-#pragma unroll
-            for (int m = 0; m < 32; ++m)
-                x[rev_c<5>(m)] = AX ? lds64(caddr(buf0, gch, gh) ^ (16u * (unsigned)dsw((m * T) >> 1)))
-                                    : lds64(caddr(buf0, gch ^ dsw((m * T) >> 1), lt ? gh : (m & 1)));
-            for (int64_t it = g0; it < ngroups; it += gridDim.x) {
-                const int64_t grp = gidx(it), nxt = it + gridDim.x;
-                const unsigned bcur = buf0 + (unsigned)cur * BUFSZ, bnxt = buf0 + (unsigned)(cur ^ 1) * BUFSZ;
-                __syncthreads();  // the copy-out of the group before last has left bnxt
-                int kk_nxt = 0;
-                if (nxt < ngroups) {
-                    issue_tile(nxt, bnxt);
-                    const int64_t nl = gidx(nxt) * LPC + lj;
-                    if (a.kvec && nl < a.total_lines) kk_nxt = __ldg(a.kvec + k_index(a, nl));
-                }
-                cp_commit();
-                const int kin = a.kin_const + a.kin_sign * kk, kout = a.kout_const + a.kout_sign * kk;
-                bool bad = false;
-                if (kin) scale32<DBG>(x, kin, bad);
-                int U, V, P, H;
-                run_stages<ID, CPB, DBG, LT>(x, U, V, P, H, L, bcur, ebase, &dbg, bad);
-                if (kout) scale32<DBG>(x, kout, bad);
-                if (__syncthreads_or(bad)) {
-                    replay_lines(a, grp * LPC, LPC, tile_g + (bcur - buf0), lt > 5 ? 0 : 5 - lt, W * 32, LPR - 1);
-                } else if (H > 0) {
-                    publish4(x, bcur, ebase, P, H);
-                } else {
-                    publish2(x, bcur, ebase, U, V);
-                }
-                cp_wait<0>();     // tile nxt has landed (this thread's copies) ...
-                __syncthreads();  // ... everybody's, and the results of grp are published
-                // copy-out of grp, interleaved with the gather of nxt
-                const int64_t gl = grp * LPC + 2 * pa;
-                const bool v2 = gl + 1 < a.total_lines, v1 = gl < a.total_lines && !v2;
-                const int64_t img = gl >> LN;
-                float4* dst = reinterpret_cast<float4*>(a.out + img * (int64_t)N * N + (int64_t)pq0 * N + (gl & (N - 1)));
-                const int64_t rs = (int64_t)T * N;
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const unsigned c16 = 16u * (unsigned)dsw(T * k);
-                    const float2 v0 = AX ? lds64(caddr(bcur, pch0, ph0) ^ c16) : lds64(caddr(bcur, pch0 ^ dsw(T * k), ph0));
-                    const float2 w0 = AX ? lds64(caddr(bcur, pch1, ph1) ^ c16) : lds64(caddr(bcur, pch1 ^ dsw(T * k), ph1));
-#pragma unroll
-                    for (int m = 2 * k; m < 2 * k + 2; ++m)  // (after the last group: unused reads)
-                        x[rev_c<5>(m)] = AX ? lds64(caddr(bnxt, gch, gh) ^ (16u * (unsigned)dsw((m * T) >> 1)))
-                                            : lds64(caddr(bnxt, gch ^ dsw((m * T) >> 1), lt ? gh : (m & 1)));
-                    if (v2) dst[k * rs] = make_float4(v0.x, v0.y, w0.x, w0.y);
-                    if (v1) *reinterpret_cast<float2*>(dst + k * rs) = v0;
-                }
-                cur ^= 1;
-                kk = kk_nxt;
-            }
-            cp_wait<0>();
-            return;
-        }
-    }
-#endif
-#if MXFFT_DEFER_COPYOUT
-    // n <= 256 transposed-store passes: group g's results stay in its buffer and
-    // leave while group g+1's first two (register) stages compute -- the copy-out
-    // is branch-free (predicated stores) so the compiler can interleave its
-    // shared-memory reads and global stores with that arithmetic.  Group g+2's
-    // tile is then issued into the freed buffer after stage 1.
-    if constexpr (LT >= 0 && LT <= MXFFT_PAIR_STORE_MAXLT && !DBG && MXFFT_PAIR_STORE) {
-        if (a.tstore && !a.col_mode && !(a.prof_flags & 3) && !a.reverse) {
-            auto copy_out = [&](int64_t g, unsigned bsrc) {
-                const int64_t gl = g * LPC + 2 * pa;
-                const bool v2 = g >= 0 && gl + 1 < a.total_lines;         // both lines of the pair
-                const bool v1 = g >= 0 && gl < a.total_lines && !v2;      // only the first
-                const int64_t glc = g >= 0 ? gl : 0;
-                const int64_t img = glc >> LN;
-                float4* dst = reinterpret_cast<float4*>(a.out + img * (int64_t)N * N + (int64_t)pq0 * N + (glc & (N - 1)));
-                const int64_t rs = (int64_t)T * N;
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const unsigned c16 = 16u * (unsigned)dsw(T * k);
-                    const float2 v0 = AX ? lds64(caddr(bsrc, pch0, ph0) ^ c16) : lds64(caddr(bsrc, pch0 ^ dsw(T * k), ph0));
-                    const float2 v1v = AX ? lds64(caddr(bsrc, pch1, ph1) ^ c16) : lds64(caddr(bsrc, pch1 ^ dsw(T * k), ph1));
-                    if (v2) dst[k * rs] = make_float4(v0.x, v0.y, v1v.x, v1v.y);
-                    if (v1) *reinterpret_cast<float2*>(dst + k * rs) = v0;
-                }
-            };
-            int cur = 0;
-            int kk = 0, kk_nxt = 0;
-            if ((int64_t)blockIdx.x < ngroups) {
-                issue_tile(blockIdx.x, buf0);
-                const int64_t nl = (int64_t)blockIdx.x * LPC + lj;
-                if (a.kvec && nl < a.total_lines) kk = __ldg(a.kvec + k_index(a, nl));
-            }
-            cp_commit();
-            int64_t prev = -1;
-            for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-                const unsigned bcur = buf0 + (unsigned)cur * BUFSZ, both = buf0 + (unsigned)(cur ^ 1) * BUFSZ;
-                cp_wait<0>();     // this thread's copies of group grp have landed
-                __syncthreads();  // ... everybody's, and group prev's results are published
-                const int kin = a.kin_const + a.kin_sign * kk, kout = a.kout_const + a.kout_sign * kk;
-                float2 x[32];
-                bool bad = false;
-#pragma unroll
-                for (int m = 0; m < 32; ++m)
-                    x[rev_c<5>(m)] = AX ? lds64(caddr(bcur, gch, gh) ^ (16u * (unsigned)dsw((m * T) >> 1)))
-                                        : lds64(caddr(bcur, gch ^ dsw((m * T) >> 1), lt ? gh : (m & 1)));
-                if (kin) scale32<DBG>(x, kin, bad);
-                copy_out(prev, both);  // group prev leaves while stages 0-1 of grp compute
-                const int64_t nxt = grp + gridDim.x;
-                auto mid = [&]() {
-                    __syncthreads();  // everybody has read group prev out of 'both'
-                    if (nxt < ngroups) {
-                        issue_tile(nxt, both);
-                        const int64_t nl = nxt * LPC + lj;
-                        kk_nxt = a.kvec && nl < a.total_lines ? __ldg(a.kvec + k_index(a, nl)) : 0;
-                    }
-                    cp_commit();
-                };
-                int U, V, P, H;
-                run_stages<ID, CPB, DBG, LT>(x, U, V, P, H, L, bcur, ebase, &dbg, bad, mid);
-                if (kout) scale32<DBG>(x, kout, bad);
-                if (__syncthreads_or(bad)) {
-                    replay_lines(a, grp * LPC, LPC, tile_g + (bcur - buf0), lt > 5 ? 0 : 5 - lt, W * 32, LPR - 1);
-                } else if (H > 0) {
-                    publish4(x, bcur, ebase, P, H);
-                } else {
-                    publish2(x, bcur, ebase, U, V);
-                }
-                prev = grp;
-                cur ^= 1;
-                kk = kk_nxt;
-            }
-            __syncthreads();
-            copy_out(prev, buf0 + (unsigned)(cur ^ 1) * BUFSZ);
-            cp_wait<0>();
-            return;
-        }
-    }
-#endif
     auto body = [&](const int64_t grp, const unsigned bcur, const int kk) {
         const int64_t line = grp * LPC + lj;
         const int kin = a.kin_const + a.kin_sign * kk, kout = a.kout_const + a.kout_sign * kk;
@@ -1221,32 +1053,6 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
             }
         }
     };
-#if MXFFT_SINGLE_BUF
-    // one tile buffer per CTA (more CTAs per SM); the next tile is prefetched
-    // into L2 only, so its load into shared memory is short
-    for (int64_t grp_it = blockIdx.x; grp_it < ngroups; grp_it += gridDim.x) {
-        const int64_t grp = a.reverse ? ngroups - 1 - grp_it : grp_it;
-        __syncthreads();  // the previous group's copy-out reads are done
-        issue_tile(grp_it, buf0);
-        cp_commit();
-        const int64_t nx = grp_it + gridDim.x;
-        if (tid == 0 && nx < ngroups && !col_in) {
-            const int64_t g2 = a.reverse ? ngroups - 1 - nx : nx;
-            const int64_t b2 = g2 * LPC * (int64_t)N;
-            const int64_t left = a.total_lines * (int64_t)N - b2;
-            const int64_t cnt = left < (int64_t)GEL ? left : (int64_t)GEL;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.in + b2), "r"((unsigned)(cnt * 8))
-                         : "memory");
-        }
-        const int64_t l0 = grp * LPC + lj;
-        const int kk = a.kvec && l0 < a.total_lines ? __ldg(a.kvec + k_index(a, l0)) : 0;
-        cp_wait<0>();
-        __syncthreads();
-        body(grp, buf0, kk);
-    }
-    cp_wait<0>();
-    return;
-#endif
     // iteration "grp - gridDim.x" only issues the first tile (one issue site)
     int cur = 1;
     int kk_nxt = 0;  // kvec entry of this thread's line in the next group, loaded a group ahead
