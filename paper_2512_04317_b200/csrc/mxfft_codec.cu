@@ -225,9 +225,47 @@ __global__ void k_rss(const T* __restrict__ x, int64_t groups, int coils, int64_
 // (np.ascontiguousarray(rows.T), fftcore.py:352): 64 x 64 tiles through
 // shared memory; every global access is a 512-byte warp-contiguous run.
 constexpr int TT = 64;
+#ifndef MXFFT_TRANSPOSE_V2
+#define MXFFT_TRANSPOSE_V2 1  // 16-byte global accesses, XOR-swizzled tile (when everything is 16-byte aligned)
+#endif
+template <bool V2>
 __global__ void __launch_bounds__(256) k_transpose_c64(const float2* __restrict__ x, float2* __restrict__ y,
                                                        int n, int tiles_per_dim, int64_t ntiles, int64_t ldx,
                                                        int64_t bsx) {
+if constexpr (V2) {
+    // Each warp moves whole 512-byte rows as float4 (two complex per thread).
+    // Tile element (r, c) lives at column c ^ ((r >> 1) & 15): a half-warp of
+    // the store pass reads column k of rows 2l (or 2l + 1), l < 16, which then
+    // hit 16 different 8-byte bank slots.
+    __shared__ float2 tile[TT][TT];
+    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;  // 32 lanes x 8 warps
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t per = (int64_t)tiles_per_dim * tiles_per_dim;
+        const int64_t b = t / per;
+        const int r = (int)(t - b * per);
+        const int i0 = (r / tiles_per_dim) * TT, j0 = (r % tiles_per_dim) * TT;
+        const float2* xb = x + b * bsx;
+        float2* yb = y + b * (int64_t)n * n;
+        float4 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)  // rows w + 8q, columns 2l, 2l + 1
+            v[q] = __ldg(reinterpret_cast<const float4*>(xb + (int64_t)(i0 + w + 8 * q) * ldx + j0) + l);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int rr = w + 8 * q, f = (rr >> 1) & 15;
+            tile[rr][(2 * l) ^ f] = make_float2(v[q].x, v[q].y);
+            tile[rr][(2 * l + 1) ^ f] = make_float2(v[q].z, v[q].w);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {  // output row j0 + k, k = w + 8q: input rows 2l, 2l + 1 at column k
+            const int k = w + 8 * q;
+            const float2 a = tile[2 * l][k ^ (l & 15)], c = tile[2 * l + 1][k ^ (l & 15)];
+            reinterpret_cast<float4*>(yb + (int64_t)(j0 + k) * n + i0)[l] = make_float4(a.x, a.y, c.x, c.y);
+        }
+        __syncthreads();
+    }
+    } else {
     __shared__ float2 tile[TT][TT + 1];
     const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4 threads
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -244,6 +282,7 @@ __global__ void __launch_bounds__(256) k_transpose_c64(const float2* __restrict_
         for (int k = ty; k < TT; k += 4) yb[(int64_t)(j0 + k) * n + i0 + tx] = tile[tx][k];
         __syncthreads();
     }
+    }
 }
 
 cudaError_t launch_transpose_c64(const void* x, void* y, int64_t batch, int n, cudaStream_t st,
@@ -255,8 +294,14 @@ cudaError_t launch_transpose_c64(const void* x, void* y, int64_t batch, int n, c
     const int tpd = n / TT;
     const int64_t ntiles = batch * (int64_t)tpd * tpd;
     const unsigned grid = (unsigned)(ntiles < 148 * 8 ? ntiles : 148 * 8);
-    k_transpose_c64<<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(x), reinterpret_cast<float2*>(y), n,
-                                          tpd, ntiles, ldx, bsx);
+    const bool v2 = MXFFT_TRANSPOSE_V2 && ((ldx | bsx) & 1) == 0 &&
+                    ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
+    if (v2)
+        k_transpose_c64<true><<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(x), reinterpret_cast<float2*>(y),
+                                                    n, tpd, ntiles, ldx, bsx);
+    else
+        k_transpose_c64<false><<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(x), reinterpret_cast<float2*>(y),
+                                                     n, tpd, ntiles, ldx, bsx);
     note_launch();
     return cudaGetLastError();
 }
