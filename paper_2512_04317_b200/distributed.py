@@ -166,6 +166,25 @@ def _bracket(keys_sorted: np.ndarray, q: float, widen: float):
     return lo, hi, top, n
 
 
+def _bracket_dev(keys_sorted, n: int, q: float, widen: float):
+    """_bracket on a sorted torch tensor (any device) whose first n entries are
+    finite: gathers only the three order statistics it needs."""
+    import torch
+
+    if n == 0:
+        return np.float32(0.0), np.float32(np.inf), np.float32(0.0), n
+    rs = (n - 1) * q
+    d = int((8 + 4.0 * math.sqrt(rs + 1.0)) * widen)
+    ilo, ihi = int(math.floor(rs)) - d, int(math.ceil(rs)) + 1 + d
+    idx = torch.tensor([max(ilo, 0), min(ihi, n - 1), n - 1], dtype=torch.int64, device=keys_sorted.device)
+    v = keys_sorted[idx].cpu().numpy().astype(np.float32)
+    f32 = np.float32
+    lo = f32(0.0) if ilo <= 0 else f32(v[0]) * f32(1 - 2.0**-20)
+    hi = f32(np.inf) if ihi >= n else f32(v[1]) * f32(1 + 2.0**-20)
+    top = f32(v[2]) * f32(1 - 2.0**-20)
+    return lo, hi, top, n
+
+
 def compute_prescale_global(x_local, cfg: PrescaleConfig, comm: Comm = None, ops=None,
                             nsamples: int = 1 << 18) -> PrescaleResult:
     """compute_prescale (prescale.py:61-73) over ONE segment whose points are
@@ -182,19 +201,24 @@ def compute_prescale_global(x_local, cfg: PrescaleConfig, comm: Comm = None, ops
     npts = x.numel()
     q = cfg.tau / 100.0
     s_local = min(max(4, (nsamples // comm.world) // 4 * 4), npts // 4 * 4)
-    keys = comm.all_gather_cat(ops.sample_keys(x, s_local))
-    keys = torch.sort(keys).values.cpu().numpy()
+    keys = torch.sort(comm.all_gather_cat(ops.sample_keys(x, s_local))).values
+    # the sorted sample stays where it is: only the few order statistics and
+    # bracket counts the host needs are read back (not the whole sample)
+    n_fin = int(torch.isfinite(keys).sum())
     dev = x.device
     for widen in (1.0, 4.0, 32.0, None):
         if widen is None:  # last resort: every nonzero point is a candidate
             lo, hi, top, nsamp = np.float32(0.0), np.float32(np.inf), np.float32(0.0), 0
         else:
-            lo, hi, top, nsamp = _bracket(keys, q, widen)
+            lo, hi, top, nsamp = _bracket_dev(keys, n_fin, q, widen)
         if nsamp == 0:
             cand_cap, top_cap = npts, npts
         else:
-            f = (min(nsamp, int(np.searchsorted(keys[:nsamp], hi, side="right")))
-                 - int(np.searchsorted(keys[:nsamp], lo, side="left"))) / nsamp
+            fin = keys[:nsamp]
+            edges = torch.tensor([float(hi), float(lo)], dtype=fin.dtype, device=fin.device)
+            above = int(torch.searchsorted(fin, edges[:1], right=True).item())
+            below_lo = int(torch.searchsorted(fin, edges[1:], right=False).item())
+            f = (min(nsamp, above) - below_lo) / nsamp
             cand_cap = min(npts, int(npts * f * 2) + 65536)
             top_cap = min(npts, int(4 * npts / nsamp) + 4096)
         (nnz, below, ncand, ntop, flags), cand, topb = ops.count_range(x, float(lo), float(hi), float(top),
