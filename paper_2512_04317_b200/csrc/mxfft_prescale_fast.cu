@@ -73,6 +73,9 @@ constexpr int64_t FUSED_MAX = int64_t(1) << 18;
 #ifndef MXFFT_PS_LEAN_SMALL_NT
 #define MXFFT_PS_LEAN_SMALL_NT 128  // lean statistics: threads per CTA for segments <= 2^15 points (128: C4 162.4 -> 158.9 us vs 256)
 #endif
+#ifndef MXFFT_CR_MINB
+#define MXFFT_CR_MINB 4  // count_range kernel: min CTAs per SM for the register budget (4: 63 registers, no spills)
+#endif
 #ifndef MXFFT_PS_PREFETCH
 #define MXFFT_PS_PREFETCH 4  // lean statistics: stream rounds prefetched into L2 ahead of the loads
 #endif
@@ -1623,7 +1626,9 @@ cudaError_t launch_prescale_sample_keys(const float2* x, int64_t npts, int64_t n
 // per-chunk kernel (k_ps_count) issues one same-address atomic per warp and
 // chunk, which serialises at ~2.6 ms for a 16384^2 image.
 constexpr int CR_BUF = 2048;  // candidates buffered per CTA
-__global__ void __launch_bounds__(CNT_THREADS) k_ps_count_range(const float2* __restrict__ x, int64_t npts,
+constexpr int CR_PER_THREAD = 8;  // complex values per thread per chunk (double-buffered)
+constexpr int CR_CHUNK = CNT_THREADS * CR_PER_THREAD;
+__global__ void __launch_bounds__(CNT_THREADS, MXFFT_CR_MINB) k_ps_count_range(const float2* __restrict__ x, int64_t npts,
                                                                SegState* st, float2* cand, int64_t cap,
                                                                float2* top, int64_t topcap) {
     __shared__ float2 buf[CR_BUF];
@@ -1643,19 +1648,26 @@ __global__ void __launch_bounds__(CNT_THREADS) k_ps_count_range(const float2* __
     unsigned below = 0;
     float ksum = 0.f;
     const float4* x4 = reinterpret_cast<const float4*>(x);
-    const int64_t npairs = npts / 2, nchunks = (npairs + CHUNK / 2 - 1) / (CHUNK / 2);
+    const int64_t npairs = npts / 2, nchunks = (npairs + CR_CHUNK / 2 - 1) / (CR_CHUNK / 2);
     const unsigned lane = threadIdx.x & 31;
-    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        const int64_t p0 = c * (CHUNK / 2);
-        float4 v[CNT_PER_THREAD / 2];
+    float4 vn[CR_PER_THREAD / 2];  // the next chunk's loads are in flight while this one is classified
+    auto load_chunk = [&](int64_t c) {
+        const int64_t p0 = c * (CR_CHUNK / 2);
 #pragma unroll
-        for (int it = 0; it < CNT_PER_THREAD / 2; ++it) {
+        for (int it = 0; it < CR_PER_THREAD / 2; ++it) {
             const int64_t pi = p0 + it * CNT_THREADS + threadIdx.x;
-            v[it] = pi < npairs ? __ldg(x4 + pi) : make_float4(0.f, 0.f, 0.f, 0.f);
+            vn[it] = (c < nchunks && pi < npairs) ? __ldg(x4 + pi) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
+    };
+    load_chunk(blockIdx.x);
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        float4 v[CR_PER_THREAD / 2];
+#pragma unroll
+        for (int it = 0; it < CR_PER_THREAD / 2; ++it) v[it] = vn[it];
+        load_chunk(c + gridDim.x);
         unsigned cbits = 0, tbits = 0;
 #pragma unroll
-        for (int it = 0; it < CNT_PER_THREAD / 2; ++it) {
+        for (int it = 0; it < CR_PER_THREAD / 2; ++it) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const float re = h ? v[it].z : v[it].x, im = h ? v[it].w : v[it].y;
@@ -1692,7 +1704,7 @@ __global__ void __launch_bounds__(CNT_THREADS) k_ps_count_range(const float2* __
             unsigned slot = (wbase & 0x7fffffffu) + incl - cnt;
             if (cbits) {
 #pragma unroll
-                for (int it = 0; it < CNT_PER_THREAD / 2; ++it)
+                for (int it = 0; it < CR_PER_THREAD / 2; ++it)
 #pragma unroll
                     for (int h = 0; h < 2; ++h)
                         if ((cbits >> (2 * it + h)) & 1) {
@@ -1707,7 +1719,7 @@ __global__ void __launch_bounds__(CNT_THREADS) k_ps_count_range(const float2* __
             unsigned slot = warp_reserve(__popc(tbits), &st->ntop);
             if (tbits) {
 #pragma unroll
-                for (int it = 0; it < CNT_PER_THREAD / 2; ++it)
+                for (int it = 0; it < CR_PER_THREAD / 2; ++it)
 #pragma unroll
                     for (int h = 0; h < 2; ++h)
                         if ((tbits >> (2 * it + h)) & 1) {
@@ -1765,12 +1777,17 @@ cudaError_t launch_prescale_count_range(const float2* x, int64_t npts, float lo,
     SegState* s = reinterpret_cast<SegState*>(state);
     k_ps_state_init<<<1, 1, 0, st>>>(s, lo, hi, top);
     note_launch();
-    const int64_t cps = (npts + CHUNK - 1) / CHUNK;
+    const int64_t cps = (npts + CR_CHUNK - 1) / CR_CHUNK;
     if (cps > 0) {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int64_t grid = cps < (int64_t)sms * 6 ? cps : (int64_t)sms * 6;
+        static int per_sm = 0, sms = 148;
+        if (!per_sm) {  // a resident (persistent) grid
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ps_count_range, CNT_THREADS, 0);
+            if (per_sm < 1) per_sm = 1;
+        }
+        const int64_t grid = cps < (int64_t)sms * per_sm ? cps : (int64_t)sms * per_sm;
         k_ps_count_range<<<(unsigned)grid, CNT_THREADS, 0, st>>>(x, npts, s, cand, cap, topb, topcap);
         note_launch();
     }
