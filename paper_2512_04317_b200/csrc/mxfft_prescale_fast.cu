@@ -83,7 +83,7 @@ constexpr int64_t FUSED_MAX = int64_t(1) << 18;
 #define MXFFT_PS_LEAN 1  // k_ps_lean for segments of 2^13 .. 2^17 points
 #endif
 #ifndef MXFFT_FUSED_MIN_SEG
-#define MXFFT_FUSED_MIN_SEG 32  // fewer segments: the grid-wide path
+#define MXFFT_FUSED_MIN_SEG 1  // fewer segments: the grid-wide path (1: per-segment kernels always; 256^2 x1 stats 34.6 -> 22.8 us)
 #endif
 // fused kernel: 256 threads for segments <= 2^15 points
 // (several CTAs per SM hide each other's select phase), else 512; 4096 candidates
