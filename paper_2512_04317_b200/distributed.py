@@ -150,25 +150,11 @@ class CudaOps:
         return out
 
 
-def _bracket(keys_sorted: np.ndarray, q: float, widen: float):
-    """Sample ranks around the tau-quantile -> FP32 key bracket [lo, hi] and the
-    peak threshold (the same rule as the fused kernel, k_ps_fused)."""
-    n = int(np.count_nonzero(np.isfinite(keys_sorted)))
-    if n == 0:
-        return np.float32(0.0), np.float32(np.inf), np.float32(0.0), n
-    rs = (n - 1) * q
-    d = int((8 + 4.0 * math.sqrt(rs + 1.0)) * widen)
-    ilo, ihi = int(math.floor(rs)) - d, int(math.ceil(rs)) + 1 + d
-    f32 = np.float32
-    lo = f32(0.0) if ilo <= 0 else f32(keys_sorted[ilo]) * f32(1 - 2.0**-20)
-    hi = f32(np.inf) if ihi >= n else f32(keys_sorted[ihi]) * f32(1 + 2.0**-20)
-    top = f32(keys_sorted[n - 1]) * f32(1 - 2.0**-20)
-    return lo, hi, top, n
-
-
 def _bracket_dev(keys_sorted, n: int, q: float, widen: float):
-    """_bracket on a sorted torch tensor (any device) whose first n entries are
-    finite: gathers only the three order statistics it needs."""
+    """Sample ranks around the tau-quantile -> FP32 key bracket [lo, hi] and the
+    peak threshold (the same rule as the fused kernel, k_ps_fused), from a
+    sorted torch tensor (any device) whose first n entries are finite; only the
+    three order statistics it needs are read back."""
     import torch
 
     if n == 0:
