@@ -213,6 +213,45 @@ int32_t mxfft_cabs(const void* x, int32_t is_c128, int64_t n, double* out, uintp
 int32_t mxfft_rss(const void* x, int32_t is_c128, int64_t groups, int32_t coils, int64_t npix,
                   double* out, uintptr_t stream);
 
+/* The fused small-image pipeline (BASELINE configs[3]): one n x n image per
+ * CTA, the whole per-image pipeline of forward_pipeline / roundtrip_pipeline
+ * (mri.py:84-107, one coil) in ONE kernel -- compute_prescale's statistics
+ * (prescale.py:61-73) on the image held in shared memory, x 2^k on load, the
+ * row and column passes of fft_2d (fftcore.py:344-353) [then the inverse
+ * fft_2d and x 1/n^2], x 2^-k on store.  x, y: complex64 (nimg, n, n), out of
+ * place; d_res: one mxfft_prescale_result per image (flags as
+ * mxfft_prescale_stats); d_k: optional per-image k.  Results are identical to
+ * mxfft_prescale_stats + mxfft_fft2.  Supported when
+ * mxfft_pipeline_fused_supported(plan) != 0 (n = 128, a hardware MX format,
+ * B in {16, 32, 64}). */
+int32_t mxfft_pipeline_fused_supported(mxfft_plan plan);
+int32_t mxfft_pipeline_fused(mxfft_plan plan, const void* x, void* y, int64_t nimg, int32_t roundtrip,
+                             const mxfft_prescale_cfg* cfg, mxfft_prescale_result* d_res, int32_t* d_k,
+                             uintptr_t stream);
+
+/* mxfft_rss with the pipelines' FP64 epilogue folded in: every coil value of
+ * group g is multiplied by 2^(k_sign * d_k[g] + exp_const) in FP64 (exact)
+ * before |.| -- the x 1/N^2 and undo_prescale of roundtrip_pipeline /
+ * forward_pipeline (mri.py:84-107, prescale.py:89-91) done in FP64 as the
+ * reference does.  d_k may be NULL (then only exp_const applies). */
+int32_t mxfft_rss_scaled(const void* x, int32_t is_c128, int64_t groups, int32_t coils, int64_t npix,
+                         const int32_t* d_k, int32_t k_sign, int32_t exp_const, double* out, uintptr_t stream);
+
+/* apply_prescale (prescale.py:76-86) on complex128 input followed by the
+ * transform's complex64 cast (fftcore.py:262): y (complex64) =
+ * x (complex128) * 2^d_k[seg], the product in FP64, rounded to FP32 once;
+ * nseg contiguous segments of seg_points values. */
+int32_t mxfft_prescale_apply_c128(const void* x, void* y, int64_t nseg, int64_t seg_points, const int32_t* d_k,
+                                  uintptr_t stream);
+
+/* data * math.ldexp(1.0, k) (apply_prescale / undo_prescale, prescale.py:76-91)
+ * on n elements of dtype 0 = float32, 1 = float64, 2 = complex64,
+ * 3 = complex128; `factor` is 2^k already rounded to the array's precision
+ * (numpy rounds the Python-float scalar the same way).  Complex elements are
+ * multiplied as numpy multiplies by the scalar cast to complex:
+ * (re f - im 0, re 0 + im f).  x may alias y. */
+int32_t mxfft_scale(const void* x, void* y, int64_t n, int32_t dtype, double factor, uintptr_t stream);
+
 /* Test instrumentation: run the 1-D row transform stage by stage through the
  * same device code as mxfft_fft_rows and record, per stage s (arrays laid out
  * [stage][batch][...]): v-block scale exponents v_exp (int32, n/2/cpb per row),

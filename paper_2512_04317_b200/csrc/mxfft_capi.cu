@@ -3,7 +3,10 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 
 #include "../../include/mxfft_b200.h"
 #include "mxfft_common.cuh"
@@ -12,6 +15,57 @@
 namespace mxfft {
 static std::atomic<long long> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+static std::mutex g_attr_mu;
+static std::map<std::tuple<const void*, int, int>, int> g_smem_attr;          // (k, dev, -) -> limit set
+static std::map<std::tuple<const void*, int, int, size_t>, int> g_occ;       // (k, dev, nt, smem) -> CTAs/SM
+static std::map<std::pair<int, int>, int> g_dev_attr;                        // (dev, attr) -> value
+
+cudaError_t ensure_smem_attr(const void* k, int smem_max) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(g_attr_mu);
+    auto key = std::make_tuple(k, dev, 0);
+    auto it = g_smem_attr.find(key);
+    if (it != g_smem_attr.end() && it->second >= smem_max) return cudaSuccess;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+    if (e == cudaSuccess) g_smem_attr[key] = smem_max;
+    return e;
+}
+
+cudaError_t cached_occupancy(const void* k, int nt, size_t smem, int* occ) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(g_attr_mu);
+    auto key = std::make_tuple(k, dev, nt, smem);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) {
+        *occ = it->second;
+        return cudaSuccess;
+    }
+    int o = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, nt, smem);
+    if (e != cudaSuccess) return e;
+    o = o < 1 ? 1 : o;
+    g_occ[key] = o;
+    *occ = o;
+    return cudaSuccess;
+}
+
+int device_attr(cudaDeviceAttr a) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(g_attr_mu);
+    auto key = std::make_pair(dev, (int)a);
+    auto it = g_dev_attr.find(key);
+    if (it != g_dev_attr.end()) return it->second;
+    int v = 0;
+    cudaDeviceGetAttribute(&v, a, dev);
+    g_dev_attr[key] = v;
+    return v;
+}
 cudaError_t plan_encode(Plan& p, const double* d_tw, cudaStream_t st);
 cudaError_t launch_prescale(const void* x, int is_c128, int64_t nseg, int64_t npts,
                             const mxfft_prescale_cfg& c, mxfft_prescale_result* out, int32_t* kvec,
@@ -70,6 +124,22 @@ static bool check_fmt(const mxfft_format* f, std::string& why) {
 static FmtDesc desc_of(const mxfft_format* f) {
     return make_fmt(f->exponent_bits, f->mantissa_bits, f->policy, f->bias);
 }
+
+// a plan's tables live on the device it was created on
+static int32_t check_plan(mxfft_plan plan) {
+    if (!plan) return fail(MXFFT_ERR_VALUE, "null plan");
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (dev != plan->p.device)
+        return fail(MXFFT_ERR_VALUE, "plan was created on device " + std::to_string(plan->p.device) +
+                                         ", current device is " + std::to_string(dev));
+    return MXFFT_OK;
+}
+#define CHECK_PLAN(plan)                            \
+    do {                                            \
+        const int32_t _c = check_plan(plan);        \
+        if (_c != MXFFT_OK) return _c;              \
+    } while (0)
 
 static int ilog2(int64_t n) {
     int s = 0;
@@ -141,6 +211,7 @@ int32_t mxfft_plan_create(mxfft_plan* plan, int32_t n, const mxfft_format* fmt,
     p.block_size = block_size;
     p.cpb = cpb;
     p.fmt = desc_of(fmt);
+    cudaGetDevice(&p.device);
     const int st = p.log2n;
     const int nb = m / cpb;
     cudaStream_t s = (cudaStream_t)stream;
@@ -180,7 +251,7 @@ int32_t mxfft_plan_destroy(mxfft_plan plan) {
 
 int32_t mxfft_plan_twiddles(mxfft_plan plan, double* h_codes_re, double* h_codes_im,
                             double* h_scales) {
-    if (!plan) return fail(MXFFT_ERR_VALUE, "null plan");
+    CHECK_PLAN(plan);
     const Plan& p = plan->p;
     const int m = p.n / 2, nb = m / p.cpb, st = p.log2n;
     CK(cudaMemcpy(h_codes_re, p.d_wcr, sizeof(double) * st * m, cudaMemcpyDeviceToHost), "plan_twiddles");
@@ -196,7 +267,7 @@ int32_t mxfft_plan_twiddles(mxfft_plan plan, double* h_codes_re, double* h_codes
 
 int32_t mxfft_fft_rows(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t inverse,
                        uintptr_t stream) {
-    if (!plan) return fail(MXFFT_ERR_VALUE, "null plan");
+    CHECK_PLAN(plan);
     if (batch < 0) return fail(MXFFT_ERR_SHAPE, "negative batch");
     if (batch == 0) return MXFFT_OK;
     LinePass lp;
@@ -213,7 +284,7 @@ int32_t mxfft_fft_rows(mxfft_plan plan, const void* x, void* y, int64_t batch, i
 
 int32_t mxfft_fft_rows_scaled(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t inverse,
                               int32_t exp_in, int32_t exp_out, uintptr_t stream) {
-    if (!plan) return fail(MXFFT_ERR_VALUE, "null plan");
+    CHECK_PLAN(plan);
     if (batch < 0) return fail(MXFFT_ERR_SHAPE, "negative batch");
     if (batch == 0) return MXFFT_OK;
     LinePass lp;
@@ -231,7 +302,7 @@ int32_t mxfft_fft_rows_scaled(mxfft_plan plan, const void* x, void* y, int64_t b
 
 int32_t mxfft_fft_cols(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t inverse,
                        uintptr_t stream) {
-    if (!plan) return fail(MXFFT_ERR_VALUE, "null plan");
+    CHECK_PLAN(plan);
     if (batch < 0) return fail(MXFFT_ERR_SHAPE, "negative batch");
     if (batch == 0) return MXFFT_OK;
     LinePass lp;
@@ -255,7 +326,7 @@ int64_t mxfft_fft2_workspace_bytes(mxfft_plan plan, int64_t batch) {
 int32_t mxfft_fft2(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t mode,
                    const int32_t* d_k, int32_t k_group, void* workspace, int64_t workspace_bytes,
                    uintptr_t stream) {
-    if (!plan) return fail(MXFFT_ERR_VALUE, "null plan");
+    CHECK_PLAN(plan);
     if (mode < 0 || mode > 2) return fail(MXFFT_ERR_VALUE, "mode must be 0 (forward), 1 (inverse) or 2 (round trip)");
     if (batch < 0) return fail(MXFFT_ERR_SHAPE, "negative batch");
     if (batch == 0) return MXFFT_OK;
@@ -405,10 +476,49 @@ int32_t mxfft_rss(const void* x, int32_t is_c128, int64_t groups, int32_t coils,
     return MXFFT_OK;
 }
 
+int32_t mxfft_pipeline_fused_supported(mxfft_plan plan) { return plan && mx_image_ok(plan->p) ? 1 : 0; }
+
+int32_t mxfft_pipeline_fused(mxfft_plan plan, const void* x, void* y, int64_t nimg, int32_t roundtrip,
+                             const mxfft_prescale_cfg* cfg, mxfft_prescale_result* d_res, int32_t* d_k,
+                             uintptr_t stream) {
+    CHECK_PLAN(plan);
+    if (!cfg) return fail(MXFFT_ERR_VALUE, "null config");
+    if (nimg < 0) return fail(MXFFT_ERR_SHAPE, "negative batch");
+    if (!mx_image_ok(plan->p))
+        return fail(MXFFT_ERR_UNSUPPORTED_SIZE, "the fused pipeline needs n = 128, a hardware MX format and B in {16, 32, 64}");
+    if (!d_res) return fail(MXFFT_ERR_VALUE, "null result rows");
+    if (x == y) return fail(MXFFT_ERR_VALUE, "the fused pipeline is out of place (exact replays re-read the input)");
+    CK(run_mx_image(plan->p, x, y, nimg, roundtrip ? 1 : 0, *cfg, d_res, d_k, (cudaStream_t)stream), "pipeline_fused");
+    return MXFFT_OK;
+}
+
+int32_t mxfft_rss_scaled(const void* x, int32_t is_c128, int64_t groups, int32_t coils, int64_t npix,
+                         const int32_t* d_k, int32_t k_sign, int32_t exp_const, double* out, uintptr_t stream) {
+    if (coils < 1) return fail(MXFFT_ERR_SHAPE, "need at least one coil");
+    if (groups < 0 || npix < 0) return fail(MXFFT_ERR_SHAPE, "negative size");
+    CK(launch_rss(x, is_c128, groups, coils, npix, out, (cudaStream_t)stream, d_k, k_sign, exp_const), "rss_scaled");
+    return MXFFT_OK;
+}
+
+int32_t mxfft_prescale_apply_c128(const void* x, void* y, int64_t nseg, int64_t seg_points, const int32_t* d_k,
+                                  uintptr_t stream) {
+    if (nseg < 0 || seg_points < 0) return fail(MXFFT_ERR_SHAPE, "negative size");
+    if (!d_k) return fail(MXFFT_ERR_VALUE, "null k vector");
+    CK(launch_prescale_apply_c128(x, y, seg_points, nseg, d_k, (cudaStream_t)stream), "prescale_apply_c128");
+    return MXFFT_OK;
+}
+
+int32_t mxfft_scale(const void* x, void* y, int64_t n, int32_t dtype, double factor, uintptr_t stream) {
+    if (n < 0) return fail(MXFFT_ERR_SHAPE, "negative size");
+    if (dtype < 0 || dtype > 3) return fail(MXFFT_ERR_VALUE, "dtype must be 0 (f32), 1 (f64), 2 (c64) or 3 (c128)");
+    CK(launch_scale(x, y, n, dtype, factor, (cudaStream_t)stream), "scale");
+    return MXFFT_OK;
+}
+
 int32_t mxfft_fft_rows_debug(mxfft_plan plan, const void* x, void* y, int64_t batch,
                              int32_t inverse, int32_t* v_exp, float* v_codes, int32_t* p_exp,
                              int32_t* p_shift, float* p_codes, void* stage_out, uintptr_t stream) {
-    if (!plan) return fail(MXFFT_ERR_VALUE, "null plan");
+    CHECK_PLAN(plan);
     const Plan& p = plan->p;
     if (!mx_lines_ok(p)) return fail(MXFFT_ERR_VALUE, "debug capture needs a line-kernel plan");
     if (p.n > 4096) return fail(MXFFT_ERR_UNSUPPORTED_SIZE, "debug capture supports n <= 4096");

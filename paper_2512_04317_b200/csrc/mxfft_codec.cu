@@ -203,21 +203,61 @@ __device__ __forceinline__ double np_cabs(double re, double im) {
 }
 
 // rss (mri.py:70-81): sqrt(sum_c |T_c|^2), coils accumulated in order.
+// With kvec / econst, every coil value of group g is first multiplied by
+// 2^(ksign * kvec[g] + econst) in FP64 (exact): the pipelines' x 1/N^2 and
+// undo_prescale (mri.py:101-107, prescale.py:89-91) applied in FP64, as the
+// reference does, before |.|.
 template <typename T>
 __global__ void k_rss(const T* __restrict__ x, int64_t groups, int coils, int64_t npix,
-                      double* __restrict__ out) {
+                      const int32_t* __restrict__ kvec, int ksign, int econst, double* __restrict__ out) {
     const int64_t total = groups * npix;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t g = i / npix, p = i - g * npix;
+        const int e = (kvec ? ksign * kvec[g] : 0) + econst;
+        const double f = ldexp(1.0, e);
         double acc = 0.0;
         for (int c = 0; c < coils; ++c) {
             const T v = x[(g * coils + c) * npix + p];
-            const double m = np_cabs((double)v.x, (double)v.y);
+            const double m = e ? np_cabs(__dmul_rn((double)v.x, f), __dmul_rn((double)v.y, f))
+                               : np_cabs((double)v.x, (double)v.y);
             const double sq = __dmul_rn(m, m);
             acc = c == 0 ? sq : __dadd_rn(acc, sq);
         }
         out[i] = __dsqrt_rn(acc);
+    }
+}
+
+// apply_prescale (prescale.py:76-86) followed by the complex64 cast of the
+// transform's first gather (fftcore.py:262): y = complex64(x * 2^k[seg]),
+// the product taken in FP64 (exact) and rounded to FP32 once.
+__global__ void k_prescale_apply_c128(const double2* __restrict__ x, float2* __restrict__ y, int64_t seg_points,
+                                      int64_t total, const int32_t* __restrict__ kvec) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double f = ldexp(1.0, kvec[i / seg_points]);
+        const double2 v = x[i];
+        y[i] = make_float2(__double2float_rn(__dmul_rn(v.x, f)), __double2float_rn(__dmul_rn(v.y, f)));
+    }
+}
+
+// data * math.ldexp(1.0, k) of apply_prescale for float32 / float64 arrays
+// (flat real scalars; complex arrays as interleaved pairs): the factor comes
+// in already rounded to the array's precision, as numpy rounds the weak
+// Python-float scalar, and each product is rounded once.
+// Complex arrays are multiplied as numpy multiplies complex by the scalar
+// cast to complex, (re f - im 0, re 0 + im f): identical to (re f, im f)
+// except for infinities and NaNs (inf * 0 = NaN), which it reproduces.
+template <typename T, bool CPLX>
+__global__ void k_scale(const T* __restrict__ x, T* __restrict__ y, int64_t n, T f) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (CPLX) {
+            const T re = x[2 * i], im = x[2 * i + 1];
+            y[2 * i] = re * f - im * T(0);
+            y[2 * i + 1] = re * T(0) + im * f;
+        } else {
+            y[i] = x[i] * f;
+        }
     }
 }
 
@@ -327,14 +367,39 @@ cudaError_t launch_cabs(const void* x, int is_c128, int64_t n, double* out, cuda
 }
 
 cudaError_t launch_rss(const void* x, int is_c128, int64_t groups, int coils, int64_t npix,
-                       double* out, cudaStream_t st) {
+                       double* out, cudaStream_t st, const int32_t* kvec, int ksign, int econst) {
     if (groups * npix <= 0) return cudaSuccess;
     if (is_c128)
         k_rss<double2><<<grid_for(groups * npix, 256), 256, 0, st>>>(
-            reinterpret_cast<const double2*>(x), groups, coils, npix, out);
+            reinterpret_cast<const double2*>(x), groups, coils, npix, kvec, ksign, econst, out);
     else
         k_rss<float2><<<grid_for(groups * npix, 256), 256, 0, st>>>(
-            reinterpret_cast<const float2*>(x), groups, coils, npix, out);
+            reinterpret_cast<const float2*>(x), groups, coils, npix, kvec, ksign, econst, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prescale_apply_c128(const void* x, void* y, int64_t seg_points, int64_t nseg,
+                                       const int32_t* kvec, cudaStream_t st) {
+    const int64_t total = seg_points * nseg;
+    if (total <= 0) return cudaSuccess;
+    k_prescale_apply_c128<<<grid_for(total, 256), 256, 0, st>>>(reinterpret_cast<const double2*>(x),
+                                                               reinterpret_cast<float2*>(y), seg_points, total,
+                                                               kvec);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scale(const void* x, void* y, int64_t n, int dtype, double f, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    const int g = grid_for(n, 256);
+    switch (dtype) {
+        case 0: k_scale<float, false><<<g, 256, 0, st>>>((const float*)x, (float*)y, n, (float)f); break;
+        case 1: k_scale<double, false><<<g, 256, 0, st>>>((const double*)x, (double*)y, n, f); break;
+        case 2: k_scale<float, true><<<g, 256, 0, st>>>((const float*)x, (float*)y, n, (float)f); break;
+        case 3: k_scale<double, true><<<g, 256, 0, st>>>((const double*)x, (double*)y, n, f); break;
+        default: return cudaErrorInvalidValue;
+    }
     note_launch();
     return cudaGetLastError();
 }

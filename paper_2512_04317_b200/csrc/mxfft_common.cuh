@@ -209,4 +209,16 @@ struct TwEntry {
 // launch bookkeeping (gpu_launches)
 void note_launch(int n = 1);
 
+// Per-device launch setup (mxfft_capi.cu), thread-safe and keyed by the
+// current device, so a second GPU in the same process gets its own attributes
+// and grid sizes:
+//  - ensure_smem_attr: raise kernel k's dynamic shared memory limit to
+//    smem_max bytes (once per (k, device));
+//  - cached_occupancy: CTAs per SM of k at (nt threads, smem bytes), cached per
+//    (k, device, nt, smem);
+//  - device_attr: an attribute of the current device, cached.
+cudaError_t ensure_smem_attr(const void* k, int smem_max);
+cudaError_t cached_occupancy(const void* k, int nt, size_t smem, int* occ);
+int device_attr(cudaDeviceAttr a);
+
 }  // namespace mxfft

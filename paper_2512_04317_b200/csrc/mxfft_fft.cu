@@ -74,12 +74,9 @@ cudaError_t run_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
     g.kin_const = lp.kin_const;
     const size_t smem = (size_t)p.n * sizeof(float2);
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(k_lines_generic, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             227 * 1024);
+    {
+        cudaError_t e = ensure_smem_attr((const void*)k_lines_generic, 227 * 1024);
         if (e != cudaSuccess) return e;
-        attr_done = true;
     }
     const int64_t lines = lp.col_mode ? lp.batch * p.n : lp.total_lines;
     k_lines_generic<<<(unsigned)lines, 256, smem, st>>>(g);

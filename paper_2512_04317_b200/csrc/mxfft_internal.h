@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/mxfft_b200.h"
 #include "mxfft_common.cuh"
 
 namespace mxfft {
@@ -21,6 +22,7 @@ struct Plan {
     unsigned* d_tw16_inv = nullptr;  // conjugated twiddles (fftcore.py:267-268)
     signed char* d_twe8 = nullptr;   // log2 scale of the block holding butterfly j
     int trivial01 = 0;  // stage 0/1 twiddles are exactly 1 and -i at scale 2^-emax
+    int device = 0;     // the tables live on this device; transforms must run there
 };
 
 // One pass of 1-D transforms over a set of lines.
@@ -95,6 +97,11 @@ extern int g_profile_stage_limit;
 extern int g_lines_ctas_per_sm;
 extern int g_profile_flags;  // < 0: off (see mxfft_profile_stage_limit)
 bool mx_lines_ok(const Plan& p);
+// fused small-image pipeline (mxfft_image.cu)
+bool mx_image_ok(const Plan& p);
+cudaError_t run_mx_image(const Plan& p, const void* x, void* y, int64_t nimg, int roundtrip,
+                         const mxfft_prescale_cfg& cfg, mxfft_prescale_result* res, int32_t* kvec,
+                         cudaStream_t st);
 cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st);
 cudaError_t run_lines(const Plan& p, const LinePass& lp, cudaStream_t st);
 
@@ -122,7 +129,11 @@ cudaError_t launch_prescale_count_range(const float2* x, int64_t npts, float lo,
                                         void* state, float2* cand, int64_t cap, float2* topb,
                                         int64_t topcap, cudaStream_t st);
 cudaError_t launch_rss(const void* x, int is_c128, int64_t groups, int coils, int64_t npix,
-                       double* out, cudaStream_t st);
+                       double* out, cudaStream_t st, const int32_t* kvec = nullptr, int ksign = 0,
+                       int econst = 0);
+cudaError_t launch_prescale_apply_c128(const void* x, void* y, int64_t seg_points, int64_t nseg,
+                                       const int32_t* kvec, cudaStream_t st);
+cudaError_t launch_scale(const void* x, void* y, int64_t n, int dtype, double f, cudaStream_t st);
 cudaError_t launch_selftest_hwq(const FmtDesc& f, unsigned long long* mism, unsigned* first_bad,
                                 cudaStream_t st);
 

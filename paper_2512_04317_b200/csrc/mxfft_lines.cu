@@ -101,13 +101,7 @@ cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
         // n = 64 .. 512: pad the twiddle prefix so that the tile buffers start on a
         // 4 KB boundary of the shared window (dynamic shared memory begins after
         // the per-block reserved area); the kernels rely on it (see AX)
-        static int reserved = -1;
-        if (reserved < 0) {
-            int dev = 0, r = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&r, cudaDevAttrReservedSharedMemoryPerBlock, dev);
-            reserved = r;
-        }
+        const int reserved = device_attr(cudaDevAttrReservedSharedMemoryPerBlock);
         while ((reserved + a.tw_chunks * 16) % 4096) a.tw_chunks += 64;
     }
     // 128-thread kernels double-buffer their group tile (cp.async pipeline)

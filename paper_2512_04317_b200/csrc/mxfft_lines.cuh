@@ -1400,23 +1400,18 @@ __global__ void __launch_bounds__(512, 1) k_mx_lines_big(MxLinesArgs a) {
 // ---------------------------------------------------------------------------
 template <int ID, int CPB, bool DBG, int LT, bool BIGK>
 static cudaError_t launch_t(const MxLinesArgs& a, size_t smem, cudaStream_t st) {
-    static int occ = 0;
-    static int sms = 0;
     const int nt = BIGK ? (1 << a.log2T) : 128;
     void (*k)(MxLinesArgs);
     if constexpr (BIGK) k = k_mx_lines_big<ID, CPB, DBG, LT>;
     else k = k_mx_lines<ID, CPB, DBG, LT>;
-    if (!occ) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        int dev;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        int o = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, BIGK ? 512 : 128, smem);
-        if (e != cudaSuccess) return e;
-        occ = o < 1 ? 1 : o;
-    }
+    // per (device, kernel, threads, shared memory): the run-time-n variants
+    // (LT = -1) serve several n with different tiles
+    cudaError_t e = ensure_smem_attr((const void*)k, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    const int sms = device_attr(cudaDevAttrMultiProcessorCount);
+    int occ = 1;
+    e = cached_occupancy((const void*)k, nt, smem, &occ);
+    if (e != cudaSuccess) return e;
     const int lines_per_cta = nt >> a.log2T;
     const int64_t groups = (a.total_lines + lines_per_cta - 1) / lines_per_cta;
     const int per_sm = g_lines_ctas_per_sm > 0 && g_lines_ctas_per_sm < occ ? g_lines_ctas_per_sm : occ;
@@ -1429,20 +1424,16 @@ static cudaError_t launch_t(const MxLinesArgs& a, size_t smem, cudaStream_t st) 
 
 template <int ID, int CPB, int LT>
 static cudaError_t launch_cl2(const MxLinesArgs& a0, cudaStream_t st) {
-    static bool attr = false;
     MxLinesArgs a = a0;
     constexpr int NH = 32 << LT;
     a.tw_chunks = ((NH * 5 + 1023) / 1024) * 64;
     const size_t smem = (size_t)a.tw_chunks * 16 + (size_t)NH * 8 + 128;
     auto k = k_mx_lines_cl2<ID, CPB, LT>;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        cudaError_t e = ensure_smem_attr((const void*)k, (int)smem);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = device_attr(cudaDevAttrMultiProcessorCount);
     const int64_t nclusters = a.total_lines < sms ? a.total_lines : sms;  // two CTAs per SM
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(2 * nclusters));

@@ -109,15 +109,10 @@ cudaError_t launch_fp16_rows(const void* x, int x_is_c128, void* y, int64_t batc
     int log2n = 0;
     while ((1 << log2n) < n) ++log2n;
     const size_t smem = (size_t)n * sizeof(float2);
-    static bool attr[2] = {false, false};
-    if (!attr[x_is_c128]) {
-        cudaError_t e = x_is_c128
-                            ? cudaFuncSetAttribute(k_fp16_lines<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   227 * 1024)
-                            : cudaFuncSetAttribute(k_fp16_lines<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   227 * 1024);
+    {
+        cudaError_t e = x_is_c128 ? ensure_smem_attr((const void*)k_fp16_lines<double2>, 227 * 1024)
+                                  : ensure_smem_attr((const void*)k_fp16_lines<float2>, 227 * 1024);
         if (e != cudaSuccess) return e;
-        attr[x_is_c128] = true;
     }
     const FmtDesc f16 = make_fmt(5, 10, POL_IEEE, 15);
     const int nt = n / 2 < 512 ? (n / 2 < 32 ? 32 : n / 2) : 512;

@@ -378,20 +378,19 @@ cudaError_t launch_prescale(const void* x, int is_c128, int64_t nseg, int64_t np
     cfg.k_min = c.k_min;
     cfg.k_max = c.k_max;
     const size_t smem = sizeof(PsShared);
-    static bool done[2] = {false, false};
     if (is_c128) {
-        if (!done[1]) {
-            cudaFuncSetAttribute(k_prescale<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            done[1] = true;
+        {
+            cudaError_t e = ensure_smem_attr((const void*)k_prescale<double2>, (int)smem);
+            if (e != cudaSuccess) return e;
         }
         k_prescale<double2><<<(unsigned)nseg, PS_THREADS, smem, st>>>(
             reinterpret_cast<const double2*>(x), npts, cfg, out, kvec, nullptr, nullptr);
         note_launch();
         return cudaGetLastError();
     }
-    if (!done[0]) {
-        cudaFuncSetAttribute(k_prescale<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        done[0] = true;
+    {
+        cudaError_t e = ensure_smem_attr((const void*)k_prescale<float2>, (int)smem);
+        if (e != cudaSuccess) return e;
     }
     if (ws && prescale_fast_ok(npts) && ws_bytes >= prescale_fast_ws_bytes(nseg, npts)) {
         // sampled fast path; segments it cannot settle are listed for the exact kernel

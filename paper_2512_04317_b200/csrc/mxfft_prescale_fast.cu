@@ -29,13 +29,13 @@
 #include "../../include/mxfft_b200.h"
 #include "mxfft_common.cuh"
 #include "mxfft_internal.h"
+#include "mxfft_stats.cuh"
 
 namespace mxfft {
 
 constexpr int SAMPLE_MAX = 4096;
 constexpr int SEL_THREADS = 256;
 constexpr int TOPCAP = 2048;
-constexpr int NBIN = 512;
 constexpr int WCAP = 2048;  // exact-sort window capacity
 constexpr int CNT_THREADS = 256;
 constexpr int CNT_PER_THREAD = 16;  // complex values per thread per chunk
@@ -107,154 +107,7 @@ int64_t prescale_fast_ws_bytes(int64_t nseg, int64_t npts) {
     return st + fb + nseg * (cand_cap(npts) + TOPCAP) * (int64_t)sizeof(float2);
 }
 
-__device__ __forceinline__ double np_cabs_f(double re, double im) {
-    const double a = fabs(re), b = fabs(im);
-    const double larger = fmax(a, b), smaller = fmin(a, b);
-    if (larger == 0.0) return 0.0;
-    const double r = __ddiv_rn(smaller, larger);
-    return __dmul_rn(__dsqrt_rn(__fma_rn(r, r, 1.0)), larger);
-}
 
-// squared-magnitude key (FP32); points with |re|,|im| outside [2^-60, 2^60]
-// are flagged and the segment goes to the exact kernel
-__device__ __forceinline__ float skey(float re, float im) { return __fmaf_rn(re, re, __fmul_rn(im, im)); }
-
-template <typename T>
-struct Limits;
-template <>
-struct Limits<unsigned> {
-    static __device__ __forceinline__ unsigned max() { return 0xffffffffu; }
-    static __device__ __forceinline__ unsigned shfl_xor(unsigned v, int j) { return __shfl_xor_sync(0xffffffffu, v, j); }
-};
-template <>
-struct Limits<double> {
-    static __device__ __forceinline__ double max() { return DBL_MAX; }
-    static __device__ __forceinline__ double shfl_xor(double v, int j) { return __shfl_xor_sync(0xffffffffu, v, j); }
-};
-
-// Block-wide ascending bitonic sort of a[0..P) (P <= NT * SLOTS) with the
-// elements in registers: element i = tid + NT * s lives in slot s of thread
-// tid (pads past P sort last).  Compare-exchange distance j < 32: warp shuffle;
-// j >= NT: between two slots of the same thread; otherwise through shared
-// memory.  SLOTS is exact (sort_block picks it), so no slot is predicated off.
-template <typename T, int NT, int SLOTS>
-__device__ void reg_bitonic_sort(T* a, int P) {
-    constexpr int PE = NT * SLOTS;
-    const int tid = threadIdx.x;
-    T r[SLOTS];
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-        const int i = tid + NT * s;
-        r[s] = i < P ? a[i] : Limits<T>::max();
-    }
-#pragma unroll 1
-    for (int k = 2; k <= PE; k <<= 1) {
-#pragma unroll 1
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j >= NT) {
-#pragma unroll
-                for (int jb = 1; jb < SLOTS; jb <<= 1) {  // compile-time slot pairs
-                    if (jb != j / NT) continue;
-#pragma unroll
-                    for (int s = 0; s < SLOTS; ++s) {
-                        const int sp = s ^ jb;
-                        if (sp > s) {
-                            const bool asc = ((tid + NT * s) & k) == 0;
-                            const T x = r[s], y = r[sp];
-                            if ((x > y) == asc) {
-                                r[s] = y;
-                                r[sp] = x;
-                            }
-                        }
-                    }
-                }
-            } else if (j >= 32) {
-                __syncthreads();
-#pragma unroll
-                for (int s = 0; s < SLOTS; ++s) a[tid + NT * s] = r[s];
-                __syncthreads();
-#pragma unroll
-                for (int s = 0; s < SLOTS; ++s) {
-                    const int i = tid + NT * s, l = i ^ j;
-                    const T y = a[l];
-                    const bool asc = (i & k) == 0, low = i < l;
-                    // the lower index keeps the min when ascending
-                    r[s] = (low == asc) ? (y < r[s] ? y : r[s]) : (y > r[s] ? y : r[s]);
-                }
-            } else {
-#pragma unroll
-                for (int s = 0; s < SLOTS; ++s) {
-                    const int i = tid + NT * s;
-                    const T y = Limits<T>::shfl_xor(r[s], j);
-                    const bool asc = (i & k) == 0, low = (i & j) == 0;
-                    r[s] = (low == asc) ? (y < r[s] ? y : r[s]) : (y > r[s] ? y : r[s]);
-                }
-            }
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s)
-        if (tid + NT * s < P) a[tid + NT * s] = r[s];
-    __syncthreads();
-}
-
-// Order statistics without sorting: the elements of rank r0, r1, r2 of
-// a[0..P) (ascending; ties broken by index, so ranks are a permutation) go to
-// out[0..2] (a rank < 0 is skipped).  Each element's rank is counted against
-// broadcast shared-memory reads -- no barriers between phases.
-template <typename T, int NT>
-__device__ void rank_select(const T* a, int P, int r0, int r1, int r2, T* out) {
-    for (int i = threadIdx.x; i < P; i += NT) {
-        const T v = a[i];
-        int r = 0;
-        int j = 0;
-        for (; j + 4 <= P; j += 4) {
-            const T u0 = a[j], u1 = a[j + 1], u2 = a[j + 2], u3 = a[j + 3];
-            r += (u0 < v) | ((u0 == v) & (j < i));
-            r += (u1 < v) | ((u1 == v) & (j + 1 < i));
-            r += (u2 < v) | ((u2 == v) & (j + 2 < i));
-            r += (u3 < v) | ((u3 == v) & (j + 3 < i));
-        }
-        for (; j < P; ++j) {
-            const T u = a[j];
-            r += (u < v) | ((u == v) & (j < i));
-        }
-        if (r == r0) out[0] = v;
-        if (r == r1) out[1] = v;
-        if (r == r2) out[2] = v;
-    }
-    __syncthreads();
-}
-
-template <typename T, int NT, int MAXS>
-__device__ void sort_block(T* a, int P);
-
-// The elements of rank r0 and r1 of a[0..P) -> out[0], out[1]: counted ranks
-// for small P (P^2 / NT compares, no barriers), a register sort beyond.
-template <typename T, int NT, int MAXS>
-__device__ void pick_two(T* a, int P, int r0, int r1, T* out) {
-    if (P <= 2 * NT) {
-        rank_select<T, NT>(a, P, r0, r1, -1, out);
-        return;
-    }
-    sort_block<T, NT, MAXS>(a, P);
-    if (threadIdx.x == 0) {
-        out[0] = a[r0];
-        out[1] = a[r1];
-    }
-    __syncthreads();
-}
-
-// sort a[0..P), P <= NT * MAXS, with the smallest power-of-two slot count
-template <typename T, int NT, int MAXS>
-__device__ void sort_block(T* a, int P) {
-    if (P <= NT || MAXS == 1) return reg_bitonic_sort<T, NT, 1>(a, P);
-    if (P <= 2 * NT || MAXS == 2) return reg_bitonic_sort<T, NT, (MAXS < 2 ? MAXS : 2)>(a, P);
-    if (P <= 4 * NT || MAXS == 4) return reg_bitonic_sort<T, NT, (MAXS < 4 ? MAXS : 4)>(a, P);
-    if (P <= 8 * NT || MAXS == 8) return reg_bitonic_sort<T, NT, (MAXS < 8 ? MAXS : 8)>(a, P);
-    return reg_bitonic_sort<T, NT, MAXS>(a, P);
-}
 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(SEL_THREADS) k_ps_sample(const float2* __restrict__ xall, int64_t npts,
@@ -403,9 +256,6 @@ __global__ void __launch_bounds__(CNT_THREADS, 4) k_ps_count(const float2* __res
 }
 
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int round_half_away_d(double v) {
-    return v >= 0 ? (int)floor(__dadd_rn(v, 0.5)) : (int)ceil(__dsub_rn(v, 0.5));
-}
 
 struct SelShared {
     unsigned hist[NBIN];
@@ -418,21 +268,8 @@ struct SelShared {
     unsigned woff, wend;
 };
 
-// bin of a key bit pattern inside [klo, khi] (monotone non-decreasing in k)
-__device__ __forceinline__ int kbin(unsigned k, unsigned klo, float inv) {
-    k = k < klo ? klo : k;
-    const int b = (int)((float)(k - klo) * inv);
-    return b >= NBIN ? NBIN - 1 : b;
-}
-// (approximately) the smallest key bit pattern of bin b; only used by the
-// rounding guard, which has a 2^-18 relative margin
-__device__ __forceinline__ unsigned bin_lo(int b, unsigned klo, float inv) {
-    return klo + (unsigned)ceilf((float)b / inv);
-}
 
 __device__ __forceinline__ void fail_seg(int* list, int* list_n, int seg) { list[atomicAdd(list_n, 1)] = seg; }
-__device__ void finish_result(const mxfft_prescale_cfg& c, double a_max, double p_tau, unsigned long long nnz,
-                              mxfft_prescale_result* out, int32_t* kvec, int seg);
 
 __global__ void __launch_bounds__(SEL_THREADS) k_ps_select(SegState* st, int* list, int* list_n, const float2* cand,
                                                            int64_t cap, const float2* top, double q,
@@ -548,33 +385,6 @@ __global__ void __launch_bounds__(SEL_THREADS) k_ps_select(SegState* st, int* li
     if (tid == 0) finish_result(c, a_max, p_tau, nnz, out, kvec, seg);
 }
 
-// k (prescale.py:61-73) from a_max / p_tau; flags bit 1 marks a log2 within a
-// few ulps of a rounding boundary (the host re-checks it)
-__device__ void finish_result(const mxfft_prescale_cfg& c, double a_max, double p_tau, unsigned long long nnz,
-                              mxfft_prescale_result* out, int32_t* kvec, int seg) {
-    const double EPS = 1e-30;
-    const double r1 = __ddiv_rn(c.target, a_max > EPS ? a_max : EPS);
-    const double r2 = __ddiv_rn(c.tau_min, p_tau > EPS ? p_tau : EPS);
-    const double L1 = log2(r1), L2 = log2(r2);
-    const int k1 = round_half_away_d(L1);
-    const int k2 = (int)ceil(L2);
-    int k = max(k1, k2);
-    k = min(max(k, c.k_min), c.k_max);
-    const double d1 = fabs(fabs(L1 - trunc(L1)) - 0.5);
-    const double d2 = fabs(L2 - rint(L2));
-    const bool pow2 = (__double_as_longlong(r2) & 0xFFFFFFFFFFFFFll) == 0;
-    const int amb = (d1 < 1e-12 * fmax(1.0, fabs(L1)) || (d2 < 1e-12 * fmax(1.0, fabs(L2)) && !pow2)) ? 2 : 0;
-    mxfft_prescale_result r;
-    r.a_max = a_max;
-    r.p_tau = p_tau;
-    r.k1 = k1;
-    r.k2 = k2;
-    r.k = k;
-    r.flags = amb;
-    r.nnz = (int64_t)nnz;
-    out[seg] = r;
-    if (kvec) kvec[seg] = k;
-}
 
 // ---------------------------------------------------------------------------
 // fused sample -> count -> select, one CTA per segment (segments <= 2^18 points)
@@ -1040,31 +850,6 @@ struct LeanShared {
     unsigned woff, wend;
 };
 
-// block-wide sum of three counters (all threads get the totals)
-template <int NT>
-__device__ __forceinline__ void block_sum3(unsigned& a, unsigned& b, unsigned& c, unsigned* wa, unsigned* wb,
-                                           unsigned* wc) {
-    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-    for (int o = 16; o; o >>= 1) {
-        a += __shfl_xor_sync(0xffffffffu, a, o);
-        b += __shfl_xor_sync(0xffffffffu, b, o);
-        c += __shfl_xor_sync(0xffffffffu, c, o);
-    }
-    __syncthreads();
-    if (lane == 0) {
-        wa[wp] = a;
-        wb[wp] = b;
-        wc[wp] = c;
-    }
-    __syncthreads();
-    a = b = c = 0;
-#pragma unroll
-    for (int i = 0; i < NT / 32; ++i) {
-        a += wa[i];
-        b += wb[i];
-        c += wc[i];
-    }
-}
 
 template <int NT, int K, int WC, int OV>
 __global__ void __launch_bounds__(NT, 1024 / NT)
@@ -1471,47 +1256,34 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
     // the fused kernel streams a segment with ONE CTA: with few segments the
     // grid-wide path (sample / multi-CTA count / select) fills the GPU better
     if (npts <= FUSED_MAX && nseg >= MXFFT_FUSED_MIN_SEG) {
-        static bool attr = false;
-        if (!attr) {
-            cudaError_t e = cudaFuncSetAttribute(k_ps_fused<256, 4096, 1, 256, 1024, 1024>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)sizeof(FusedShared<256, 4096, 256, 1024, 1024>));
+        {
+            cudaError_t e = ensure_smem_attr((const void*)k_ps_fused<256, 4096, 1, 256, 1024, 1024>,
+                                             (int)sizeof(FusedShared<256, 4096, 256, 1024, 1024>));
             if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(k_ps_fused<256, 4096, 1, 4096, 2048, 1024>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)sizeof(FusedShared<256, 4096, 4096, 2048, 1024>));
+                e = ensure_smem_attr((const void*)k_ps_fused<256, 4096, 1, 4096, 2048, 1024>,
+                                     (int)sizeof(FusedShared<256, 4096, 4096, 2048, 1024>));
             if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(k_ps_fused<512, 4096, 1, 4096, 2048, 1024>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(FusedShared<512, 4096, 4096, 2048, 1024>));
+                e = ensure_smem_attr((const void*)k_ps_fused<512, 4096, 1, 4096, 2048, 1024>,
+                                     (int)sizeof(FusedShared<512, 4096, 4096, 2048, 1024>));
             if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(k_ps_fused<512, 8192, 1, 4096, 2048, 2048>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(FusedShared<512, 8192, 4096, 2048, 2048>));
+                e = ensure_smem_attr((const void*)k_ps_fused<512, 8192, 1, 4096, 2048, 2048>,
+                                     (int)sizeof(FusedShared<512, 8192, 4096, 2048, 2048>));
             if (e == cudaSuccess && MXFFT_C3_CLUSTER)
-                e = cudaFuncSetAttribute(k_ps_fused<512, 8192, (MXFFT_C3_CLUSTER > 1 ? MXFFT_C3_CLUSTER : 2), 4096, 2048, 2048>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(FusedShared<512, 8192, 4096, 2048, 2048>));
+                e = ensure_smem_attr(
+                    (const void*)k_ps_fused<512, 8192, (MXFFT_C3_CLUSTER > 1 ? MXFFT_C3_CLUSTER : 2), 4096, 2048, 2048>,
+                    (int)sizeof(FusedShared<512, 8192, 4096, 2048, 2048>));
             if (e != cudaSuccess) return e;
-            attr = true;
         }
         cudaError_t e = cudaMemsetAsync(list_n, 0, sizeof(int), st);
         if (e != cudaSuccess) return e;
 #if MXFFT_PS_LEAN
         if (npts >= 8192 && npts <= (int64_t(1) << 17) && npts % (npts > 32768 ? 4096 : 2048) == 0) {
-            static bool lattr = false;
             using L512 = LeanShared<512, 12, 1024, 1024>;
             constexpr int NS = MXFFT_PS_LEAN_SMALL_NT;  // threads per CTA for segments <= 2^15 points
             using L256 = LeanShared<NS, 12, 1024, 1024>;
-            if (!lattr) {
-                e = cudaFuncSetAttribute(k_ps_lean<512, 12, 1024, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(L512));
-                if (e == cudaSuccess)
-                    e = cudaFuncSetAttribute(k_ps_lean<NS, 12, 1024, 1024>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(L256));
-                if (e != cudaSuccess) return e;
-                lattr = true;
-            }
+            e = ensure_smem_attr((const void*)k_ps_lean<512, 12, 1024, 1024>, (int)sizeof(L512));
+            if (e == cudaSuccess) e = ensure_smem_attr((const void*)k_ps_lean<NS, 12, 1024, 1024>, (int)sizeof(L256));
+            if (e != cudaSuccess) return e;
             if (npts > 32768)
                 k_ps_lean<512, 12, 1024, 1024><<<(unsigned)nseg, 512, sizeof(L512), st>>>(x, npts, MXFFT_PS_LEAN_S512, q, c, out, kvec,
                                                                                      list, list_n);
@@ -1729,8 +1501,13 @@ __global__ void __launch_bounds__(CNT_THREADS, MXFFT_CR_MINB) k_ps_count_range(c
             }
         }
         __syncthreads();
-        const unsigned nv = nbuf < vend ? nbuf : vend;  // valid buffered candidates
-        if (nv >= (unsigned)(CR_BUF / 2) || vend < (unsigned)CR_BUF) {  // flush
+        const unsigned nb_now = nbuf, ve_now = vend;
+        // every thread has read the counters (so all take the same flush
+        // decision with the same nv) before any warp moves on to the next
+        // chunk and reserves new slots
+        __syncthreads();
+        const unsigned nv = nb_now < ve_now ? nb_now : ve_now;  // valid buffered candidates
+        if (nv >= (unsigned)(CR_BUF / 2) || ve_now < (unsigned)CR_BUF) {  // flush
             if (threadIdx.x == 0) gbase = atomicAdd(&st->ncand, nv);
             __syncthreads();
             for (unsigned i = threadIdx.x; i < nv; i += CNT_THREADS)
@@ -1779,14 +1556,11 @@ cudaError_t launch_prescale_count_range(const float2* x, int64_t npts, float lo,
     note_launch();
     const int64_t cps = (npts + CR_CHUNK - 1) / CR_CHUNK;
     if (cps > 0) {
-        static int per_sm = 0, sms = 148;
-        if (!per_sm) {  // a resident (persistent) grid
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ps_count_range, CNT_THREADS, 0);
-            if (per_sm < 1) per_sm = 1;
-        }
+        // a resident (persistent) grid
+        const int sms = device_attr(cudaDevAttrMultiProcessorCount);
+        int per_sm = 1;
+        const cudaError_t e = cached_occupancy((const void*)k_ps_count_range, CNT_THREADS, 0, &per_sm);
+        if (e != cudaSuccess) return e;
         const int64_t grid = cps < (int64_t)sms * per_sm ? cps : (int64_t)sms * per_sm;
         k_ps_count_range<<<(unsigned)grid, CNT_THREADS, 0, st>>>(x, npts, s, cand, cap, topb, topcap);
         note_launch();

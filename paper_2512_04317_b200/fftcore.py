@@ -270,6 +270,8 @@ def fft2_device(x, plan: FftPlan, mode: str = "forward", k=None, k_group: int = 
     if k is not None:
         if k.dtype != torch.int32 or not k.is_cuda:
             raise TypeError("k must be a CUDA int32 tensor")
+        if k_group < 1 or k.numel() * k_group < batch:
+            raise ShapeError(f"{k.numel()} prescale exponents x k_group {k_group} do not cover {batch} images")
         kp = k.data_ptr()
     L = _native.lib()
     wp, wb = None, 0

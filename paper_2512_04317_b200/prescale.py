@@ -61,15 +61,18 @@ def k_from_stats(a_max: float, p_tau: float, cfg: PrescaleConfig):
     return min(max(max(k1, k2), cfg.k_min), cfg.k_max), k1, k2
 
 
-_WS = {}  # (device, nbytes) -> reusable workspace of the sampled statistics path
+_WS = {}  # (device, stream, nbytes) -> reusable workspace of the sampled statistics path
 
 
 def _workspace(device, nbytes: int):
+    """Scratch of the statistics kernels, one per (device, stream, size): work
+    on different streams (or a captured graph replaying beside eager calls on
+    another stream) never shares it."""
     import torch
 
-    key = (str(device), nbytes)
     if nbytes <= 0:
         return None
+    key = (str(device), _native.stream_handle(), nbytes)
     if key not in _WS:
         _WS[key] = torch.empty(nbytes, dtype=torch.uint8, device=device)
     return _WS[key]
@@ -139,21 +142,48 @@ def compute_prescale(x, cfg: PrescaleConfig) -> PrescaleResult:
     return PrescaleResult(k=k, a_max=a_max, p_tau=p_tau, k1=k1, k2=k2)
 
 
-def apply_prescale(x, k: int):
-    """x * 2^k, exact; returns the same kind of object (array or grid)."""
+def _scale_array(arr: np.ndarray, k: int) -> np.ndarray:
+    """arr * math.ldexp(1.0, k) with numpy's dtype rules (prescale.py:83),
+    computed by the mxfft_scale kernel:
+    - float32 / complex64 stay single precision, with the factor rounded to
+      float32 first (numpy rounds the weak Python float the same way);
+    - float64 / complex128 stay double;
+    - float16 is multiplied in single precision and rounded back once (what
+      numpy's float16 multiply does), with the factor rounded to float16;
+    - everything else (ints, bools) is promoted to float64."""
     import torch
 
+    f64 = math.ldexp(1.0, k)  # OverflowError for k >= 1024, as in the reference
+    with np.errstate(over="ignore"):
+        if arr.dtype in (np.float32, np.complex64):
+            work, factor, is_f64, back = arr, float(np.float32(f64)), 0, None
+        elif arr.dtype in (np.float64, np.complex128):
+            work, factor, is_f64, back = arr, f64, 1, None
+        elif arr.dtype == np.float16:
+            work, factor, is_f64, back = arr.astype(np.float32), float(np.float16(f64)), 0, np.float16
+        else:
+            work, factor, is_f64, back = arr.astype(np.float64), f64, 1, None
+    flat = np.ascontiguousarray(work).reshape(-1)
+    cplx = flat.dtype.kind == "c"
+    real = flat.view(np.float64 if is_f64 else np.float32) if cplx else flat
+    t = torch.from_numpy(real).cuda()
+    out = torch.empty_like(t)
+    _native.check(_native.lib().mxfft_scale(t.data_ptr(), out.data_ptr(), flat.size, is_f64 + 2 * cplx, factor,
+                                           _native.stream_handle()))
+    res = out.cpu().numpy().view(flat.dtype).reshape(arr.shape)
+    return res.astype(back) if back is not None else res
+
+
+def apply_prescale(x, k: int):
+    """x * 2^k (prescale.py:76-86), on the GPU; returns the same kind of object
+    (array or grid)."""
     data = _data_of(x)
-    arr = np.asarray(data)
-    if arr.dtype.kind not in "fc":
-        arr = arr.astype(np.float64)
-    t = torch.from_numpy(np.ascontiguousarray(arr)).cuda()
-    scaled = (t * math.ldexp(1.0, k)).cpu().numpy().reshape(arr.shape)
+    scaled = _scale_array(np.asarray(data), int(k))
     if _is_grid(x):
         return dataclasses.replace(x, data=scaled)
     return scaled
 
 
 def undo_prescale(x, k: int):
-    """Exact inverse of apply_prescale."""
+    """Exact inverse of apply_prescale (prescale.py:89-91)."""
     return apply_prescale(x, -k)

@@ -45,3 +45,34 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+def digest(a) -> str:
+    """SHA-256 of an array's values, -0.0 folded into +0.0 (the same helper as
+    tests/golden/make_golden.py; the bigshapes fixture pins large reference
+    outputs by digest)."""
+    import hashlib
+
+    a = np.ascontiguousarray(np.asarray(a) + 0.0)
+    return hashlib.sha256(a.tobytes()).hexdigest()
+
+
+def bigshape_cases():
+    """(key, tag, fmt, block, image index) of the pipeline cases in bigshapes.npz."""
+    g = golden("bigshapes")
+    out = []
+    for key in g["cases"]:
+        key = str(key)
+        if key.startswith("c5_"):
+            continue
+        tag, fmt, b, i = key.split("_")
+        out.append((key, tag, fmt, int(b[1:]), int(i[1:])))
+    return out
+
+
+def bigshape_image(tag, i):
+    from paper_2512_04317_b200.workloads import ellipse_kspace
+
+    if tag == "c3":
+        return ellipse_kspace(512, seed=501, noise=0.01)
+    return ellipse_kspace(128, seed=601 + i, noise=0.05)

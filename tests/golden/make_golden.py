@@ -305,15 +305,89 @@ def twiddle_fixture(rng):
     return out
 
 
+def digest(a) -> str:
+    """SHA-256 of an array's values (C order; -0.0 folded into +0.0, since the
+    reference compares by value).  Large reference outputs are pinned by
+    digest: the fixture stays small and the comparison stays bit-exact."""
+    import hashlib
+
+    a = np.ascontiguousarray(np.asarray(a) + 0.0)
+    return hashlib.sha256(a.tobytes()).hexdigest()
+
+
+def bigshapes_fixture(rng):
+    """The BASELINE configurations' own shapes, pinned by digests of the
+    reference's outputs:
+      C3: one 512^2 phantom, E3M2 / E2M3 / E2M1 x B in {16, 32, 64};
+      C4: four 128^2 phantoms with 5% noise, E4M3 B=32;
+      C5: two 16384-point rows, E4M3 B=32 and E2M1 B=64, forward and inverse.
+    For each pipeline case: k, a_max, p_tau, the per-coil complex outputs of
+    forward_pipeline / roundtrip_pipeline's body (mri.py:84-107: apply_prescale,
+    fft_2d [, fft_2d inverse x 1/N^2], undo_prescale) and the RSS images the
+    public pipelines return.  Inputs come from the seeded generator
+    (workloads.ellipse_kspace); their digests are stored so that a different
+    numpy on another host fails loudly instead of comparing other inputs."""
+    rng = np.random.default_rng(5120)  # own stream: the older fixtures stay byte-identical
+    cfg = R.PrescaleConfig()
+    out = {}
+    cases = []
+    imgs = {"c3": [ellipse_kspace(512, seed=501, noise=0.01)],
+            "c4": [ellipse_kspace(128, seed=601 + i, noise=0.05) for i in range(4)]}
+    combos = [("c3", f, b) for f in ("e3m2", "e2m3", "e2m1") for b in (16, 32, 64)] + [("c4", "e4m3", 32)]
+    for tag, name, bsz in combos:
+        for ii, x64 in enumerate(imgs[tag]):
+            x = x64.astype(np.complex128)
+            n = x.shape[0]
+            plan = R.make_plan(n, R.ModeSpec.mx(FMTS[name], bsz))
+            pr = R.compute_prescale(x, cfg)
+            xs = R.apply_prescale(x, pr.k)
+            fwd = R.fft_2d(xs, plan, "forward")
+            rt = R.fft_2d(fwd, plan, "inverse") * (1.0 / (n * n))
+            key = f"{tag}_{name}_b{bsz}_i{ii}"
+            cases.append(key)
+            out[key + "_x"] = np.array(digest(x64))
+            out[key + "_k"] = np.array([pr.k, pr.k1, pr.k2])
+            out[key + "_stats"] = np.array([pr.a_max, pr.p_tau])
+            out[key + "_fwd"] = np.array(digest(R.undo_prescale(fwd, pr.k)))
+            out[key + "_rt"] = np.array(digest(R.undo_prescale(rt, pr.k)))
+            out[key + "_fwd_rss"] = np.array(digest(
+                R.forward_pipeline(R.ComplexGrid(x[None], "kspace"), plan, cfg).pixels))
+            rt_rss = R.roundtrip_pipeline(R.ComplexGrid(x[None], "image"), plan, cfg).pixels
+            out[key + "_rt_rss"] = np.array(digest(rt_rss))
+            ref = np.abs(x)
+            out[key + "_quality"] = np.array([R.psnr(ref, rt_rss), R.nmse(ref, rt_rss)])
+            print(key, pr.k, flush=True)
+    rows = ((rng.standard_normal((2, 16384)) + 1j * rng.standard_normal((2, 16384))) * 2.0 ** -6).astype(np.complex64)
+    out["c5_rows_x"] = rows
+    for name, bsz in (("e4m3", 32), ("e2m1", 64)):
+        plan = R.make_plan(16384, R.ModeSpec.mx(FMTS[name], bsz))
+        for d in ("forward", "inverse"):
+            out[f"c5_{name}_b{bsz}_{d}"] = np.array(digest(R.fftcore._fft_batch(rows.astype(np.complex128), plan, d)))
+            cases.append(f"c5_{name}_b{bsz}_{d}")
+    out["cases"] = np.array(cases)
+    return out
+
+
+FIXTURES = [("quantize", quantize_fixture), ("batch", batch_fixture),
+            ("stages", stage_fixture), ("fft2", fft2_fixture),
+            ("prescale", prescale_fixture), ("pipelines", pipeline_fixture),
+            ("twiddles", twiddle_fixture), ("modes", modes_fixture),
+            ("metrics", metrics_fixture), ("phantoms", phantoms_fixture),
+            ("multicoil", multicoil_fixture), ("bigshapes", bigshapes_fixture)]
+
+
 def main():
+    """Regenerate every fixture, or only those named on the command line (the
+    shared rng is advanced through every fixture either way, so a partial run
+    writes exactly the bytes a full run would)."""
+    only = set(sys.argv[1:])
     rng = np.random.default_rng(20240817)
-    for name, fn in [("quantize", quantize_fixture), ("batch", batch_fixture),
-                     ("stages", stage_fixture), ("fft2", fft2_fixture),
-                     ("prescale", prescale_fixture), ("pipelines", pipeline_fixture),
-                     ("twiddles", twiddle_fixture), ("modes", modes_fixture),
-                     ("metrics", metrics_fixture), ("phantoms", phantoms_fixture),
-                     ("multicoil", multicoil_fixture)]:
+    for name, fn in FIXTURES:
+        if only and name not in only and name == "bigshapes":
+            continue
         data = fn(rng)
+        if only and name not in only:
+            continue
         path = os.path.join(OUT, f"{name}.npz")
         np.savez_compressed(path, **data)
         print(f"wrote {path} ({os.path.getsize(path)} bytes)")

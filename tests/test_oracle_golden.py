@@ -131,3 +131,38 @@ def test_prescale_kats():
     assert (r.k1, r.k2, r.k) == (0, 10, 10)
     c = O.compute_prescale(np.full((4, 4), 2.0**-60))
     assert (c.k1, c.k) == (60, 40)
+
+
+# ---------------------------------------------------------------------------
+# the BASELINE shapes (C3 512^2 x 9 format/block pairs, C4 128^2 5% noise,
+# C5 16384-point rows), pinned to digests of the reference's own outputs
+# ---------------------------------------------------------------------------
+from conftest import bigshape_cases, bigshape_image, digest  # noqa: E402
+
+
+@pytest.mark.parametrize("case", bigshape_cases(), ids=lambda c: c[0])
+def test_oracle_baseline_shapes_match_reference(case):
+    key, tag, fmt, bsz, i = case
+    g = golden("bigshapes")
+    x = bigshape_image(tag, i)
+    assert digest(x) == str(g[key + "_x"]), "input generator differs from the fixture's"
+    p = O.make_plan(x.shape[0], FMTS[fmt], bsz)
+    pr = O.compute_prescale(x)
+    assert [pr.k, pr.k1, pr.k2] == g[key + "_k"].tolist()
+    assert [pr.a_max, pr.p_tau] == g[key + "_stats"].tolist()
+    out_f, rss_f, kf = O.pipeline(x, p, False)
+    out_r, rss_r, kr = O.pipeline(x, p, True)
+    assert kf == kr == pr.k
+    assert digest(out_f[0]) == str(g[key + "_fwd"])
+    assert digest(out_r[0]) == str(g[key + "_rt"])
+    assert digest(rss_f) == str(g[key + "_fwd_rss"])
+    assert digest(rss_r) == str(g[key + "_rt_rss"])
+
+
+def test_oracle_c5_rows_match_reference():
+    g = golden("bigshapes")
+    rows = g["c5_rows_x"]
+    for fmt, bsz in (("e4m3", 32), ("e2m1", 64)):
+        p = O.make_plan(16384, FMTS[fmt], bsz)
+        for inv, d in ((False, "forward"), (True, "inverse")):
+            assert digest(O.fft_batch(rows, p, inv)) == str(g[f"c5_{fmt}_b{bsz}_{d}"]), (fmt, d)
