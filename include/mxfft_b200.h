@@ -225,6 +225,11 @@ int32_t mxfft_rss(const void* x, int32_t is_c128, int64_t groups, int32_t coils,
  * mxfft_pipeline_fused_supported(plan) != 0 (n = 128, a hardware MX format,
  * B in {16, 32, 64}). */
 int32_t mxfft_pipeline_fused_supported(mxfft_plan plan);
+/* Scheduling knob: with on != 0 (the default) mxfft_fft2 runs batches of
+ * n = 128 images (plans for which mxfft_pipeline_fused_supported holds) on the
+ * same one-image-per-CTA kernel, given the per-image k, instead of four line
+ * passes; results are identical. */
+void mxfft_fused_image(int32_t on);
 int32_t mxfft_pipeline_fused(mxfft_plan plan, const void* x, void* y, int64_t nimg, int32_t roundtrip,
                              const mxfft_prescale_cfg* cfg, mxfft_prescale_result* d_res, int32_t* d_k,
                              uintptr_t stream);

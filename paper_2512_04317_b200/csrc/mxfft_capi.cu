@@ -332,6 +332,15 @@ int32_t mxfft_fft2(mxfft_plan plan, const void* x, void* y, int64_t batch, int32
     if (batch == 0) return MXFFT_OK;
     const Plan& p = plan->p;
     cudaStream_t s = (cudaStream_t)stream;
+    if (g_fused_image && mx_image_ok(p)) {
+        // n = 128: one image per CTA, every pass in shared memory (exact replays
+        // re-read an image from x before any of its outputs is written, so x
+        // may alias y here too)
+        const mxfft_prescale_cfg dummy{1.0, 1.0, 1.0, 0, 0};
+        CK(run_mx_image(p, x, y, batch, mode, dummy, nullptr, nullptr, d_k, k_group > 0 ? k_group : 1, s),
+           "fft2 (fused image kernel)");
+        return MXFFT_OK;
+    }
     const int64_t nn = (int64_t)p.n * p.n;
     const int npass = mode == 2 ? 4 : 2;
     // With a workspace every pass is a row pass that stores its lines transposed
@@ -476,6 +485,8 @@ int32_t mxfft_rss(const void* x, int32_t is_c128, int64_t groups, int32_t coils,
     return MXFFT_OK;
 }
 
+void mxfft_fused_image(int32_t on) { mxfft::g_fused_image = on ? 1 : 0; }
+
 int32_t mxfft_pipeline_fused_supported(mxfft_plan plan) { return plan && mx_image_ok(plan->p) ? 1 : 0; }
 
 int32_t mxfft_pipeline_fused(mxfft_plan plan, const void* x, void* y, int64_t nimg, int32_t roundtrip,
@@ -488,7 +499,8 @@ int32_t mxfft_pipeline_fused(mxfft_plan plan, const void* x, void* y, int64_t ni
         return fail(MXFFT_ERR_UNSUPPORTED_SIZE, "the fused pipeline needs n = 128, a hardware MX format and B in {16, 32, 64}");
     if (!d_res) return fail(MXFFT_ERR_VALUE, "null result rows");
     if (x == y) return fail(MXFFT_ERR_VALUE, "the fused pipeline is out of place (exact replays re-read the input)");
-    CK(run_mx_image(plan->p, x, y, nimg, roundtrip ? 1 : 0, *cfg, d_res, d_k, (cudaStream_t)stream), "pipeline_fused");
+    CK(run_mx_image(plan->p, x, y, nimg, roundtrip ? 2 : 0, *cfg, d_res, d_k, nullptr, 1, (cudaStream_t)stream),
+       "pipeline_fused");
     return MXFFT_OK;
 }
 

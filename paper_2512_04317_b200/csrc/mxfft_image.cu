@@ -10,19 +10,25 @@ cudaError_t run_mx_image_e2m3(const ImageArgs&, int, size_t, int, cudaStream_t);
 cudaError_t run_mx_image_e3m2(const ImageArgs&, int, size_t, int, cudaStream_t);
 cudaError_t run_mx_image_e2m1(const ImageArgs&, int, size_t, int, cudaStream_t);
 
+int g_fused_image = 1;
+
 bool mx_image_ok(const Plan& p) {
     return p.n == IM_N && p.fmt.id != F_GENERIC && (p.cpb == 8 || p.cpb == 16 || p.cpb == 32);
 }
 
-cudaError_t run_mx_image(const Plan& p, const void* x, void* y, int64_t nimg, int roundtrip,
+cudaError_t run_mx_image(const Plan& p, const void* x, void* y, int64_t nimg, int mode,
                          const mxfft_prescale_cfg& cfg, mxfft_prescale_result* res, int32_t* kvec,
-                         cudaStream_t st) {
+                         const int32_t* kin, int k_group, cudaStream_t st) {
     if (nimg <= 0) return cudaSuccess;
     ImageArgs a{};
     a.in = reinterpret_cast<const float2*>(x);
     a.out = reinterpret_cast<float2*>(y);
     a.nimg = nimg;
-    a.npass = roundtrip ? 4 : 2;
+    a.npass = mode == 2 ? 4 : 2;
+    a.first_inverse = mode == 1;
+    a.kin = kin;
+    a.stats = res != nullptr;
+    a.k_group = k_group > 0 ? k_group : 1;
     a.tw_fwd = p.d_tw16_fwd;
     a.tw_inv = p.d_tw16_inv;
     a.twe = p.d_twe8;

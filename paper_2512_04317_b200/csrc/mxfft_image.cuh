@@ -57,6 +57,10 @@ struct ImageArgs {
     double q;
     mxfft_prescale_result* res;
     int32_t* kvec;
+    const int32_t* kin;  // precomputed per-image exponents (k = kin[img / k_group])
+    int k_group;
+    int stats;           // 1: compute_prescale's statistics in the kernel (res, kvec); 0: k from kin (or 0)
+    int first_inverse;   // passes 1-2 use the inverse twiddles (an inverse-only transform)
     int tile_off;  // byte offset of the tile in dynamic shared memory (4 KB aligned in the window)
     // exact replay: reference-literal tables of the plan
     FmtDesc fmt;
@@ -805,16 +809,21 @@ __global__ void __launch_bounds__(IM_NT, 1) k_mx_image(ImageArgs a) {
         __syncthreads();  // the tile has landed (and the twiddles are in place)
         IM_T(0)
         im_prefetch_l2(a, img + 2 * (int64_t)gridDim.x);
-        im_bracket(tile_sh, F, a);
-        im_select(F, a, img, tile_sh);
-        if (F.fallback) {  // block-uniform; the tile is still intact
+        int k = 0;
+        if (!a.stats) {
+            k = a.kin ? __ldg(a.kin + img / a.k_group) : 0;
+        } else {
+            im_bracket(tile_sh, F, a);
+            im_select(F, a, img, tile_sh);
+            if (F.fallback) {  // block-uniform; the tile is still intact
 #ifdef MXFFT_IM_TIMING
-            ++nfb;
+                ++nfb;
 #endif
-            im_stats_exact(tile_sh, F, a, img);
+                im_stats_exact(tile_sh, F, a, img);
+            }
+            k = F.k;
         }
         IM_T(1)
-        const int k = F.k;
         bool bad = false;
         float2 x[32];
         int U, V, P, H;
@@ -823,11 +832,12 @@ __global__ void __launch_bounds__(IM_NT, 1) k_mx_image(ImageArgs a) {
         for (int m = 0; m < 32; ++m) x[rev_c<5>(m)] = lds64(g_row ^ (16u * (unsigned)dsw((m * IM_T) >> 1)));
         // the statistics are done with the shared union: zero it for the next
         // image's sample histogram (many barriers pass before that is read)
-        for (int i = tid; i < (int)(sizeof(F.u) / 4); i += IM_NT) reinterpret_cast<unsigned*>(&F.u)[i] = 0;
+        if (a.stats)
+            for (int i = tid; i < (int)(sizeof(F.u) / 4); i += IM_NT) reinterpret_cast<unsigned*>(&F.u)[i] = 0;
         scale32<false>(x, k, bad);
-        L.tw = twf;
-        L.tw_sh = (unsigned)__cvta_generic_to_shared(twf);
-        L.sigma = 1.f;
+        L.tw = a.first_inverse ? twi : twf;
+        L.tw_sh = (unsigned)__cvta_generic_to_shared(a.first_inverse ? twi : twf);
+        L.sigma = a.first_inverse ? -1.f : 1.f;
         run_stages<ID, CPB, false, IM_LT>(x, U, V, P, H, L, tile_sh, ebase, &dbg, bad);
         publish4(x, tile_sh, ebase, P, H);
 #pragma unroll 1

@@ -99,9 +99,12 @@ extern int g_profile_flags;  // < 0: off (see mxfft_profile_stage_limit)
 bool mx_lines_ok(const Plan& p);
 // fused small-image pipeline (mxfft_image.cu)
 bool mx_image_ok(const Plan& p);
-cudaError_t run_mx_image(const Plan& p, const void* x, void* y, int64_t nimg, int roundtrip,
+// mode 0 forward, 1 inverse, 2 round trip (x 1/n^2); kin: precomputed k (no
+// statistics in the kernel), else the statistics run in the kernel (res, kvec)
+cudaError_t run_mx_image(const Plan& p, const void* x, void* y, int64_t nimg, int mode,
                          const mxfft_prescale_cfg& cfg, mxfft_prescale_result* res, int32_t* kvec,
-                         cudaStream_t st);
+                         const int32_t* kin, int k_group, cudaStream_t st);
+extern int g_fused_image;  // mxfft_fft2 runs n = 128 batches on the fused image kernel (mxfft_fused_image)
 cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st);
 cudaError_t run_lines(const Plan& p, const LinePass& lp, cudaStream_t st);
 

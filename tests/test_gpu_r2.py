@@ -313,9 +313,20 @@ def _fused_vs_unfused(mx, torch, x, fmt, bsz, roundtrip):
     assert mx.fused_pipeline_supported(p)
     cfg = mx.PrescaleConfig()
     xd = torch.from_numpy(x).cuda()
+    from paper_2512_04317_b200 import _native
+
     y1, k1, r1 = mx.pipeline_device(xd, p, cfg, roundtrip, fused=True)
-    y0, k0, r0 = mx.pipeline_device(xd, p, cfg, roundtrip, fused=False)
+    _native.lib().mxfft_fused_image(0)  # the reference path: statistics kernel + four line passes
+    try:
+        y0, k0, r0 = mx.pipeline_device(xd, p, cfg, roundtrip, fused=False)
+        torch.cuda.synchronize()
+    finally:
+        _native.lib().mxfft_fused_image(1)
+    y2, k2, r2 = mx.pipeline_device(xd, p, cfg, roundtrip, fused=False)  # statistics + fused fft2
     torch.cuda.synchronize()
+    assert torch.equal(k2, k0) and torch.equal(r2, r0)
+    a2, b2 = y2.cpu().numpy(), y0.cpu().numpy()
+    assert ((a2 == b2) | (np.isnan(a2) & np.isnan(b2))).all()
     assert torch.equal(k1, k0)
     d1, d0 = mx.prescale.decode_results(r1), mx.prescale.decode_results(r0)
     ok = (d0["flags"] & 1) == 0  # non-finite images: only the flag matters (the reference raises)
@@ -389,3 +400,29 @@ def test_fused_pipeline_host_and_graph(mx, torch):
         mx.pipeline_host(h, p, cfg, True, out_host=out)
     y, _, _ = mx.pipeline_device(torch.from_numpy(x).cuda(), p, cfg, True)
     assert torch.equal(out, y.cpu())
+
+
+@pytest.mark.parametrize("mode", ["forward", "inverse", "roundtrip"])
+def test_fused_fft2_modes_inplace_kgroups(mx, torch, mode):
+    """mxfft_fft2 at n = 128 (the fused image kernel, given k) equals the four
+    line passes for every mode, out of place and in place, with per-stack k
+    (k_group = 2) and without k."""
+    from paper_2512_04317_b200 import _native
+    from paper_2512_04317_b200.workloads import ellipse_kspace_batch
+
+    x = torch.from_numpy(ellipse_kspace_batch(200, 128, seed=5, noise=0.05) * np.float32(2.0**-10)).cuda()
+    k = torch.tensor(np.random.default_rng(1).integers(-6, 7, 100), dtype=torch.int32, device="cuda")
+    p = mx.make_plan(128, mx.ModeSpec.mx(mx.E5M2, 16))
+    L = _native.lib()
+    for kk, g in ((None, 1), (k, 2)):
+        L.mxfft_fused_image(0)
+        try:
+            want = mx.fft2_device(x, p, mode, k=kk, k_group=g)
+            torch.cuda.synchronize()
+        finally:
+            L.mxfft_fused_image(1)
+        got = mx.fft2_device(x, p, mode, k=kk, k_group=g)
+        assert torch.equal(got, want), (mode, g)
+        y = x.clone()
+        mx.fft2_device(y, p, mode, k=kk, k_group=g, out=y)
+        assert torch.equal(y, want), ("in place", mode, g)
