@@ -62,6 +62,9 @@
 #ifndef MXFFT_UNROLL_SMEM
 #define MXFFT_UNROLL_SMEM 0  // unroll the shared-memory stages of the n-specialised kernels
 #endif
+#ifndef MXFFT_TW_FIRST
+#define MXFFT_TW_FIRST 0  // paired stages: twiddle loads before the exchange loads (measured: no gain)
+#endif
 #ifndef MXFFT_LOCAL_STAGES
 #define MXFFT_LOCAL_STAGES 5  // unrolled register stages before the shared-memory loop
 #endif
@@ -502,6 +505,27 @@ __device__ __forceinline__ void scale32(float2 (&x)[32], int e, bool& bad) {
     }
 }
 
+// global stores with an explicit state space (a generic ST has to resolve the
+// window of every address); MXFFT_STG=0 keeps plain C++ stores
+#ifndef MXFFT_STG
+#define MXFFT_STG 0  // measured: asm st.global (a "memory" clobber) 73.7 -> 77.5 us on the C2 pass
+#endif
+__device__ __forceinline__ void stg128(float4* p, float4 v) {
+#if MXFFT_STG
+    asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+#else
+    *p = v;
+#endif
+}
+__device__ __forceinline__ void stg64(float2* p, float2 v) {
+#if MXFFT_STG
+    asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+#else
+    *p = v;
+#endif
+}
+
 // shared memory accesses by 32-bit shared-window address
 __device__ __forceinline__ void sts128(unsigned addr, float2 a, float2 b) {
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a.x), "f"(a.y), "f"(b.x),
@@ -666,13 +690,9 @@ __device__ __forceinline__ void pair_stage(float2 (&x)[32], int& P, int& H, cons
     const int u0 = 8 * L.tl, j0 = u0 & (h - 1);
     P = ((u0 >> s) << (s + 2)) + j0;
     H = h;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const unsigned a = run4_addr(rb, ebase + P + k * h);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) lds128(a ^ (16u * c), x[8 * k + 2 * c], x[8 * k + 2 * c + 1]);
-    }
     unsigned w0[8], w1[8], w2[8];
+#if MXFFT_TW_FIRST
+    // the twiddles do not depend on the exchange: their loads go out first
 #pragma unroll
     for (int i = 0; i < 8; i += 4) {
         const uint4 q0 = lds128u(L.tw_sh + 4u * (unsigned)tws(h + j0 + i));
@@ -682,6 +702,24 @@ __device__ __forceinline__ void pair_stage(float2 (&x)[32], int& P, int& H, cons
         w1[i] = q1.x, w1[i + 1] = q1.y, w1[i + 2] = q1.z, w1[i + 3] = q1.w;
         w2[i] = q2.x, w2[i + 1] = q2.y, w2[i + 2] = q2.z, w2[i + 3] = q2.w;
     }
+#endif
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const unsigned a = run4_addr(rb, ebase + P + k * h);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) lds128(a ^ (16u * c), x[8 * k + 2 * c], x[8 * k + 2 * c + 1]);
+    }
+#if !MXFFT_TW_FIRST
+#pragma unroll
+    for (int i = 0; i < 8; i += 4) {
+        const uint4 q0 = lds128u(L.tw_sh + 4u * (unsigned)tws(h + j0 + i));
+        const uint4 q1 = lds128u(L.tw_sh + 4u * (unsigned)tws(2 * h + j0 + i));
+        const uint4 q2 = lds128u(L.tw_sh + 4u * (unsigned)tws(3 * h + j0 + i));
+        w0[i] = q0.x, w0[i + 1] = q0.y, w0[i + 2] = q0.z, w0[i + 3] = q0.w;
+        w1[i] = q1.x, w1[i + 1] = q1.y, w1[i + 2] = q1.z, w1[i + 3] = q1.w;
+        w2[i] = q2.x, w2[i + 1] = q2.y, w2[i + 2] = q2.z, w2[i + 3] = q2.w;
+    }
+#endif
     const int e0 = L.twe[h + j0], e1 = L.twe[2 * h + j0], e2 = L.twe[3 * h + j0];
     float2 a[8], b[8], c[8], d[8];
 #pragma unroll
@@ -1006,7 +1044,7 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
                 if (tid + NT * k < lim) {
                     float2 p0, p1;
                     lds128(caddr(bcur, rch ^ dsw(NT * k), 0), p0, p1);
-                    dst[NT * k] = make_float4(p0.x, p0.y, p1.x, p1.y);
+                    stg128(dst + NT * k, make_float4(p0.x, p0.y, p1.x, p1.y));
                 }
             }
 #if MXFFT_PAIR_STORE
@@ -1030,7 +1068,7 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
                     o[k] = make_float4(v0.x, v0.y, v1.x, v1.y);
                 }
 #pragma unroll
-                for (int k = 0; k < PB; ++k) dst[(k0 + k) * rs] = o[k];
+                for (int k = 0; k < PB; ++k) stg128(dst + (k0 + k) * rs, o[k]);
             }
 #endif
         } else {  // columns, or rows stored transposed: line gl -> column (gl mod n) of image gl/n
@@ -1044,11 +1082,11 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
 #pragma unroll
                 for (int k = 0; k < 32; ++k) o[k] = lds64(caddr(bcur, tch ^ dsw((T * k) >> 1), th ^ ((T * k) & 1)));
 #pragma unroll
-                for (int k = 0; k < 32; ++k) dst[(int64_t)k * T * N] = o[k];
+                for (int k = 0; k < 32; ++k) stg64(dst + (int64_t)k * T * N, o[k]);
 #else
 #pragma unroll
                 for (int k = 0; k < 32; ++k)
-                    dst[(int64_t)k * T * N] = lds64(caddr(bcur, tch ^ dsw((T * k) >> 1), th ^ ((T * k) & 1)));
+                    stg64(dst + (int64_t)k * T * N, lds64(caddr(bcur, tch ^ dsw((T * k) >> 1), th ^ ((T * k) & 1))));
 #endif
             }
         }
@@ -1172,11 +1210,11 @@ __device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
                 if (oes == 1) {
 #pragma unroll
                     for (int i = 0; i < 8; i += 2)
-                        *reinterpret_cast<float4*>(dk + i) =
-                            make_float4(x[8 * k + i].x, x[8 * k + i].y, x[8 * k + i + 1].x, x[8 * k + i + 1].y);
+                        stg128(reinterpret_cast<float4*>(dk + i),
+                               make_float4(x[8 * k + i].x, x[8 * k + i].y, x[8 * k + i + 1].x, x[8 * k + i + 1].y));
                 } else {
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) dk[i * oes] = x[8 * k + i];
+                    for (int i = 0; i < 8; ++i) stg64(dk + i * oes, x[8 * k + i]);
                 }
             }
             __syncthreads();

@@ -28,6 +28,8 @@ for path in libs:
         if hasattr(L, name):
             getattr(L, name).argtypes = argt
             getattr(L, name).restype = rest
+    if hasattr(L, "mxfft_fused_image"):
+        L.mxfft_fused_image(int(os.environ.get("AB_FUSED", "0")))  # A/B the line passes unless asked
     h = ctypes.c_void_p()
     assert L.mxfft_plan_create(ctypes.byref(h), n, ctypes.byref(c), 32, tw.ctypes.data, 0) == 0
     wsb = int(L.mxfft_fft2_workspace_bytes(h, batch))
