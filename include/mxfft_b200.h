@@ -249,6 +249,18 @@ int32_t mxfft_rss_scaled(const void* x, int32_t is_c128, int64_t groups, int32_t
 int32_t mxfft_prescale_apply_c128(const void* x, void* y, int64_t nseg, int64_t seg_points, const int32_t* d_k,
                                   uintptr_t stream);
 
+/* _mx_multiply_batch (fftcore.py:150-183) / butterfly_mx (fftcore.py:186-235):
+ * v complex128 (rows, m) in blocks of cpb complex values; twiddle codes
+ * wcr, wci (m/cpb, cpb) and scales ws (m/cpb), FP64, shared by every row.
+ * wv (complex128 (rows, m), may be NULL) receives the decoded MX products w*v
+ * (v encoded per block, products in the reference's product dtype,
+ * renormalized, requantized); with u (complex128, may be NULL) also
+ * y0 = u32 + wv32 and y1 = u32 - wv32 (complex64).  *d_nonfinite is set
+ * for a non-finite v block (the reference raises InvalidValue). */
+int32_t mxfft_mx_multiply_f64(const void* v, const double* wcr, const double* wci, const double* ws, int64_t rows,
+                              int32_t m, int32_t cpb, const mxfft_format* fmt, void* wv, const void* u, void* y0,
+                              void* y1, int32_t* d_nonfinite, uintptr_t stream);
+
 /* data * math.ldexp(1.0, k) (apply_prescale / undo_prescale, prescale.py:76-91)
  * on n elements of dtype 0 = float32, 1 = float64, 2 = complex64,
  * 3 = complex128; `factor` is 2^k already rounded to the array's precision

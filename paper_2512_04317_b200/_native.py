@@ -71,6 +71,7 @@ SIGNATURES = {
     "mxfft_pipeline_fused": ([_vp, _vp, _vp, _i64, _i32, ctypes.POINTER(PrescaleCfgC), _vp, _vp, _u], _i32),
     "mxfft_rss_scaled": ([_vp, _i32, _i64, _i32, _i64, _vp, _i32, _i32, _vp, _u], _i32),
     "mxfft_prescale_apply_c128": ([_vp, _vp, _i64, _i64, _vp, _u], _i32),
+    "mxfft_mx_multiply_f64": ([_vp, _vp, _vp, _vp, _i64, _i32, _i32, _fp, _vp, _vp, _vp, _vp, _vp, _u], _i32),
     "mxfft_scale": ([_vp, _vp, _i64, _i32, ctypes.c_double, _u], _i32),
     "mxfft_cabs": ([_vp, _i32, _i64, _vp, _u], _i32),
     "mxfft_prescale_sample_keys": ([_vp, _i64, _i64, _vp, _u], _i32),

@@ -520,6 +520,20 @@ int32_t mxfft_prescale_apply_c128(const void* x, void* y, int64_t nseg, int64_t 
     return MXFFT_OK;
 }
 
+int32_t mxfft_mx_multiply_f64(const void* v, const double* wcr, const double* wci, const double* ws, int64_t rows,
+                              int32_t m, int32_t cpb, const mxfft_format* fmt, void* wv, const void* u, void* y0,
+                              void* y1, int32_t* d_nonfinite, uintptr_t stream) {
+    std::string why;
+    if (!check_fmt(fmt, why)) return fail(MXFFT_ERR_VALUE, why);
+    if (rows < 0 || m < 0) return fail(MXFFT_ERR_SHAPE, "negative size");
+    if (cpb < 1 || m % cpb) return fail(MXFFT_ERR_SHAPE, "cpb must divide m (fftcore.py:139-141 reshape)");
+    if (u && (!y0 || !y1)) return fail(MXFFT_ERR_VALUE, "butterfly outputs missing");
+    CK(launch_mx_multiply(v, wcr, wci, ws, rows, m, cpb, desc_of(fmt), wv, u, y0, y1, d_nonfinite,
+                          (cudaStream_t)stream),
+       "mx_multiply_f64");
+    return MXFFT_OK;
+}
+
 int32_t mxfft_scale(const void* x, void* y, int64_t n, int32_t dtype, double factor, uintptr_t stream) {
     if (n < 0) return fail(MXFFT_ERR_SHAPE, "negative size");
     if (dtype < 0 || dtype > 3) return fail(MXFFT_ERR_VALUE, "dtype must be 0 (f32), 1 (f64), 2 (c64) or 3 (c128)");

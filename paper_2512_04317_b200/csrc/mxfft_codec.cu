@@ -192,6 +192,110 @@ cudaError_t plan_encode(Plan& p, const double* d_tw, cudaStream_t st) {
     return cudaSuccess;
 }
 
+// _mx_multiply_batch (fftcore.py:150-183) and butterfly_mx (fftcore.py:186-235)
+// on FP64 operands, one thread per MX block of cpb complex values: the v block
+// is encoded (fftcore.py:131-147: amax of |re|, |im|, shared power-of-two
+// scale, quantize_array of v * 2^-e), the mantissa-space products are taken in
+// the reference's product dtype (FP32 unless the format is too wide,
+// fftcore.py:163), renormalized by 2^-shift when the block maximum exceeds
+// max_finite (exact integer shift, fftcore.py:172-177), requantized and
+// decoded with the scale ws * sv * 2^shift.  wv (complex128) receives the
+// decoded products; with u, y0 = u32 + wv32 and y1 = u32 - wv32 (complex64).
+// Twiddle tables (wcr, wci: nb x cpb, ws: nb) are shared by every row.
+__global__ void k_mx_multiply(const double2* __restrict__ v, const double* __restrict__ wcr,
+                              const double* __restrict__ wci, const double* __restrict__ ws, int64_t rows, int m,
+                              int cpb, FmtDesc f, double2* __restrict__ wv, const double2* __restrict__ u,
+                              float2* __restrict__ y0, float2* __restrict__ y1, int32_t* nonfinite) {
+    const int nb = m / cpb;
+    for (int64_t gb = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gb < rows * nb;
+         gb += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = gb / nb;
+        const int blk = (int)(gb - row * nb);
+        const double2* vb = v + row * m + (int64_t)blk * cpb;
+        double amax = 0.0;
+        bool bad = false;
+        for (int i = 0; i < cpb; ++i) {
+            const double2 t = vb[i];
+            bad |= !isfinite(t.x) || !isfinite(t.y);
+            amax = fmax(amax, fmax(fabs(t.x), fabs(t.y)));
+        }
+        if (bad) {
+            if (nonfinite) *nonfinite = 1;
+            continue;
+        }
+        const int se = block_scale_exp(amax, f);
+        const double inv = ldexp(1.0, -se);
+        const double* xr = wcr + (int64_t)blk * cpb;
+        const double* xi = wci + (int64_t)blk * cpb;
+        // products and their block maximum
+        double ap = 0.0;
+        for (int i = 0; i < cpb; ++i) {
+            const double2 t = vb[i];
+            const double yr = quantize_ref(__dmul_rn(t.x, inv), f), yi = quantize_ref(__dmul_rn(t.y, inv), f);
+            if (f.prod_f32) {
+                const float pr = __fsub_rn(__fmul_rn((float)xr[i], (float)yr), __fmul_rn((float)xi[i], (float)yi));
+                const float pi = __fadd_rn(__fmul_rn((float)xr[i], (float)yi), __fmul_rn((float)xi[i], (float)yr));
+                ap = fmax(ap, (double)fmaxf(fabsf(pr), fabsf(pi)));
+            } else {
+                const double pr = __dsub_rn(__dmul_rn(xr[i], yr), __dmul_rn(xi[i], yi));
+                const double pi = __dadd_rn(__dmul_rn(xr[i], yi), __dmul_rn(xi[i], yr));
+                ap = fmax(ap, fmax(fabs(pr), fabs(pi)));
+            }
+        }
+        int sh = 0;
+        if (ap > f.max_finite) {
+            int ea, em;
+            const double ma = frexp(ap, &ea), mm = frexp(f.max_finite, &em);
+            sh = ea - em + (ma > mm ? 1 : 0);  // = ceil(log2(ap / max_finite)), exactly
+        }
+        const double s_out = __dmul_rn(__dmul_rn(ws[blk], ldexp(1.0, se)), ldexp(1.0, sh));
+        for (int i = 0; i < cpb; ++i) {
+            const double2 t = vb[i];
+            const double yr = quantize_ref(__dmul_rn(t.x, inv), f), yi = quantize_ref(__dmul_rn(t.y, inv), f);
+            double pr, pi;
+            if (f.prod_f32) {
+                float r = __fsub_rn(__fmul_rn((float)xr[i], (float)yr), __fmul_rn((float)xi[i], (float)yi));
+                float im = __fadd_rn(__fmul_rn((float)xr[i], (float)yi), __fmul_rn((float)xi[i], (float)yr));
+                if (sh) {
+                    const float fac = (float)ldexp(1.0, -sh);
+                    r = __fmul_rn(r, fac);
+                    im = __fmul_rn(im, fac);
+                }
+                pr = r;
+                pi = im;
+            } else {
+                pr = __dsub_rn(__dmul_rn(xr[i], yr), __dmul_rn(xi[i], yi));
+                pi = __dadd_rn(__dmul_rn(xr[i], yi), __dmul_rn(xi[i], yr));
+                if (sh) {
+                    pr = __dmul_rn(pr, ldexp(1.0, -sh));
+                    pi = __dmul_rn(pi, ldexp(1.0, -sh));
+                }
+            }
+            const double2 w = make_double2(__dmul_rn(quantize_ref(pr, f), s_out), __dmul_rn(quantize_ref(pi, f), s_out));
+            const int64_t o = row * m + (int64_t)blk * cpb + i;
+            if (wv) wv[o] = w;
+            if (u) {
+                const double2 uu = u[o];
+                const float ur = (float)uu.x, ui = (float)uu.y, wr = (float)w.x, wi = (float)w.y;
+                y0[o] = make_float2(__fadd_rn(ur, wr), __fadd_rn(ui, wi));
+                y1[o] = make_float2(__fsub_rn(ur, wr), __fsub_rn(ui, wi));
+            }
+        }
+    }
+}
+
+cudaError_t launch_mx_multiply(const void* v, const double* wcr, const double* wci, const double* ws, int64_t rows,
+                               int m, int cpb, const FmtDesc& f, void* wv, const void* u, void* y0, void* y1,
+                               int32_t* nonfinite, cudaStream_t st) {
+    const int64_t nblk = rows * (m / cpb);
+    if (nblk <= 0) return cudaSuccess;
+    k_mx_multiply<<<grid_for(nblk, 128), 128, 0, st>>>(
+        reinterpret_cast<const double2*>(v), wcr, wci, ws, rows, m, cpb, f, reinterpret_cast<double2*>(wv),
+        reinterpret_cast<const double2*>(u), reinterpret_cast<float2*>(y0), reinterpret_cast<float2*>(y1), nonfinite);
+    note_launch();
+    return cudaGetLastError();
+}
+
 // |z| exactly as numpy 2.3.5 computes np.abs(complex128) on FMA hosts:
 // larger * sqrt(fma(r, r, 1)), r = smaller / larger (IEEE-rounded ops only).
 __device__ __forceinline__ double np_cabs(double re, double im) {

@@ -137,6 +137,9 @@ cudaError_t launch_rss(const void* x, int is_c128, int64_t groups, int coils, in
 cudaError_t launch_prescale_apply_c128(const void* x, void* y, int64_t seg_points, int64_t nseg,
                                        const int32_t* kvec, cudaStream_t st);
 cudaError_t launch_scale(const void* x, void* y, int64_t n, int dtype, double f, cudaStream_t st);
+cudaError_t launch_mx_multiply(const void* v, const double* wcr, const double* wci, const double* ws, int64_t rows,
+                               int m, int cpb, const FmtDesc& f, void* wv, const void* u, void* y0, void* y1,
+                               int32_t* nonfinite, cudaStream_t st);
 cudaError_t launch_selftest_hwq(const FmtDesc& f, unsigned long long* mism, unsigned* first_bad,
                                 cudaStream_t st);
 

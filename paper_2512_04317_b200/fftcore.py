@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _native, mxblock
 from .errors import InvalidValue, ShapeError, UnsupportedSize
-from .minifloat import MinifloatFormat, get_format, quantize_device
+from .minifloat import MinifloatFormat, get_format
 
 MODE_CODES = {"forward": 0, "inverse": 1, "roundtrip": 2}
 
@@ -413,44 +413,44 @@ def _encode_blocks_batch(vr, vi, cpb: int, fmt: MinifloatFormat):
     return codes[..., 0::2].copy(), codes[..., 1::2].copy(), scales.reshape(b, nb)
 
 
-def _mx_multiply_device(vr, vi, w_enc, fmt: MinifloatFormat, cpb: int):
-    """Blockwise MX complex product w*v (fftcore.py:150-183) composed from device
-    ops: GPU encode, exact products in the reference's product dtype, exact
-    integer renormalization shift, GPU requantization."""
+def _mx_multiply_kernel(vr, vi, w_enc, fmt: MinifloatFormat, cpb: int, u=None):
+    """mxfft_mx_multiply_f64: the blockwise MX complex product w*v of
+    fftcore.py:150-183 (and, given u, the butterfly of fftcore.py:186-235) in
+    one CUDA kernel.  Returns wv complex128 (batch, m) [, y0, y1 complex64]."""
     import torch
 
     vr = np.asarray(vr, dtype=np.float64)
+    vi = np.asarray(vi, dtype=np.float64)
     b, m = vr.shape
-    wcr, wci, ws = w_enc
-    cvr, cvi, sv = _encode_blocks_batch(vr, vi, cpb, fmt)
-    pdt = torch.float32 if 2 * (fmt.emax + 1) <= 126 else torch.float64
-
-    def dev(a):
-        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
-
-    xr, xi = dev(wcr).to(pdt), dev(wci).to(pdt)
-    yr, yi = dev(cvr).to(pdt), dev(cvi).to(pdt)
-    p_r = xr * yr - xi * yi
-    p_i = xr * yi + xi * yr
-    s_out = dev(ws) * dev(sv)
-    amax = torch.maximum(p_r.abs(), p_i.abs()).amax(dim=-1).to(torch.float64)
-    ma, ea = torch.frexp(amax)
-    mm, em = np.frexp(fmt.max_finite)
-    shift = torch.where(amax > fmt.max_finite, ea - int(em) + (ma > float(mm)).to(torch.int32),
-                        torch.zeros_like(ea))
-    one = torch.ones_like(shift, dtype=torch.float64)
-    fac = torch.ldexp(one, -shift).to(pdt)
-    p_r = p_r * fac[..., None]
-    p_i = p_i * fac[..., None]
-    s_out = s_out * torch.ldexp(one, shift)
-    c_r = quantize_device(p_r.to(torch.float64), fmt)
-    c_i = quantize_device(p_i.to(torch.float64), fmt)
-    so = s_out[..., None]
-    return torch.complex(c_r * so, c_i * so).reshape(b, m)
+    wcr, wci, ws = (np.ascontiguousarray(np.asarray(t, dtype=np.float64)) for t in w_enc)
+    nb = m // cpb
+    if wcr.size != nb * cpb or ws.size != nb:
+        raise ShapeError("twiddle blocks do not match the operand length")
+    v = torch.from_numpy(np.ascontiguousarray(vr + 1j * vi)).cuda()
+    dev = [torch.from_numpy(t.reshape(-1)).cuda() for t in (wcr, wci, ws)]
+    wv = torch.empty((b, m), dtype=torch.complex128, device="cuda")
+    nf = torch.zeros(1, dtype=torch.int32, device="cuda")
+    args = [None, None, None]
+    if u is not None:
+        ud = torch.from_numpy(np.ascontiguousarray(np.asarray(u, dtype=np.complex128).reshape(b, m))).cuda()
+        y0 = torch.empty((b, m), dtype=torch.complex64, device="cuda")
+        y1 = torch.empty_like(y0)
+        args = [ud.data_ptr(), y0.data_ptr(), y1.data_ptr()]
+    c = fmt.as_c()
+    _native.check(_native.lib().mxfft_mx_multiply_f64(v.data_ptr(), dev[0].data_ptr(), dev[1].data_ptr(),
+                                                      dev[2].data_ptr(), b, m, cpb, ctypes.byref(c), wv.data_ptr(),
+                                                      *args, nf.data_ptr(), _native.stream_handle()))
+    if int(nf.item()):
+        raise InvalidValue("non-finite block element")
+    if u is not None:
+        return wv.cpu().numpy(), y0.cpu().numpy(), y1.cpu().numpy()
+    return wv.cpu().numpy()
 
 
 def _mx_multiply_batch(vr, vi, w_enc, fmt: MinifloatFormat, cpb: int) -> np.ndarray:
-    return _mx_multiply_device(vr, vi, w_enc, fmt, cpb).cpu().numpy()
+    """Blockwise MX complex multiply w*v for a whole stage (fftcore.py:150-183),
+    on the GPU (mxfft_mx_multiply_f64)."""
+    return _mx_multiply_kernel(vr, vi, w_enc, fmt, cpb)
 
 
 def butterfly_mx(u, v, w, fmt: MinifloatFormat):
@@ -469,9 +469,6 @@ def butterfly_mx(u, v, w, fmt: MinifloatFormat):
         raise ShapeError("butterfly operands must have matching lengths")
     cpb = v.size
     wr, wi = mxblock.mantissas_block(w_blk)
-    w_enc = (wr.reshape(1, 1, cpb), wi.reshape(1, 1, cpb), np.array([[w_blk.scale]]))
-    import torch
-
-    wv = _mx_multiply_device(v.real[None], v.imag[None], w_enc, fmt, cpb)[0].to(torch.complex64)
-    u32 = torch.from_numpy(u).cuda().to(torch.complex64)
-    return (u32 + wv).cpu().numpy(), (u32 - wv).cpu().numpy()
+    w_enc = (wr.reshape(1, cpb), wi.reshape(1, cpb), np.array([w_blk.scale]))
+    _, y0, y1 = _mx_multiply_kernel(v.real[None], v.imag[None], w_enc, fmt, cpb, u=u[None])
+    return y0[0], y1[0]

@@ -426,3 +426,108 @@ def test_fused_fft2_modes_inplace_kgroups(mx, torch, mode):
         y = x.clone()
         mx.fft2_device(y, p, mode, k=kk, k_group=g, out=y)
         assert torch.equal(y, want), ("in place", mode, g)
+
+
+def test_count_range_flush_stress_deterministic(mx, torch):
+    """The global statistics' streaming pass (k_ps_count_range) with a bracket
+    wide enough that every CTA flushes its shared candidate buffer many times
+    (the path of the round-1 shared-memory race): 30 runs give the same
+    counts and the same candidate multiset as numpy.  compute-sanitizer is
+    closed on this GPU pool, so determinism under stress stands in for a
+    racecheck log."""
+    from paper_2512_04317_b200 import distributed as D
+    from tests_cpu_keys import keys_np
+
+    rng = np.random.default_rng(17)
+    n = 1 << 21
+    z = (rng.standard_normal(n) + 1j * rng.standard_normal(n)).astype(np.complex64)
+    z[rng.random(n) < 0.1] = 0
+    k = keys_np(z)
+    k64 = z.real.astype(np.float64) ** 2 + z.imag.astype(np.float64) ** 2
+
+    def clear(t):  # a threshold no key lies within 1e-5 of (so FP32 key rounding cannot matter)
+        t = np.float32(t)
+        while (np.abs(k64 - float(t)) <= 1e-5 * float(t)).any():
+            t = np.float32(t * np.float32(1.0001))
+        return t
+
+    lo, hi = clear(0.05), clear(3.0)
+    top = clear(np.sort(k64[z != 0])[-50] * 1.00002)
+    want_c = np.sort_complex(z[(k >= lo) & (k <= hi) & np.isfinite(k)])
+    want_t = np.sort_complex(z[(k >= top) & np.isfinite(k)])
+    zd = torch.from_numpy(z).cuda()
+    ops = D.CudaOps()
+    first = None
+    for _ in range(30):
+        counts, cand, topv = ops.count_range(zd, float(lo), float(hi), float(top), n, n)
+        got = (counts, np.sort_complex(cand.cpu().numpy()), np.sort_complex(topv.cpu().numpy()))
+        if first is None:
+            first = got
+            nnz = int((z != 0).sum())
+            below = int(((k < lo) & np.isfinite(k)).sum())
+            assert counts[:4] == (nnz, below, len(want_c), len(want_t)) and counts[4] == 0, counts
+            assert np.array_equal(got[1], want_c) and np.array_equal(got[2], want_t)
+        else:
+            assert got[0] == first[0] and np.array_equal(got[1], first[1]) and np.array_equal(got[2], first[2])
+
+
+def test_butterfly_mx_kernel_reference_kats(mx, torch):
+    """butterfly_mx / _mx_multiply_batch run as the mxfft_mx_multiply_f64 kernel;
+    the reference's own known answers (tests/test_fftcore.py:109-162): unit
+    twiddle with u = 0 gives decode(encode(v)), v = 0 gives u, a wide format
+    converges to the exact product, renormalization keeps the bound, and the
+    batched multiply equals the single-block butterfly bit for bit; plus the
+    stage products of the reference capture (tests/golden/stages.npz)."""
+    rng = np.random.default_rng(20240817)
+    E4M3 = mx.E4M3
+    v = rng.standard_normal(4) + 1j * rng.standard_normal(4)
+    y0, y1 = mx.butterfly_mx(np.zeros(4, complex), v, np.ones(4, complex), E4M3)
+    inter = np.empty(8)
+    inter[0::2], inter[1::2] = v.real, v.imag
+    want = mx.decode_block_mx(mx.encode_block_mx(inter, E4M3)).astype(np.complex64)
+    assert np.array_equal(y0, want) and np.array_equal(y1, -y0)
+    u = rng.standard_normal(4) + 1j * rng.standard_normal(4)
+    y0, y1 = mx.butterfly_mx(u, np.zeros(4, complex), np.exp(-2j * np.pi * np.arange(4) / 8), E4M3)
+    assert np.array_equal(y0, u.astype(np.complex64)) and np.array_equal(y1, u.astype(np.complex64))
+    WIDE = mx.MinifloatFormat("wide", 8, 23, "ieee")
+    u = rng.standard_normal(16) + 1j * rng.standard_normal(16)
+    v = rng.standard_normal(16) + 1j * rng.standard_normal(16)
+    w = np.exp(-2j * np.pi * rng.uniform(0, 1, 16))
+    y0, y1 = mx.butterfly_mx(u, v, w, WIDE)
+    rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)
+    assert rel(y0, u + w * v) <= 1e-6 and rel(y1, u - w * v) <= 1e-6
+    m = E4M3.max_finite
+    vv, ww = np.array([m + 0j, m + 0j]), np.array([m + 0j, -m + 0j])
+    y0, y1 = mx.butterfly_mx(np.zeros(2, complex), vv, ww, E4M3)
+    assert np.all(np.isfinite(y0)) and np.all(np.isfinite(y1))
+    exact = ww * vv
+    assert np.all(np.abs(y0 - exact) <= 2.0 ** np.floor(np.log2(np.abs(exact))) * 2.0**-E4M3.mantissa_bits)
+    for _ in range(20):
+        cpb = int(rng.choice([1, 4, 16]))
+        u = rng.standard_normal(cpb) + 1j * rng.standard_normal(cpb)
+        v = rng.standard_normal(cpb) + 1j * rng.standard_normal(cpb)
+        w = np.exp(-2j * np.pi * rng.uniform(0, 1, cpb))
+        w_enc = mx.fftcore._encode_blocks_batch(w.real[None], w.imag[None], cpb, E4M3)
+        wv = mx.fftcore._mx_multiply_batch(v.real[None], v.imag[None], w_enc, E4M3, cpb)[0]
+        y0, y1 = mx.butterfly_mx(u, v, w, E4M3)
+        u32 = u.astype(np.complex64)
+        assert np.array_equal(y0, u32 + wv.astype(np.complex64))
+        assert np.array_equal(y1, u32 - wv.astype(np.complex64))
+    # the reference's per-stage products (stage capture of _fft_batch, golden)
+    g = golden("stages")
+    for ci, case in enumerate(g["cases"]):
+        name, bsz, n = str(case).split(":")
+        bsz, n = int(bsz), int(n)
+        fmt = mx.get_mx_format(name)
+        p = mx.make_plan(n, mx.ModeSpec.mx(fmt, bsz))
+        cpb = min(bsz // 2, n // 2)
+        codes_r, codes_i, scales = p.mx_twiddles[n.bit_length() - 2]  # the last stage: half = n/2
+        outs = g[f"c{ci}_forward_out"]  # (stages, batch, n) reference stage outputs
+        st = n.bit_length() - 1
+        prev = outs[st - 2].astype(np.complex128)  # input of the last stage
+        half = n // 2
+        vv = prev[:, half:]
+        wv = mx.fftcore._mx_multiply_batch(vv.real, vv.imag, (codes_r, codes_i, scales), fmt, cpb)
+        u32 = prev[:, :half].astype(np.complex64)
+        got = np.concatenate([u32 + wv.astype(np.complex64), u32 - wv.astype(np.complex64)], axis=1)
+        assert np.array_equal(got, outs[st - 1]), case
