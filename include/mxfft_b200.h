@@ -117,6 +117,15 @@ int32_t mxfft_fft_rows(mxfft_plan plan, const void* x, void* y, int64_t batch, i
 int32_t mxfft_fft_rows_scaled(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t inverse,
                               int32_t exp_in, int32_t exp_out, uintptr_t stream);
 
+/* mxfft_fft_rows_scaled reading its lines from the receive layout of a
+ * row-slab all-to-all transpose (the distributed 2-D transform,
+ * paper_2512_04317_b200/distributed.py): x is (n / seg_len, lines, seg_len)
+ * complex64 and element q of line c is x[q / seg_len][c][q mod seg_len], so
+ * the next pass needs no permute copy; y is (lines, n), out of place.
+ * seg_len: a power of two dividing n (seg_len == n: plain rows). */
+int32_t mxfft_fft_rows_seg(mxfft_plan plan, const void* x, void* y, int64_t lines, int32_t inverse, int32_t exp_in,
+                           int32_t exp_out, int32_t seg_len, uintptr_t stream);
+
 /* Batched 1-D MX transform along the COLUMNS of `batch` n x n complex64 images
  * (the second pass of fft_2d, fftcore.py:352, without materialising rows.T);
  * x may alias y.  With mxfft_fft_rows this gives either pass of fft_2d alone. */

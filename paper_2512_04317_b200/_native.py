@@ -53,6 +53,7 @@ SIGNATURES = {
     "mxfft_plan_destroy": ([_vp], _i32),
     "mxfft_plan_twiddles": ([_vp, _vp, _vp, _vp], _i32),
     "mxfft_fft_rows": ([_vp, _vp, _vp, _i64, _i32, _u], _i32),
+    "mxfft_fft_rows_seg": ([_vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _u], _i32),
     "mxfft_fft_cols": ([_vp, _vp, _vp, _i64, _i32, _u], _i32),
     "mxfft_fft_rows_scaled": ([_vp, _vp, _vp, _i64, _i32, _i32, _i32, _u], _i32),
     "mxfft_fft2": ([_vp, _vp, _vp, _i64, _i32, _vp, _i32, _vp, _i64, _u], _i32),

@@ -300,6 +300,36 @@ int32_t mxfft_fft_rows_scaled(mxfft_plan plan, const void* x, void* y, int64_t b
     return MXFFT_OK;
 }
 
+int32_t mxfft_fft_rows_seg(mxfft_plan plan, const void* x, void* y, int64_t lines, int32_t inverse, int32_t exp_in,
+                           int32_t exp_out, int32_t seg_len, uintptr_t stream) {
+    CHECK_PLAN(plan);
+    if (lines < 0) return fail(MXFFT_ERR_SHAPE, "negative batch");
+    if (lines == 0) return MXFFT_OK;
+    const int n = plan->p.n;
+    if (seg_len < 2 || (seg_len & (seg_len - 1)) || seg_len > n || n % seg_len)
+        return fail(MXFFT_ERR_SHAPE, "seg_len must be a power of two dividing n");
+    if (x == y) return fail(MXFFT_ERR_VALUE, "segmented rows are out of place");
+    LinePass lp;
+    lp.in = x;
+    lp.out = y;
+    lp.lines_per_image = 1;
+    lp.total_lines = lines;
+    lp.img_elems = n;
+    lp.inverse = inverse ? 1 : 0;
+    lp.kin_const = exp_in;
+    lp.kout_const = exp_out;
+    lp.seg_log2 = ilog2(seg_len);
+    lp.seg_stride = lines * (int64_t)seg_len;
+    if (seg_len < n) {
+        if (!mx_lines_ok(plan->p)) return fail(MXFFT_ERR_VALUE, "segmented rows need a line-kernel plan");
+        CK(run_mx_lines(plan->p, lp, (cudaStream_t)stream), "fft_rows_seg");
+    } else {
+        lp.seg_log2 = 0;  // one segment: plain rows
+        CK(run_lines(plan->p, lp, (cudaStream_t)stream), "fft_rows_seg");
+    }
+    return MXFFT_OK;
+}
+
 int32_t mxfft_fft_cols(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t inverse,
                        uintptr_t stream) {
     CHECK_PLAN(plan);

@@ -41,6 +41,8 @@ struct LinePass {
     int kin_sign = 0, kout_sign = 0, kout_const = 0, kin_const = 0;
     int stage_limit = -1;
     int reverse = 0;  // walk the groups last to first (the previous pass's latest output is still in L2)
+    int seg_log2 = 0;  // rows mode, > 0: element q of line c is in[(q >> seg_log2) * seg_stride + c * 2^seg_log2 + (q & mask)]
+    int64_t seg_stride = 0;
     int32_t* d_vexp = nullptr;
     float* d_vcodes = nullptr;
     int32_t* d_pexp = nullptr;
@@ -62,6 +64,8 @@ struct MxLinesArgs {
     int k_group, kin_sign, kout_sign, kout_const, kin_const, stage_limit;
     int lpi_shift;  // log2(lines_per_image) when it is a power of two, else -1
     int reverse;    // group order last to first
+    int seg_log2;   // segmented input (the all-to-all receive layout), 0 = off
+    int64_t seg_stride;
     int prof_flags;  // profiling only: bit 0 skip tile loads, bit 1 skip stores
     int tw_chunks;
     // exact replay (replay_lines): reference-literal tables of the plan

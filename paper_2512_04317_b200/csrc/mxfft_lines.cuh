@@ -563,6 +563,14 @@ __device__ __forceinline__ Run mkrun(unsigned rb, int e) {
 }
 __device__ __forceinline__ unsigned radr(const Run& r, int k) { return r.a0 | (r.f ^ (unsigned)(k << 4)); }
 
+// segmented rows input (seg_log2 > 0): the all-to-all receive layout of a
+// row-slab transpose, (G, lines, R) with R = 2^seg_log2 -- element q of line c
+// lives in segment q / R at offset c R + q mod R
+__device__ __forceinline__ int64_t seg_off(const MxLinesArgs& a, int64_t line, int q) {
+    const int R = 1 << a.seg_log2;
+    return (int64_t)(q >> a.seg_log2) * a.seg_stride + line * R + (q & (R - 1));
+}
+
 // prescale-exponent entry of a line: kvec[(line / lines_per_image) / k_group]
 // (a shift and no division in the common power-of-two / one-image-per-k case)
 __device__ __forceinline__ int64_t k_index(const MxLinesArgs& a, int64_t line) {
@@ -869,13 +877,14 @@ static __device__ __noinline__ void replay_lines(const MxLinesArgs& a, int64_t g
             base = gl * n;
             es = 1;
         }
+        const bool seg = !a.col_mode && a.seg_log2;
         const int64_t img = gl / a.lines_per_image;
         const int kk = a.kvec ? a.kvec[img / a.k_group] : 0;
         const int kin = a.kin_sign * kk + a.kin_const, kout = a.kout_sign * kk + a.kout_const;
         __syncthreads();
         for (int i = tid; i < n; i += nthr) {
             const int r = (int)(__brev((unsigned)i) >> (32 - a.log2n));
-            *acc(i) = gscale(a.in[base + (int64_t)r * es], kin);
+            *acc(i) = gscale(a.in[seg ? seg_off(a, gl, r) : base + (int64_t)r * es], kin);
         }
         __syncthreads();
         const int last = a.stage_limit < a.log2n ? a.stage_limit : a.log2n;
@@ -975,7 +984,17 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
     auto issue_tile = [&](int64_t grp_, unsigned buf) {
         if (a.prof_flags & 1) return;
         const int64_t grp = a.reverse ? ngroups - 1 - grp_ : grp_;
-        if (!col_in) {
+        if (LT < 0 && a.seg_log2) {  // segmented rows (run-time-n variant only): per-chunk addresses
+            const int64_t l0 = grp * LPC;
+#pragma unroll 4
+            for (int k = 0; k < 16; ++k) {
+                const int e = 2 * (tid + NT * k);
+                const int64_t line = l0 + (e >> (lt + 5));
+                const bool ok = line < a.total_lines;
+                cp_async16(caddr(buf, rch ^ dsw(NT * k), 0),
+                           ok ? (const void*)(a.in + seg_off(a, line, e & (N - 1))) : (const void*)a.in, ok);
+            }
+        } else if (!col_in) {
             const int64_t base = grp * LPC * (int64_t)N;
             const float4* src = reinterpret_cast<const float4*>(a.in + base) + tid;
             const int64_t lim = (a.total_lines * (int64_t)N - base) / 2;  // chunks left
@@ -1175,7 +1194,11 @@ __device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
         if (DBG) dbg.row = line;
         float2 x[32];
         bool bad = false;
-        {
+        if (a.seg_log2 && !a.col_mode) {  // segmented rows: element m T + rcol of the line
+#pragma unroll
+            for (int m = 0; m < 32; ++m) x[rev_c<5>(m)] = __ldg(a.in + seg_off(a, line, m * T + rcol));
+            if (kin) scale32<DBG>(x, kin, bad);
+        } else {
             const float2* src = a.in + base + (int64_t)rcol * es;
             const int64_t stride = (int64_t)T * es;
 #pragma unroll
@@ -1185,7 +1208,11 @@ __device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
 #if MXFFT_BIG_PREFETCH
         // while this line computes, its successor (a contiguous row) streams into
         // L2, so the next load phase hits L2 instead of waiting on HBM
-        if (!a.col_mode && tid < 4 && grp + gridDim.x < ngroups) {
+        if (!a.col_mode && a.seg_log2 && grp + gridDim.x < ngroups && tid < (N >> a.seg_log2)) {
+            // the next line's segments, one per thread
+            const char* nx = reinterpret_cast<const char*>(a.in + seg_off(a, grp + gridDim.x, tid << a.seg_log2));
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx), "r"(8u << a.seg_log2) : "memory");
+        } else if (!a.col_mode && !a.seg_log2 && tid < 4 && grp + gridDim.x < ngroups) {
             const char* nx = reinterpret_cast<const char*>(a.in + (grp + gridDim.x) * (int64_t)N);
             const unsigned part = (unsigned)N * 2u;  // bytes per prefetching thread (N * 8 / 4)
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx + (size_t)tid * part), "r"(part)
@@ -1516,7 +1543,7 @@ static cudaError_t disp_lt(const MxLinesArgs& a, size_t smem, cudaStream_t st) {
         return cudaErrorInvalidValue;
     }
     if constexpr (!DBG && CPB >= 8) {
-        if (a.col_mode || a.stage_limit < a.log2n) return launch_t<ID, CPB, DBG, -1, false>(a, smem, st);
+        if (a.col_mode || a.seg_log2 || a.stage_limit < a.log2n) return launch_t<ID, CPB, DBG, -1, false>(a, smem, st);
         switch (a.log2T) {
             case 0: return launch_t<ID, CPB, DBG, 0, false>(a, smem, st);
             case 1: return launch_t<ID, CPB, DBG, 1, false>(a, smem, st);

@@ -104,6 +104,18 @@ class CudaOps:
                                                           int(exp_out), _native.stream_handle()))
         return y
 
+    def rows_seg(self, recv, plan, inverse: bool, exp_in: int = 0, exp_out: int = 0):
+        """Row pass reading its lines straight from an all-to-all receive buffer
+        (G, R, R): line c = recv[0][c] | recv[1][c] | ... (mxfft_fft_rows_seg) --
+        no permute copy between the exchange and the pass."""
+        import torch
+
+        G, R, _ = recv.shape
+        y = torch.empty((R, G * R), dtype=recv.dtype, device=recv.device)
+        _native.check(_native.lib().mxfft_fft_rows_seg(plan.handle, recv.data_ptr(), y.data_ptr(), R, int(inverse),
+                                                       int(exp_in), int(exp_out), R, _native.stream_handle()))
+        return y
+
     def sample_keys(self, x, nsamples: int):
         import torch
 
@@ -250,18 +262,27 @@ def compute_prescale_global(x_local, cfg: PrescaleConfig, comm: Comm = None, ops
     return PrescaleResult(k=k, a_max=a_max, p_tau=p_tau, k1=k1, k2=k2)
 
 
-def _transpose_slabs(a, comm: Comm, ops):
-    """(R, N) = this rank's rows of A  ->  (R, N) = this rank's rows of A^T
-    (one all-to-all of R x R blocks).  The sender transposes
-    each block on the way into the send buffer; the receiver only interleaves
-    contiguous runs of R."""
+def _exchange(a, comm: Comm, ops):
+    """(R, N) = this rank's rows of A  ->  the receive buffer (G, R, R) of one
+    all-to-all of R x R blocks: recv[i][c][r] =
+    A[i R + r][me R + c], i.e. row c of this rank's rows of A^T is the
+    concatenation recv[0][c] | recv[1][c] | ...  The sender transposes each
+    block on the way into the send buffer (one kernel); the next row pass
+    reads the receive layout directly (CudaOps.rows_seg)."""
     import torch
 
     G = comm.world
-    R, N = a.shape
     send = ops.block_transpose(a, G)  # [j][c][r] = A[me*R + r][j*R + c]
     recv = torch.empty_like(send)
-    comm.all_to_all(recv, send)  # recv[i][c][r] = A[i*R + r][me*R + c]
+    comm.all_to_all(recv, send)
+    return recv
+
+
+def _transpose_slabs(a, comm: Comm, ops):
+    """(R, N) = this rank's rows of A  ->  (R, N) = this rank's rows of A^T,
+    materialised (only for a restored output layout)."""
+    R, N = a.shape
+    recv = _exchange(a, comm, ops)
     return recv.permute(1, 0, 2).reshape(R, N).contiguous()  # [c][i*R + r] = A^T[me*R + c][i*R + r]
 
 
@@ -287,9 +308,15 @@ def fft2_slab(x_slab, plan, mode: str = "forward", comm: Comm = None, ops=None, 
     y = x_slab.contiguous()
     for i, inv in enumerate(dirs):
         first, last = i == 0, i == len(dirs) - 1
-        if i > 0:  # every later pass works on the rows of the previous result's transpose
-            y = _transpose_slabs(y, comm, ops)
-        y = ops.rows(y, plan, inv, exp_in=k if first else 0, exp_out=out_exp if last else 0)
+        e_in, e_out = (k if first else 0), (out_exp if last else 0)
+        if i == 0:
+            y = ops.rows(y, plan, inv, exp_in=e_in, exp_out=e_out)
+        elif hasattr(ops, "rows_seg"):
+            # every later pass works on the rows of the previous result's
+            # transpose, read straight from the all-to-all receive buffer
+            y = ops.rows_seg(_exchange(y, comm, ops), plan, inv, exp_in=e_in, exp_out=e_out)
+        else:
+            y = ops.rows(_transpose_slabs(y, comm, ops), plan, inv, exp_in=e_in, exp_out=e_out)
     return _transpose_slabs(y, comm, ops) if restore else y
 
 

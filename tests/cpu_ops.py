@@ -38,6 +38,10 @@ class OracleOps:
         y = O.fft_batch(a, plan.oplan, inverse).astype(np.complex128) * 2.0**exp_out
         return torch.from_numpy(y.astype(np.complex64))
 
+    def rows_seg(self, recv, plan, inverse, exp_in=0, exp_out=0):
+        G, R, _ = recv.shape
+        return self.rows(recv.permute(1, 0, 2).reshape(R, G * R).contiguous(), plan, inverse, exp_in, exp_out)
+
     def sample_keys(self, x, nsamples):
         z = x.numpy()
         nsec = z.size // 4

@@ -531,3 +531,61 @@ def test_butterfly_mx_kernel_reference_kats(mx, torch):
         u32 = prev[:, :half].astype(np.complex64)
         got = np.concatenate([u32 + wv.astype(np.complex64), u32 - wv.astype(np.complex64)], axis=1)
         assert np.array_equal(got, outs[st - 1]), case
+
+
+@pytest.mark.parametrize("n,R", [(1024, 128), (1024, 512), (16384, 2048), (16384, 8192)])
+def test_rows_seg_reads_alltoall_layout(mx, torch, n, R):
+    """mxfft_fft_rows_seg on an all-to-all receive buffer (G, R, R) equals the
+    row pass on the permuted (materialised) rows, bit for bit, with the fused
+    power-of-two scalings."""
+    from paper_2512_04317_b200 import distributed as D
+
+    G = n // R
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n + R)
+    recv = torch.complex(torch.randn((G, R, R), generator=g, device="cuda"),
+                         torch.randn((G, R, R), generator=g, device="cuda")) * 2.0**-3
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.E4M3, 32))
+    ops = D.CudaOps()
+    for inv, ei, eo in ((False, 0, 0), (True, 3, -5)):
+        got = ops.rows_seg(recv, p, inv, exp_in=ei, exp_out=eo)
+        want = ops.rows(recv.permute(1, 0, 2).reshape(R, n).contiguous(), p, inv, exp_in=ei, exp_out=eo)
+        assert torch.equal(got, want), (n, R, inv)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_slab_restore_false_is_transposed_result(mx, torch, G):
+    """fft2_slab(restore=False) -- three all-to-alls per round trip, passes read
+    the receive buffers directly -- leaves rank r with rows r R .. of the
+    transposed result (the column slabs of A)."""
+    from paper_2512_04317_b200 import distributed as D
+    from paper_2512_04317_b200.workloads import ellipse_kspace
+
+    n = 512
+    x = ellipse_kspace(n, 31, noise=0.01)
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.E4M3, 32))
+    want = mx.fft2_device(torch.from_numpy(x[None].copy()).cuda(), p, "roundtrip", k=None)[0].cpu().numpy()
+    shared = {"world": G, "bar": threading.Barrier(G), "box": [None] * G}
+    out = [None] * G
+    errs = []
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                r0, r1 = D.shard_range(n, r, G)
+                xs = torch.from_numpy(x[r0:r1].copy()).cuda()
+                y = D.fft2_slab(xs, p, "roundtrip", comm=ThreadComm(shared, r), restore=False)
+                torch.cuda.current_stream().synchronize()
+                out[r] = y.cpu().numpy()
+        except BaseException as e:
+            errs.append(e)
+            shared["bar"].abort()
+
+    ts = [threading.Thread(target=rank_main, args=(r,)) for r in range(G)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs[0]
+    assert np.array_equal(np.concatenate(out), want.T)
