@@ -239,6 +239,12 @@ int32_t mxfft_pipeline_fused_supported(mxfft_plan plan);
  * same one-image-per-CTA kernel, given the per-image k, instead of four line
  * passes; results are identical. */
 void mxfft_fused_image(int32_t on);
+/* Scheduling knob: with on != 0 (the default) mxfft_fft2 runs n >= 16384
+ * passes as stages 0 .. L-2 on the decimated half rows (the n/2-point line
+ * kernel) followed by the last stage fused into the transposed store, when
+ * the workspace holds two image copies (mxfft_fft2_workspace_bytes);
+ * results are identical. */
+void mxfft_split_last_stage(int32_t on);
 int32_t mxfft_pipeline_fused(mxfft_plan plan, const void* x, void* y, int64_t nimg, int32_t roundtrip,
                              const mxfft_prescale_cfg* cfg, mxfft_prescale_result* d_res, int32_t* d_k,
                              uintptr_t stream);

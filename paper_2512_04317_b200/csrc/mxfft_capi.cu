@@ -232,6 +232,36 @@ int32_t mxfft_plan_create(mxfft_plan* plan, int32_t n, const mxfft_format* fmt,
         return cuda_fail(e, "plan_create");
     }
     cudaFree(d_tw);
+    if (mx_lines_ok(p) && last_stage_ok(p)) {
+        // the n/2-point plan of the first L-1 stages (split row passes of
+        // mxfft_fft2): kernel tables are the prefix of this plan's; the
+        // reference-layout rows (exact replays) are copied
+        Plan* hp = new Plan;
+        *hp = p;
+        hp->half = nullptr;
+        hp->n = n / 2;
+        hp->log2n = p.log2n - 1;
+        const int hm = n / 4, hnb = hm / p.cpb;
+        hp->d_wcr = hp->d_wci = nullptr;
+        hp->d_wsexp = nullptr;
+        if ((e = cudaMalloc(&hp->d_wcr, sizeof(double) * hp->log2n * hm)) != cudaSuccess ||
+            (e = cudaMalloc(&hp->d_wci, sizeof(double) * hp->log2n * hm)) != cudaSuccess ||
+            (e = cudaMalloc(&hp->d_wsexp, sizeof(int) * hp->log2n * hnb)) != cudaSuccess ||
+            (e = cudaMemcpy2D(hp->d_wcr, sizeof(double) * hm, p.d_wcr, sizeof(double) * m, sizeof(double) * hm,
+                              hp->log2n, cudaMemcpyDeviceToDevice)) != cudaSuccess ||
+            (e = cudaMemcpy2D(hp->d_wci, sizeof(double) * hm, p.d_wci, sizeof(double) * m, sizeof(double) * hm,
+                              hp->log2n, cudaMemcpyDeviceToDevice)) != cudaSuccess ||
+            (e = cudaMemcpy2D(hp->d_wsexp, sizeof(int) * hnb, p.d_wsexp, sizeof(int) * nb, sizeof(int) * hnb,
+                              hp->log2n, cudaMemcpyDeviceToDevice)) != cudaSuccess) {
+            cudaFree(hp->d_wcr);
+            cudaFree(hp->d_wci);
+            cudaFree(hp->d_wsexp);
+            delete hp;
+            mxfft_plan_destroy(h);
+            return cuda_fail(e, "plan_create (half plan)");
+        }
+        p.half = hp;
+    }
     *plan = h;
     return MXFFT_OK;
 }
@@ -239,6 +269,13 @@ int32_t mxfft_plan_create(mxfft_plan* plan, int32_t n, const mxfft_format* fmt,
 int32_t mxfft_plan_destroy(mxfft_plan plan) {
     if (!plan) return MXFFT_OK;
     Plan& p = plan->p;
+    if (p.half) {  // (its kernel tables alias this plan's)
+        cudaFree(p.half->d_wcr);
+        cudaFree(p.half->d_wci);
+        cudaFree(p.half->d_wsexp);
+        delete p.half;
+        p.half = nullptr;
+    }
     cudaFree(p.d_wcr);
     cudaFree(p.d_wci);
     cudaFree(p.d_wsexp);
@@ -350,8 +387,12 @@ int32_t mxfft_fft_cols(mxfft_plan plan, const void* x, void* y, int64_t batch, i
 
 int64_t mxfft_fft2_workspace_bytes(mxfft_plan plan, int64_t batch) {
     if (!plan || batch <= 0 || !mx_lines_ok(plan->p)) return 0;
-    return batch * (int64_t)plan->p.n * plan->p.n * 8;
+    // split row passes (n >= 16384) stage the half-row outputs in a second image buffer
+    const int64_t copies = plan->p.half ? 2 : 1;
+    return copies * batch * (int64_t)plan->p.n * plan->p.n * 8;
 }
+
+void mxfft_split_last_stage(int32_t on) { mxfft::g_split_last_stage = on ? 1 : 0; }
 
 int32_t mxfft_fft2(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t mode,
                    const int32_t* d_k, int32_t k_group, void* workspace, int64_t workspace_bytes,
@@ -373,6 +414,40 @@ int32_t mxfft_fft2(mxfft_plan plan, const void* x, void* y, int64_t batch, int32
     }
     const int64_t nn = (int64_t)p.n * p.n;
     const int npass = mode == 2 ? 4 : 2;
+    if (p.half && g_split_last_stage && workspace && workspace_bytes >= 2 * batch * nn * 8) {
+        // n >= 16384: every pass = stages 0 .. L-2 on the decimated half rows
+        // (the n/2-point line kernel, two CTAs per SM) + the last stage fused
+        // into the transposed store.  x -> W2 -> W1 [-> W2 -> W1 -> W2 -> W1] -> W2 -> y
+        float2* w1 = reinterpret_cast<float2*>(workspace);
+        float2* w2 = w1 + batch * nn;
+        for (int pass = 0; pass < npass; ++pass) {
+            const bool inv = mode == 1 || (mode == 2 && pass >= 2);
+            const bool last = pass == npass - 1;
+            LinePass lp;
+            lp.in = pass == 0 ? x : (const void*)w1;
+            lp.out = w2;
+            lp.dec = 1;
+            lp.lines_per_image = 2 * p.n;
+            lp.total_lines = batch * 2 * (int64_t)p.n;
+            lp.img_elems = nn;
+            lp.inverse = inv;
+            lp.kvec = d_k;
+            lp.k_group = k_group > 0 ? k_group : 1;
+            if (pass == 0 && d_k) lp.kin_sign = 1;
+            CK(run_mx_lines(*p.half, lp, s), "fft2 (half rows)");
+            LastStagePass ls;
+            ls.in = w2;
+            ls.out = last ? y : (void*)w1;
+            ls.batch = batch;
+            ls.inverse = inv;
+            ls.kvec = d_k;
+            ls.k_group = k_group > 0 ? k_group : 1;
+            ls.kout_sign = last && d_k ? -1 : 0;
+            ls.kout_const = last && mode == 2 ? -2 * p.log2n : 0;
+            CK(run_last_stage_transpose(p, ls, s), "fft2 (last stage + transpose)");
+        }
+        return MXFFT_OK;
+    }
     // With a workspace every pass is a row pass that stores its lines transposed
     // (rows.T of fft_2d, fftcore.py:351-353): x -> ws -> y [-> ws -> y].  Both
     // reads and writes then move whole 128-byte lines.  Without one, the

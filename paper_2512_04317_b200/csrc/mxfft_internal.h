@@ -23,7 +23,27 @@ struct Plan {
     signed char* d_twe8 = nullptr;   // log2 scale of the block holding butterfly j
     int trivial01 = 0;  // stage 0/1 twiddles are exactly 1 and -i at scale 2^-emax
     int device = 0;     // the tables live on this device; transforms must run there
+    // n >= 16384: the plan of the first log2(n) - 1 stages on n/2-point halves
+    // (kernel tables alias this plan's; reference-layout rows copied), used by
+    // mxfft_fft2's split passes (decimated half rows + last stage fused into
+    // the transpose, mxfft_laststage.cu)
+    Plan* half = nullptr;
 };
+
+// the last butterfly stage of an n-point row pass fused into the tiled
+// transpose that follows it (mxfft_laststage.cu): in = rows after stage L-2,
+// out = transposed rows after stage L-1 [x 2^kout]
+struct LastStagePass {
+    const void* in;
+    void* out;
+    int64_t batch;
+    int inverse;
+    const int32_t* kvec;
+    int k_group, kout_sign, kout_const;
+};
+bool last_stage_ok(const Plan& p);
+cudaError_t run_last_stage_transpose(const Plan& p, const LastStagePass& lp, cudaStream_t st);
+extern int g_split_last_stage;
 
 // One pass of 1-D transforms over a set of lines.
 struct LinePass {
@@ -43,6 +63,7 @@ struct LinePass {
     int reverse = 0;  // walk the groups last to first (the previous pass's latest output is still in L2)
     int seg_log2 = 0;  // rows mode, > 0: element q of line c is in[(q >> seg_log2) * seg_stride + c * 2^seg_log2 + (q & mask)]
     int64_t seg_stride = 0;
+    int dec = 0;  // rows mode: line L is half (L & 1) of row L >> 1 of length 2n, decimated (x[2q + h])
     int32_t* d_vexp = nullptr;
     float* d_vcodes = nullptr;
     int32_t* d_pexp = nullptr;
@@ -66,6 +87,7 @@ struct MxLinesArgs {
     int reverse;    // group order last to first
     int seg_log2;   // segmented input (the all-to-all receive layout), 0 = off
     int64_t seg_stride;
+    int dec;        // decimated halves of rows twice as long (the first L-1 stages of an L-stage row)
     int prof_flags;  // profiling only: bit 0 skip tile loads, bit 1 skip stores
     int tw_chunks;
     // exact replay (replay_lines): reference-literal tables of the plan

@@ -72,6 +72,7 @@ cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
     a.reverse = lp.reverse && MXFFT_REVERSE_PASSES;
     a.seg_log2 = lp.seg_log2;
     a.seg_stride = lp.seg_stride;
+    a.dec = lp.dec;
     a.lpi_shift = -1;
     if (a.lines_per_image > 0 && (a.lines_per_image & (a.lines_per_image - 1)) == 0)
         for (a.lpi_shift = 0; (1 << a.lpi_shift) < a.lines_per_image; ++a.lpi_shift) {

@@ -312,15 +312,17 @@ __device__ __forceinline__ int flog2_hot(float am) {
     return (int)(__float_as_uint(am) >> 23) - 127;  // am >= 0
 }
 
-template <int ID, int NB, int G, bool DBG>
+// SLOW: an out-of-range block takes the exact FP64-assisted path inline (as
+// the debug kernels do) instead of flagging a replay of the whole group
+template <int ID, int NB, int G, bool DBG, bool SLOW = DBG>
 __device__ __forceinline__ void mxb(float2 (&u)[NB], float2 (&v)[NB], const unsigned (&w)[NB],
                                     int ew, const LDbg* d, int bfly0, bool& bad) {
     using F = HwFmt<ID>;
     using Rg = DecodeRange<F>;
     constexpr bool PAIR = G == 2;
-    static_assert(!(DBG && G > 2), "debug kernels split a block over at most a lane pair");
+    static_assert(!((DBG || SLOW) && G > 2), "the inline exact path splits a block over at most a lane pair");
     const float am = grp_max<G>(amax_c<NB>(v));
-    const int ev = am > 0.f ? flog2_hot<DBG>(am) - F::EMAX : 0;
+    const int ev = am > 0.f ? flog2_hot<DBG || SLOW>(am) - F::EMAX : 0;
     const float inv = exp2i(-ev);
     unsigned cv[NB];
     float pr[NB], pi[NB];
@@ -339,7 +341,7 @@ __device__ __forceinline__ void mxb(float2 (&u)[NB], float2 (&v)[NB], const unsi
                        : max(0, (int)((__float_as_uint(ap) + (0x7fffffu - F::MM)) >> 23) - 127 - F::EM);
     const int E = ew + ev + sh;
     const bool fast = ((unsigned)(ev + 127) <= 253u) & ((unsigned)(E - Rg::ELO) <= (unsigned)(Rg::EHI - Rg::ELO));
-    if constexpr (!DBG) {
+    if constexpr (!DBG && !SLOW) {
         bad |= !fast;  // the group is replayed exactly (replay_lines); keep going
     } else if (__builtin_expect(!fast, 0)) {
         float2 tu[NB], tv[NB];
@@ -878,6 +880,10 @@ static __device__ __noinline__ void replay_lines(const MxLinesArgs& a, int64_t g
             es = 1;
         }
         const bool seg = !a.col_mode && a.seg_log2;
+        if (!a.col_mode && a.dec) {
+            base = (gl >> 1) * (2 * (int64_t)n) + (gl & 1);
+            es = 2;
+        }
         const int64_t img = gl / a.lines_per_image;
         const int kk = a.kvec ? a.kvec[img / a.k_group] : 0;
         const int kin = a.kin_sign * kk + a.kin_const, kout = a.kout_sign * kk + a.kout_const;
@@ -1177,6 +1183,9 @@ __device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
         if (a.col_mode) {
             base = img * (int64_t)N * N + (line - img * N);
             es = N;
+        } else if (a.dec) {  // half (line & 1) of row line >> 1, decimated: x[2q + h]
+            base = (line >> 1) * (2 * (int64_t)N) + (line & 1);
+            es = 2;
         } else {
             base = line * N;
             es = 1;
@@ -1184,6 +1193,9 @@ __device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
         if (a.tstore) {
             obase = img * (int64_t)N * N + (line - img * N);
             oes = N;
+        } else if (a.dec) {  // the halves' outputs are plain rows of N (half h of a 2N-row at h N)
+            obase = line * N;
+            oes = 1;
         } else {
             obase = base;
             oes = es;
@@ -1212,9 +1224,11 @@ __device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
             // the next line's segments, one per thread
             const char* nx = reinterpret_cast<const char*>(a.in + seg_off(a, grp + gridDim.x, tid << a.seg_log2));
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx), "r"(8u << a.seg_log2) : "memory");
-        } else if (!a.col_mode && !a.seg_log2 && tid < 4 && grp + gridDim.x < ngroups) {
-            const char* nx = reinterpret_cast<const char*>(a.in + (grp + gridDim.x) * (int64_t)N);
-            const unsigned part = (unsigned)N * 2u;  // bytes per prefetching thread (N * 8 / 4)
+        } else if (!a.col_mode && !a.seg_log2 && tid < 4 && grp + gridDim.x < ngroups && (!a.dec || !(grp & 1))) {
+            // (decimated halves: the even line of a pair prefetches the whole row)
+            const int64_t nl = grp + gridDim.x;
+            const char* nx = reinterpret_cast<const char*>(a.in + (a.dec ? (nl >> 1) * 2 * (int64_t)N : nl * (int64_t)N));
+            const unsigned part = (unsigned)N * (a.dec ? 4u : 2u);  // bytes per prefetching thread
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx + (size_t)tid * part), "r"(part)
                          : "memory");
         }

@@ -589,3 +589,34 @@ def test_slab_restore_false_is_transposed_result(mx, torch, G):
         t.join()
     assert not errs, errs[0]
     assert np.array_equal(np.concatenate(out), want.T)
+
+
+@pytest.mark.parametrize("fmt,bsz", [("e4m3", 32), ("e5m2", 16)])
+def test_split_last_stage_fft2_16384(mx, torch, fmt, bsz):
+    """n = 16384 passes as stages 0-12 on the decimated half rows (the
+    8192-point line kernel) + the last stage fused into the transposed store
+    equal the 14-stage row kernel + tiled transpose, bit for bit, for every
+    mode with k; rows scaled to extreme magnitudes exercise the exact replay
+    of the half rows and the inline exact path of the fused last stage."""
+    from paper_2512_04317_b200 import _native
+    from paper_2512_04317_b200.workloads import ellipse_kspace_device
+
+    n = 16384
+    x = ellipse_kspace_device(n, 9, noise=0.01) * (2.0**-12)
+    x[:3] *= 2.0**-110   # tiny rows: out of the fast range (subnormal block maxima)
+    x[5] *= 2.0**40      # large row (intermediates stay finite: the reference raises on non-finite ones)
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.get_mx_format(fmt), bsz))
+    L = _native.lib()
+    k = torch.tensor([-3], dtype=torch.int32, device="cuda")
+    for mode in ("forward", "inverse", "roundtrip"):
+        L.mxfft_split_last_stage(0)
+        try:
+            want = mx.fft2_device(x[None], p, mode, k=k)
+            torch.cuda.synchronize()
+        finally:
+            L.mxfft_split_last_stage(1)
+        got = mx.fft2_device(x[None], p, mode, k=k)
+        same = (got == want) | (torch.isnan(got) & torch.isnan(want))
+        assert bool(same.all()), (mode, int((~same).sum()))
+        del got, want
+        torch.cuda.empty_cache()
