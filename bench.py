@@ -455,7 +455,7 @@ def measure_batch(ctx, name, c, steps, warmup, graph=True, e2e=False, cpu_second
     if e2e:
         h_in = torch.from_numpy(x_host).pin_memory()
         h_out = torch.empty(h_in.shape, dtype=h_in.dtype).pin_memory()
-        ms_e2e = ctx.timed(lambda: mx.pipeline_host(h_in, plan, cfg, True, out_host=h_out, chunks=8),
+        ms_e2e = ctx.timed(lambda: mx.pipeline_host(h_in, plan, cfg, True, out_host=h_out, chunks=12),
                            max(5, steps // 5), 2)
         rec["e2e"] = {"value": world * pts / (ms_e2e * 1e-3) / 1e9, "unit": "Gpoints/s",
                       "h2d_bytes_per_step": world * pts * 8, "d2h_bytes_per_step": world * pts * 8,
