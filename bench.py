@@ -387,7 +387,13 @@ def measure_batch(ctx, name, c, steps, warmup, graph=True, e2e=False, cpu_second
             L.mxfft_fused_image(kn)
             g_rt, _ = graphed(lambda f=f: step(True, f))
             t[vname] = ctx.timed(g_rt, steps, warmup, flush)
+        # the fastest variant, except that the line-pass variant (whose kernel's
+        # HBM roofline is the per-pass one the other configurations report)
+        # wins ties within 2 %: the fused transform is compute-bound and moves
+        # 16 B per point per round trip, so its HBM fraction says nothing
         best = min(t, key=t.get)
+        if t["stats_then_line_passes"] <= 1.02 * t[best]:
+            best = "stats_then_line_passes"
         fused, knob = variants[best]
         alt = {"ms_per_step": t, "chosen": best,
                "value": {v: world * pts / (ms_ * 1e-3) / 1e9 for v, ms_ in t.items()}}

@@ -35,6 +35,10 @@
 
 namespace mxfft {
 
+#ifndef MXFFT_IM_PF
+#define MXFFT_IM_PF 0  // L2 prefetch of coming images: 0 none (measured fastest: 247 vs 259 us per pass with 2), 1 / 2 the next / after-next at the top of an image, 3 the next one pass before its load
+#endif
+
 constexpr int IM_N = 128, IM_LT = 2, IM_T = 4, IM_NT = 512, IM_EL = IM_N * IM_N;
 constexpr int IM_S = 1024;    // sample points of the bracket
 constexpr int IM_K = 8;       // rows of the per-thread candidate lists (+ IM_U2 sink rows)
@@ -797,7 +801,9 @@ __global__ void __launch_bounds__(IM_NT, 1) k_mx_image(ImageArgs a) {
 #endif
     int64_t img = blockIdx.x;
     if (img < a.nimg) {
+#if MXFFT_IM_PF == 2
         im_prefetch_l2(a, img + gridDim.x);
+#endif
         im_load_tile<ID, CPB>(a, img, tile_sh);
     }
     for (; img < a.nimg; img += gridDim.x) {
@@ -808,7 +814,11 @@ __global__ void __launch_bounds__(IM_NT, 1) k_mx_image(ImageArgs a) {
         cp_wait<0>();
         __syncthreads();  // the tile has landed (and the twiddles are in place)
         IM_T(0)
+#if MXFFT_IM_PF == 2
         im_prefetch_l2(a, img + 2 * (int64_t)gridDim.x);
+#elif MXFFT_IM_PF == 1
+        im_prefetch_l2(a, img + gridDim.x);
+#endif
         int k = 0;
         if (!a.stats) {
             k = a.kin ? __ldg(a.kin + img / a.k_group) : 0;
@@ -848,6 +858,9 @@ __global__ void __launch_bounds__(IM_NT, 1) k_mx_image(ImageArgs a) {
             for (int m = 0; m < 32; ++m)
                 x[rev_c<5>(m)] = lds64(tile_sh + (g_col ^ (16u * (unsigned)dsw((m * IM_T * IM_N) >> 1))));
             __syncthreads();  // all gathered: the rows may be overwritten by the exchanges
+#if MXFFT_IM_PF == 3
+            if (pass == a.npass - 1) im_prefetch_l2(a, img + gridDim.x);  // the next image, a pass ahead of its load
+#endif
             if (pass == 2) {  // the inverse transform (fftcore.py:267-268: conjugated twiddles)
                 L.tw = twi;
                 L.tw_sh = (unsigned)__cvta_generic_to_shared(twi);

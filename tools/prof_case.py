@@ -27,6 +27,8 @@ if n >= 8192:  # the host generator would take minutes at this size
 else:
     x = torch.from_numpy(ellipse_kspace_batch(batch, n, seed=0)).cuda() * (2.0 ** -14)
 plan = mx.make_plan(n, mx.ModeSpec.mx(fmt, block))
+if os.environ.get("MXFFT_FUSED_IMAGE") == "0":  # n = 128: profile the line passes instead of the fused kernel
+    mx._native.lib().mxfft_fused_image(0)
 y = torch.empty_like(x)
 cfg = mx.PrescaleConfig()
 for _ in range(reps):
