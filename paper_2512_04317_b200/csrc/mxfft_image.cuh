@@ -800,6 +800,9 @@ __global__ void __launch_bounds__(IM_NT, 1) k_mx_image(ImageArgs a) {
 #define IM_T(i)
 #endif
     int64_t img = blockIdx.x;
+    // the given k of this CTA's next image, loaded an image ahead (its latency
+    // then never sits at the top of an image)
+    int k_next = (!a.stats && a.kin && img < a.nimg) ? __ldg(a.kin + img / a.k_group) : 0;
     if (img < a.nimg) {
 #if MXFFT_IM_PF == 2
         im_prefetch_l2(a, img + gridDim.x);
@@ -821,7 +824,9 @@ __global__ void __launch_bounds__(IM_NT, 1) k_mx_image(ImageArgs a) {
 #endif
         int k = 0;
         if (!a.stats) {
-            k = a.kin ? __ldg(a.kin + img / a.k_group) : 0;
+            k = k_next;
+            const int64_t nx = img + gridDim.x;
+            if (a.kin && nx < a.nimg) k_next = __ldg(a.kin + nx / a.k_group);
         } else {
             im_bracket(tile_sh, F, a);
             im_select(F, a, img, tile_sh);
