@@ -574,6 +574,9 @@ def run_gpu(a, rank, world, local):
     import torch
     import torch.distributed as dist
 
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: rank {rank} needs GPU {local}, but only {torch.cuda.device_count()} "
+                         f"visible (--gpus {world} runs one process per GPU)")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
