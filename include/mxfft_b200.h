@@ -239,6 +239,11 @@ int32_t mxfft_pipeline_fused_supported(mxfft_plan plan);
  * same one-image-per-CTA kernel, given the per-image k, instead of four line
  * passes; results are identical. */
 void mxfft_fused_image(int32_t on);
+/* Scheduling knob: with on != 0 (the default) the n = 256 / 512 row passes of
+ * mxfft_fft2 (rows stored transposed, fftcore.py:351-353) leave each group of
+ * lines with one TMA tensor store (cp.async.bulk.tensor) from a tile published
+ * in output order, instead of a per-thread copy-out; results are identical. */
+void mxfft_tma_store(int32_t on);
 /* Scheduling knob: with on != 0 (the default) mxfft_fft2 runs n >= 16384
  * passes as stages 0 .. L-2 on the decimated half rows (the n/2-point line
  * kernel) followed by the last stage fused into the transposed store, when

@@ -591,6 +591,7 @@ int32_t mxfft_rss(const void* x, int32_t is_c128, int64_t groups, int32_t coils,
 }
 
 void mxfft_fused_image(int32_t on) { mxfft::g_fused_image = on ? 1 : 0; }
+void mxfft_tma_store(int32_t on) { mxfft::g_tma_store = on ? 1 : 0; }
 
 int32_t mxfft_pipeline_fused_supported(mxfft_plan plan) { return plan && mx_image_ok(plan->p) ? 1 : 0; }
 

@@ -1,6 +1,7 @@
 // mxfft_internal.h -- library-internal types shared by the .cu translation units.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (the encoder is fetched with cudaGetDriverEntryPoint: no libcuda link)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -101,6 +102,10 @@ struct MxLinesArgs {
     int32_t* d_pexp;
     int32_t* d_pshift;
     float* d_pcodes;
+    // transposed stores through TMA (n = 256 / 512 specialised kernels): one
+    // cp.async.bulk.tensor store per group from a tile published in output order
+    int tma_out;
+    alignas(64) CUtensorMap out_map;
 };
 
 // arguments of the generic reference-literal kernel (mxfft_fft.cu)
@@ -130,6 +135,7 @@ bool mx_image_ok(const Plan& p);
 cudaError_t run_mx_image(const Plan& p, const void* x, void* y, int64_t nimg, int mode,
                          const mxfft_prescale_cfg& cfg, mxfft_prescale_result* res, int32_t* kvec,
                          const int32_t* kin, int k_group, cudaStream_t st);
+extern int g_tma_store;    // n = 256 / 512 transposed stores through TMA (mxfft_tma_store)
 extern int g_fused_image;  // mxfft_fft2 runs n = 128 batches on the fused image kernel (mxfft_fused_image)
 cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st);
 cudaError_t run_lines(const Plan& p, const LinePass& lp, cudaStream_t st);

@@ -39,6 +39,49 @@ static cudaError_t disp_fmt(const MxLinesArgs& a, int id, int cpb, size_t smem, 
     return cudaErrorInvalidValue;
 }
 
+#ifndef MXFFT_TMA_STORE
+#define MXFFT_TMA_STORE 1  // n = 256 / 512 transposed stores as one TMA tensor store per group
+#endif
+int g_tma_store = MXFFT_TMA_STORE;
+
+// Tensor map of a transposed store (rows of n x n images stored as columns):
+// `out` seen as (batch n) rows of n complex64.  After the last radix-4 pair of
+// stages, thread tl of a line holds positions 8 tl + (n/4) k + i (k < 4, i < 8),
+// so the rows are split as (k, tl, i) and the box [k][i][tl][LPC columns] lands
+// in shared memory with the T threads of one store instruction on consecutive
+// 128-byte (64-byte) rows: under the 128B (64B) swizzle the warp's 8-byte
+// stores are free of bank conflicts.  Returns false when the driver's encoder
+// is unavailable or refuses the map (the kernel then keeps its own copy-out).
+static bool make_out_map(MxLinesArgs& a) {
+    typedef CUresult (*encode_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static encode_t enc = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            enc = reinterpret_cast<encode_t>(fn);
+        else
+            (void)cudaGetLastError();
+    }
+    if (!enc) return false;
+    const cuuint64_t n = (cuuint64_t)a.n, T = n / 32, lpc = 128 / T;
+    const cuuint64_t batch = (cuuint64_t)(a.total_lines / a.n);
+    const cuuint64_t dims[4] = {n, T, 8, 4 * batch};
+    const cuuint64_t strides[3] = {8 * n * 8, n * 8, (n / 4) * n * 8};  // bytes: 8 rows, 1 row, n/4 rows
+    const cuuint32_t box[4] = {(cuuint32_t)lpc, (cuuint32_t)T, 8, 4};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    const CUtensorMapSwizzle sw = lpc * 8 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+    const CUresult r = enc(&a.out_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, a.out, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 int g_profile_stage_limit = -1;
 int g_profile_flags = 0;
 int g_lines_ctas_per_sm = 0;  // 0: occupancy (see mxfft_lines_ctas_per_sm)
@@ -114,6 +157,11 @@ cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
     const size_t nbuf = nt == 128 ? MXFFT_NBUF : 1;
     const size_t smem = (size_t)a.tw_chunks * 16 + nbuf * (size_t)nt * 32 * sizeof(float2);
     const bool dbg = lp.d_vexp != nullptr;
+    a.tma_out = 0;
+    if (g_tma_store && !dbg && a.tstore && !a.col_mode && !a.seg_log2 && !a.dec && p.cpb >= 8 &&
+        (a.log2T == 3 || a.log2T == 4) && a.stage_limit >= a.log2n && a.lines_per_image == a.n &&
+        a.total_lines % a.n == 0 && a.prof_flags == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0)
+        a.tma_out = make_out_map(a) ? 1 : 0;
     return disp_fmt(a, p.fmt.id, p.cpb, smem, dbg, st);
 }
 

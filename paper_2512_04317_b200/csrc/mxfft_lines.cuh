@@ -597,6 +597,7 @@ struct LCtx {
     int slim;
 };
 
+
 __device__ __forceinline__ void lsync(bool big) {
     if (big) __syncthreads(); else __syncwarp();
 }
@@ -691,6 +692,37 @@ __device__ __forceinline__ void publish2(const float2 (&x)[32], unsigned rb, int
         sts128(radr(rv, k), x[16 + 2 * k], x[17 + 2 * k]);
     }
 }
+
+// Transposed publish for the TMA store (n = 256 / 512): after the last pair of
+// stages x[8k + i] is element 8 tl + (n/4) k + i of line lj; it goes to row
+// r = 8T k + T i + tl, column lj of the box [k][i][tl][LPC] (see make_out_map),
+// rows of RB = 8 LPC bytes under the TMA swizzle of that row size (16-byte
+// chunk index XOR row bits: (r & 7) for 128-byte rows, (r >> 1) & 3 for
+// 64-byte rows -- both depend on tl only).  T RB = 1024 for both sizes.
+template <int LT>
+__device__ __forceinline__ void publish_t(const float2 (&x)[32], unsigned buf, int lj, int tl) {
+    constexpr int T = 1 << LT, RB = 8 * (128 >> LT);
+    static_assert(T * RB == 1024, "n = 256 / 512 only");
+    const unsigned sw = RB == 128 ? (unsigned)(tl & 7) : (unsigned)((tl >> 1) & 3);
+    const unsigned base = buf + (((unsigned)(tl * RB + lj * 8)) ^ (sw << 4));
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(base + (unsigned)(k * 8192 + i * 1024)),
+                         "f"(x[8 * k + i].x), "f"(x[8 * k + i].y)
+                         : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_4d(const void* map, unsigned smem, int c0, int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];\n\t"
+        "cp.async.bulk.commit_group;" ::"l"(map),
+        "r"(smem), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 template <int ID, int CPB>
 __device__ __forceinline__ void pair_stage(float2 (&x)[32], int& P, int& H, const LCtx& L, unsigned rb, int ebase,
@@ -942,6 +974,7 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
     // swizzled address (thread base) ^ (constant chunk offset < 256 chunks) is one
     // LOP3 instead of an XOR plus an add
     constexpr bool AX = LT >= 1 && LT <= 4;
+    constexpr bool TMA_OK = !DBG && (LT == 3 || LT == 4) && MXFFT_PAIR_STAGES && MXFFT_LOCAL_STAGES == 5;
     if (AX && (buf0 & 4095u)) __trap();
     // this thread's line inside the buffer (tile element belem(j, q) = line j, position q)
     auto belem = [&](int j, int q) { return (j >> (lt > 5 ? 0 : 5 - lt)) * (W * 32) + (j & (LPR - 1)) * N + q; };
@@ -1051,15 +1084,28 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
 
         // publish (undo_prescale / 1/n^2 fused), then coalesced stores
         if (kout) scale32<DBG>(x, kout, bad);
+        // n = 256 / 512 transposed stores: the group leaves as one TMA tensor store
+        // from a tile published in output order (whole groups; a replayed group
+        // takes the copy-out below)
+        bool tma = TMA_OK && a.tma_out && (grp + 1) * LPC <= a.total_lines;
         if (!DBG && __syncthreads_or(bad)) {
             replay_lines(a, grp * LPC, LPC, tile_g + (bcur - buf0), lt > 5 ? 0 : 5 - lt, W * 32, LPR - 1);
+            tma = false;
+        } else if (TMA_OK && tma) {
+            if constexpr (TMA_OK) publish_t<LT>(x, bcur, lj, L.tl);
+            fence_proxy_async();
         } else if (H > 0) {
             publish4(x, bcur, ebase, P, H);
         } else {
             publish2(x, bcur, ebase, U, V);
         }
         __syncthreads();
-        if (a.prof_flags & 2) {
+        if (TMA_OK && tma) {
+            if (tid == 0) {
+                const int64_t gl = grp * LPC;
+                tma_store_4d(&a.out_map, bcur, (int)(gl & (N - 1)), 0, 0, (int)(gl >> LN) * 4);
+            }
+        } else if (a.prof_flags & 2) {
         } else if (!strided_out) {
             const int64_t base = grp * LPC * (int64_t)N;
             float4* dst = reinterpret_cast<float4*>(a.out + base) + tid;
@@ -1123,6 +1169,7 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
         const int64_t nxt = grp_it + gridDim.x;
         const unsigned bcur = buf0 + (unsigned)cur * BUFSZ, bnxt = buf0 + (unsigned)(cur ^ 1) * BUFSZ;
         cur ^= 1;
+        if (TMA_OK && tid == 0) bulk_wait_read0();  // ... the TMA store of the group before included
         __syncthreads();  // the other buffer's previous readers are done
         if (nxt < ngroups) issue_tile(nxt, bnxt);
         cp_commit();
@@ -1144,6 +1191,7 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
         body(grp, bcur, kk);
     }
     cp_wait<0>();
+    if (TMA_OK && tid == 0) bulk_wait0();
 }
 
 // Lines of n = 8192/16384 (T = 256/512; one line per CTA): direct loads from
@@ -1465,7 +1513,7 @@ __global__ void __launch_bounds__(1 << LT, 2) k_mx_lines_cl2(MxLinesArgs a) {
 }
 
 template <int ID, int CPB, bool DBG, int LT>
-__global__ void __launch_bounds__(128, MXFFT_LINES_MINB) k_mx_lines(MxLinesArgs a) {
+__global__ void __launch_bounds__(128, MXFFT_LINES_MINB) k_mx_lines(const __grid_constant__ MxLinesArgs a) {
     lines_body_pipe<ID, CPB, DBG, LT>(a);
 }
 

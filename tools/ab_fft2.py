@@ -37,10 +37,13 @@ for path in libs:
     runs.append((os.path.basename(os.path.dirname(path)), L, h, ws, wsb))
 
 stream = torch.cuda.current_stream().cuda_stream
+mode = int(os.environ.get("AB_MODE", "0"))  # 0 forward, 2 round trip (timed per pass either way)
+npass = 4 if mode == 2 else 2
+kk = torch.full((batch,), -3, dtype=torch.int32, device="cuda") if os.environ.get("AB_K") else None
 
 
 def t(L, h, ws, wsb, reps=30):
-    f = lambda: L.mxfft_fft2(h, x.data_ptr(), y.data_ptr(), batch, 0, None, 1, ws.data_ptr(), wsb, stream)
+    f = lambda: L.mxfft_fft2(h, x.data_ptr(), y.data_ptr(), batch, mode, kk.data_ptr() if kk is not None else None, 1, ws.data_ptr(), wsb, stream)
     for _ in range(3):
         assert f() == 0
     torch.cuda.synchronize()
@@ -50,7 +53,7 @@ def t(L, h, ws, wsb, reps=30):
         f()
     e1.record()
     torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps * 1e3 / 2  # per pass
+    return e0.elapsed_time(e1) / reps * 1e3 / npass  # per pass
 
 
 res = {r[0]: [] for r in runs}
