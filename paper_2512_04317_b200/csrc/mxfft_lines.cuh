@@ -974,7 +974,6 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
     // swizzled address (thread base) ^ (constant chunk offset < 256 chunks) is one
     // LOP3 instead of an XOR plus an add
     constexpr bool AX = LT >= 1 && LT <= 4;
-    constexpr bool TMA_OK = !DBG && (LT == 3 || LT == 4) && MXFFT_PAIR_STAGES && MXFFT_LOCAL_STAGES == 5;
     if (AX && (buf0 & 4095u)) __trap();
     // this thread's line inside the buffer (tile element belem(j, q) = line j, position q)
     auto belem = [&](int j, int q) { return (j >> (lt > 5 ? 0 : 5 - lt)) * (W * 32) + (j & (LPR - 1)) * N + q; };
@@ -1084,28 +1083,15 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
 
         // publish (undo_prescale / 1/n^2 fused), then coalesced stores
         if (kout) scale32<DBG>(x, kout, bad);
-        // n = 256 / 512 transposed stores: the group leaves as one TMA tensor store
-        // from a tile published in output order (whole groups; a replayed group
-        // takes the copy-out below)
-        bool tma = TMA_OK && a.tma_out && (grp + 1) * LPC <= a.total_lines;
         if (!DBG && __syncthreads_or(bad)) {
             replay_lines(a, grp * LPC, LPC, tile_g + (bcur - buf0), lt > 5 ? 0 : 5 - lt, W * 32, LPR - 1);
-            tma = false;
-        } else if (TMA_OK && tma) {
-            if constexpr (TMA_OK) publish_t<LT>(x, bcur, lj, L.tl);
-            fence_proxy_async();
         } else if (H > 0) {
             publish4(x, bcur, ebase, P, H);
         } else {
             publish2(x, bcur, ebase, U, V);
         }
         __syncthreads();
-        if (TMA_OK && tma) {
-            if (tid == 0) {
-                const int64_t gl = grp * LPC;
-                tma_store_4d(&a.out_map, bcur, (int)(gl & (N - 1)), 0, 0, (int)(gl >> LN) * 4);
-            }
-        } else if (a.prof_flags & 2) {
+        if (a.prof_flags & 2) {
         } else if (!strided_out) {
             const int64_t base = grp * LPC * (int64_t)N;
             float4* dst = reinterpret_cast<float4*>(a.out + base) + tid;
@@ -1169,7 +1155,6 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
         const int64_t nxt = grp_it + gridDim.x;
         const unsigned bcur = buf0 + (unsigned)cur * BUFSZ, bnxt = buf0 + (unsigned)(cur ^ 1) * BUFSZ;
         cur ^= 1;
-        if (TMA_OK && tid == 0) bulk_wait_read0();  // ... the TMA store of the group before included
         __syncthreads();  // the other buffer's previous readers are done
         if (nxt < ngroups) issue_tile(nxt, bnxt);
         cp_commit();
@@ -1191,7 +1176,114 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
         body(grp, bcur, kk);
     }
     cp_wait<0>();
-    if (TMA_OK && tid == 0) bulk_wait0();
+}
+
+// ---------------------------------------------------------------------------
+// n = 256 / 512 row passes stored transposed (the two passes of mxfft_fft2):
+// the group leaves with ONE TMA tensor store (make_out_map, mxfft_lines.cu).
+// Two 32 KB buffers with fixed roles: X receives the group tiles (cp.async,
+// the next group's tile is issued as soon as this group is in registers), Y is
+// the exchange region of the shared-memory stages and then holds the group in
+// output order ([k][i][tl][LPC] rows under the TMA swizzle, publish_t) for the
+// store.  Thread 0 waits for the previous store's reads of Y after the
+// gather, so that latency hides behind the gather instead of sitting at the
+// top of the group.  A group with a block outside the fast exponent range is
+// replayed exactly into Y and written by a plain loop.
+// ---------------------------------------------------------------------------
+template <int ID, int CPB, int LT>
+__device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
+    static_assert(LT == 3 || LT == 4, "n = 256 / 512");
+    constexpr int NT = 128, GEL = NT * 32, T = 1 << LT, N = 32 * T, LN = LT + 5;
+    constexpr int W = 32, LPC = NT >> LT, LPR = W >> LT;
+    extern __shared__ float4 smem4[];
+    unsigned* tw = reinterpret_cast<unsigned*>(smem4);
+    signed char* twe = reinterpret_cast<signed char*>(tw + N);
+    const int tid = threadIdx.x;
+    load_twiddles<ID, CPB, false>(tw, twe, a, N);
+    LCtx L;
+    L.tw = tw;
+    L.twe = twe;
+    L.tw_sh = (unsigned)__cvta_generic_to_shared(tw);
+    L.lt = LT;
+    L.tl = tid & (T - 1);
+    L.c = L.tl;
+    L.trivial = a.trivial01;
+    L.sigma = a.inverse ? -1.f : 1.f;
+    L.slim = a.stage_limit;
+    const int rcol = (int)(__brev((unsigned)L.c) >> (32 - LT));
+    constexpr unsigned BUFSZ = (unsigned)GEL * 8u;
+    const unsigned bx = (unsigned)__cvta_generic_to_shared(smem4 + a.tw_chunks), by = bx + BUFSZ;
+    char* const y_g = reinterpret_cast<char*>(smem4 + a.tw_chunks) + BUFSZ;  // generic view of Y (replay)
+    if (bx & 4095u) __trap();  // swizzled addresses are formed with XOR / OR on 4 KB-aligned buffers
+    auto belem = [&](int j, int q) { return (j >> (5 - LT)) * (W * 32) + (j & (LPR - 1)) * N + q; };
+    // n = 256: the two line bits within a warp are swapped (conflict-free 64-bit gather, see lines_body_pipe)
+    const int lj = (LT == 3) ? (((tid >> 3) & ~3) | (((tid >> 3) & 1) << 1) | (((tid >> 4) & 1))) : (tid >> LT);
+    const int ebase = belem(lj, 0);
+    const unsigned gaddr = caddr(bx, dsw(ebase >> 1) ^ dsw(rcol >> 1), rcol & 1);
+    const int rch = dsw(tid);
+    const int64_t ngroups = a.total_lines / LPC;  // whole groups (total_lines is a multiple of n)
+    LDbg dbg;
+
+    auto issue_tile = [&](int64_t grp_) {
+        const int64_t grp = a.reverse ? ngroups - 1 - grp_ : grp_;
+        const float4* src = reinterpret_cast<const float4*>(a.in + grp * LPC * (int64_t)N) + tid;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) cp_async16(caddr(bx, rch ^ dsw(NT * k), 0), src + NT * k, true);
+        cp_commit();
+    };
+    auto k_of = [&](int64_t grp_) {
+        const int64_t nl = (a.reverse ? ngroups - 1 - grp_ : grp_) * LPC + lj;
+        return a.kvec ? __ldg(a.kvec + k_index(a, nl)) : 0;
+    };
+
+    int64_t grp_it = blockIdx.x;
+    int kk_nxt = 0;
+    if (grp_it < ngroups) {
+        issue_tile(grp_it);
+        kk_nxt = k_of(grp_it);
+    }
+    for (; grp_it < ngroups; grp_it += gridDim.x) {
+        const int64_t nxt = grp_it + gridDim.x;
+        const int64_t grp = a.reverse ? ngroups - 1 - grp_it : grp_it;
+        const int kk = kk_nxt;
+        cp_wait<0>();
+        __syncthreads();  // the tile is in X (and the twiddles are in place)
+        float2 x[32];
+        bool bad = false;
+#pragma unroll
+        for (int m = 0; m < 32; ++m) x[rev_c<5>(m)] = lds64(gaddr ^ (16u * (unsigned)dsw((m * T) >> 1)));
+        if (nxt < ngroups) kk_nxt = k_of(nxt);
+        if (tid == 0) bulk_wait_read0();  // the previous group's store has read Y
+        __syncthreads();                  // X is in registers: free for the next tile; Y is free
+        if (nxt < ngroups) issue_tile(nxt);
+        const int kin = a.kin_const + a.kin_sign * kk, kout = a.kout_const + a.kout_sign * kk;
+        if (kin) scale32<false>(x, kin, bad);
+        int U, V, P, H;
+        run_stages<ID, CPB, false, LT>(x, U, V, P, H, L, by, ebase, &dbg, bad);
+        if (kout) scale32<false>(x, kout, bad);
+        const int64_t gl = grp * LPC;  // first line of the group: column gl mod n of image gl / n
+        if (__syncthreads_or(bad)) {
+            replay_lines(a, gl, LPC, y_g, 5 - LT, W * 32, LPR - 1);
+            float2* dst = a.out + (gl >> LN) * (int64_t)N * N + (gl & (N - 1));
+            for (int e = tid; e < GEL; e += NT) {
+                const int el = belem(e & (LPC - 1), e >> (7 - LT));
+                dst[(int64_t)(e >> (7 - LT)) * N + (e & (LPC - 1))] =
+                    *reinterpret_cast<const float2*>(y_g + 16 * dsw(el >> 1) + 8 * (el & 1));
+            }
+            continue;  // (the next group's first barrier orders these reads before any write to Y)
+        }
+        publish_t<LT>(x, by, lj, L.tl);
+        fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) tma_store_4d(&a.out_map, by, (int)(gl & (N - 1)), 0, 0, (int)(gl >> LN) * 4);
+    }
+    cp_wait<0>();
+    if (tid == 0) bulk_wait0();
+}
+
+template <int ID, int CPB, int LT>
+__global__ void __launch_bounds__(128, MXFFT_LINES_MINB) k_mx_lines_tma(const __grid_constant__ MxLinesArgs a) {
+    lines_body_tma<ID, CPB, LT>(a);
 }
 
 // Lines of n = 8192/16384 (T = 256/512; one line per CTA): direct loads from
@@ -1550,6 +1642,23 @@ static cudaError_t launch_t(const MxLinesArgs& a, size_t smem, cudaStream_t st) 
 }
 
 template <int ID, int CPB, int LT>
+static cudaError_t launch_tma(const MxLinesArgs& a, size_t smem, cudaStream_t st) {
+    void (*k)(MxLinesArgs) = k_mx_lines_tma<ID, CPB, LT>;
+    cudaError_t e = ensure_smem_attr((const void*)k, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    const int sms = device_attr(cudaDevAttrMultiProcessorCount);
+    int occ = 1;
+    e = cached_occupancy((const void*)k, 128, smem, &occ);
+    if (e != cudaSuccess) return e;
+    const int64_t groups = a.total_lines / (128 >> LT);
+    const int per_sm = g_lines_ctas_per_sm > 0 && g_lines_ctas_per_sm < occ ? g_lines_ctas_per_sm : occ;
+    const int64_t cap = (int64_t)sms * per_sm;
+    k<<<(int)(groups < cap ? groups : cap), 128, smem, st>>>(a);
+    note_launch();
+    return cudaGetLastError();
+}
+
+template <int ID, int CPB, int LT>
 static cudaError_t launch_cl2(const MxLinesArgs& a0, cudaStream_t st) {
     MxLinesArgs a = a0;
     constexpr int NH = 32 << LT;
@@ -1606,6 +1715,8 @@ static cudaError_t disp_lt(const MxLinesArgs& a, size_t smem, cudaStream_t st) {
     }
     if constexpr (!DBG && CPB >= 8) {
         if (a.col_mode || a.seg_log2 || a.stage_limit < a.log2n) return launch_t<ID, CPB, DBG, -1, false>(a, smem, st);
+        if (a.tma_out && a.log2T == 3) return launch_tma<ID, CPB, 3>(a, smem, st);
+        if (a.tma_out && a.log2T == 4) return launch_tma<ID, CPB, 4>(a, smem, st);
         switch (a.log2T) {
             case 0: return launch_t<ID, CPB, DBG, 0, false>(a, smem, st);
             case 1: return launch_t<ID, CPB, DBG, 1, false>(a, smem, st);
