@@ -244,6 +244,13 @@ void mxfft_fused_image(int32_t on);
  * lines with one TMA tensor store (cp.async.bulk.tensor) from a tile published
  * in output order, instead of a per-thread copy-out; results are identical. */
 void mxfft_tma_store(int32_t on);
+/* Scheduling knob: with on != 0 (the default) the line and image kernels are
+ * launched with programmatic stream serialization: each signals
+ * griddepcontrol.launch_dependents when it starts and passes
+ * griddepcontrol.wait before touching any data an earlier kernel produced, so
+ * the next pass's launch and set-up overlap this pass's tail; results are
+ * identical. */
+void mxfft_pdl(int32_t on);
 /* Scheduling knob: with on != 0 (the default) mxfft_fft2 runs n >= 16384
  * passes as stages 0 .. L-2 on the decimated half rows (the n/2-point line
  * kernel) followed by the last stage fused into the transposed store, when

@@ -70,6 +70,7 @@ SIGNATURES = {
     "mxfft_pipeline_fused_supported": ([_vp], _i32),
     "mxfft_fused_image": ([_i32], None),
     "mxfft_tma_store": ([_i32], None),
+    "mxfft_pdl": ([_i32], None),
     "mxfft_split_last_stage": ([_i32], None),
     "mxfft_pipeline_fused": ([_vp, _vp, _vp, _i64, _i32, ctypes.POINTER(PrescaleCfgC), _vp, _vp, _u], _i32),
     "mxfft_rss_scaled": ([_vp, _i32, _i64, _i32, _i64, _vp, _i32, _i32, _vp, _u], _i32),

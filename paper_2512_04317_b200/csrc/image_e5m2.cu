@@ -13,7 +13,7 @@ cudaError_t run_mx_image_e5m2(const ImageArgs& a, int cpb, size_t smem, int grid
     }
     cudaError_t e = ensure_smem_attr((const void*)k, (int)smem);
     if (e != cudaSuccess) return e;
-    k<<<grid, IM_NT, smem, st>>>(a);
+    k<<<grid, IM_NT, smem, st>>>(a);  // (programmatic dependent launch measured +0.8 % here: off)
     note_launch();
     return cudaGetLastError();
 }

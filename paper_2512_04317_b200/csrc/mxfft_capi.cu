@@ -14,6 +14,10 @@
 
 namespace mxfft {
 static std::atomic<long long> g_launches{0};
+#ifndef MXFFT_PDL
+#define MXFFT_PDL 1
+#endif
+int g_pdl = MXFFT_PDL;
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 static std::mutex g_attr_mu;
@@ -592,6 +596,7 @@ int32_t mxfft_rss(const void* x, int32_t is_c128, int64_t groups, int32_t coils,
 
 void mxfft_fused_image(int32_t on) { mxfft::g_fused_image = on ? 1 : 0; }
 void mxfft_tma_store(int32_t on) { mxfft::g_tma_store = on ? 1 : 0; }
+void mxfft_pdl(int32_t on) { mxfft::g_pdl = on ? 1 : 0; }
 
 int32_t mxfft_pipeline_fused_supported(mxfft_plan plan) { return plan && mx_image_ok(plan->p) ? 1 : 0; }
 

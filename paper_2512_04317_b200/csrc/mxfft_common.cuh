@@ -209,6 +209,30 @@ struct TwEntry {
 // launch bookkeeping (gpu_launches)
 void note_launch(int n = 1);
 
+// Programmatic dependent launch (mxfft_pdl): the transform kernels signal
+// griddepcontrol.launch_dependents when they start and pass
+// griddepcontrol.wait before their first access to data that an earlier kernel
+// may have produced (or may still read), so the next kernel's launch, shared
+// memory set-up and twiddle loads overlap the tail of this one.
+extern int g_pdl;
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+template <class Arg>
+inline cudaError_t launch_pdl(void (*k)(Arg), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                              const Arg& a) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = g_pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, a);
+}
+
 // Per-device launch setup (mxfft_capi.cu), thread-safe and keyed by the
 // current device, so a second GPU in the same process gets its own attributes
 // and grid sizes:

@@ -954,7 +954,9 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
     unsigned* tw = reinterpret_cast<unsigned*>(smem4);
     signed char* twe = reinterpret_cast<signed char*>(tw + N);
     const int tid = threadIdx.x;
+    pdl_launch_dependents();
     load_twiddles<ID, CPB, DBG>(tw, twe, a, N);
+    pdl_wait();  // the plan tables are static; everything below may depend on the kernel before
     LCtx L;
     L.tw = tw;
     L.twe = twe;
@@ -1199,7 +1201,9 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
     unsigned* tw = reinterpret_cast<unsigned*>(smem4);
     signed char* twe = reinterpret_cast<signed char*>(tw + N);
     const int tid = threadIdx.x;
+    pdl_launch_dependents();
     load_twiddles<ID, CPB, false>(tw, twe, a, N);
+    pdl_wait();  // the plan tables are static; everything below may depend on the kernel before
     LCtx L;
     L.tw = tw;
     L.twe = twe;
@@ -1636,7 +1640,12 @@ static cudaError_t launch_t(const MxLinesArgs& a, size_t smem, cudaStream_t st) 
     const int per_sm = g_lines_ctas_per_sm > 0 && g_lines_ctas_per_sm < occ ? g_lines_ctas_per_sm : occ;
     const int64_t cap = (int64_t)sms * per_sm;
     const int grid = (int)(groups < cap ? groups : cap);
-    k<<<grid, nt, smem, st>>>(a);
+    if constexpr (BIGK) {
+        k<<<grid, nt, smem, st>>>(a);
+    } else {
+        e = launch_pdl(k, (unsigned)grid, (unsigned)nt, smem, st, a);
+        if (e != cudaSuccess) return e;
+    }
     note_launch();
     return cudaGetLastError();
 }
@@ -1653,7 +1662,8 @@ static cudaError_t launch_tma(const MxLinesArgs& a, size_t smem, cudaStream_t st
     const int64_t groups = a.total_lines / (128 >> LT);
     const int per_sm = g_lines_ctas_per_sm > 0 && g_lines_ctas_per_sm < occ ? g_lines_ctas_per_sm : occ;
     const int64_t cap = (int64_t)sms * per_sm;
-    k<<<(int)(groups < cap ? groups : cap), 128, smem, st>>>(a);
+    e = launch_pdl(k, (unsigned)(groups < cap ? groups : cap), 128u, smem, st, a);
+    if (e != cudaSuccess) return e;
     note_launch();
     return cudaGetLastError();
 }

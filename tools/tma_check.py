@@ -59,6 +59,38 @@ def time_case(n, batch, fmt, B, mode, reps=30):
         print(f"n={n} batch={batch} {fmt} B={B} {mode} tma={on}: us/pass median {v[2]:.1f} min {v[0]:.1f}")
 
 
+def time_pdl(n, batch, fmt, B, reps=30):
+    """round-trip pipeline (statistics + passes) with programmatic dependent launch off / on"""
+    x = torch.from_numpy(ellipse_kspace_batch(batch, n, seed=0)).cuda()
+    y = torch.empty_like(x)
+    plan = mx.make_plan(n, mx.ModeSpec.mx(mx.get_mx_format(fmt), B))
+    cfg = mx.PrescaleConfig()
+    res = {0: [], 1: []}
+    outs = {}
+    for rnd in range(5):
+        for on in (0, 1):
+            L.mxfft_pdl(on)
+            for _ in range(3):
+                mx.pipeline_device(x, plan, cfg, roundtrip=True, out=y)
+            torch.cuda.synchronize()
+            outs[on] = y.clone()
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            e0.record()
+            for _ in range(reps):
+                mx.pipeline_device(x, plan, cfg, roundtrip=True, out=y)
+            e1.record()
+            torch.cuda.synchronize()
+            res[on].append(e0.elapsed_time(e1) / reps * 1e3)
+    same = torch.equal(torch.view_as_real(outs[0]), torch.view_as_real(outs[1]))
+    for on in (0, 1):
+        v = sorted(res[on])
+        print(f"pipeline n={n} batch={batch} {fmt} B={B} pdl={on}: us/step median {v[2]:.1f} min {v[0]:.1f} same={same}")
+
+
+time_pdl(256, 256, "e4m3", 32)
+time_pdl(512, 64, "e3m2", 32)
+time_pdl(128, 4096, "e4m3", 32)
+L.mxfft_pdl(1)
 time_case(256, 256, "e4m3", 32, "forward")
 time_case(256, 256, "e4m3", 32, "roundtrip")
 time_case(512, 64, "e3m2", 32, "forward")
