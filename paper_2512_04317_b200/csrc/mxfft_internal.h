@@ -106,6 +106,7 @@ struct MxLinesArgs {
     // cp.async.bulk.tensor store per group from a tile published in output order
     int tma_out;
     alignas(64) CUtensorMap out_map;
+    alignas(64) CUtensorMap in_map;  // group tiles in gather order ([segment][line][16 elements], make_in_map)
 };
 
 // arguments of the generic reference-literal kernel (mxfft_fft.cu)

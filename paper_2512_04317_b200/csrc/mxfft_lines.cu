@@ -52,10 +52,10 @@ int g_tma_store = MXFFT_TMA_STORE;
 // 128-byte (64-byte) rows: under the 128B (64B) swizzle the warp's 8-byte
 // stores are free of bank conflicts.  Returns false when the driver's encoder
 // is unavailable or refuses the map (the kernel then keeps its own copy-out).
-static bool make_out_map(MxLinesArgs& a) {
-    typedef CUresult (*encode_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+typedef CUresult (*encode_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static encode_t tensor_map_encoder() {
     static encode_t enc = nullptr;
     static bool tried = false;
     if (!tried) {
@@ -68,6 +68,30 @@ static bool make_out_map(MxLinesArgs& a) {
         else
             (void)cudaGetLastError();
     }
+    return enc;
+}
+
+// Tensor map of the group tiles (LPC contiguous rows of n complex64): rows are
+// cut into 128-byte segments of 16 elements and the box is [segment][line][16],
+// so under the 128B swizzle the 16-byte chunk index is XORed with the LINE
+// index: the bit-reversed gather of a warp (elements m T + rcol of 4 (2) lines)
+// then reads 32 distinct 8-byte bank pairs per half-warp (lines_body_tma).
+static bool make_in_map(MxLinesArgs& a) {
+    encode_t enc = tensor_map_encoder();
+    if (!enc) return false;
+    const cuuint64_t n = (cuuint64_t)a.n, T = n / 32, lpc = 128 / T;
+    const cuuint64_t dims[3] = {16, (cuuint64_t)a.total_lines, n / 16};
+    const cuuint64_t strides[2] = {n * 8, 128};  // bytes: one line, one segment
+    const cuuint32_t box[3] = {16, (cuuint32_t)lpc, (cuuint32_t)(n / 16)};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const CUresult r = enc(&a.in_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<float2*>(a.in), dims, strides,
+                           box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+static bool make_out_map(MxLinesArgs& a) {
+    encode_t enc = tensor_map_encoder();
     if (!enc) return false;
     const cuuint64_t n = (cuuint64_t)a.n, T = n / 32, lpc = 128 / T;
     const cuuint64_t batch = (cuuint64_t)(a.total_lines / a.n);
@@ -160,8 +184,9 @@ cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
     a.tma_out = 0;
     if (g_tma_store && !dbg && a.tstore && !a.col_mode && !a.seg_log2 && !a.dec && p.cpb >= 8 &&
         (a.log2T == 3 || a.log2T == 4) && a.stage_limit >= a.log2n && a.lines_per_image == a.n &&
-        a.total_lines % a.n == 0 && a.prof_flags == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0)
-        a.tma_out = make_out_map(a) ? 1 : 0;
+        a.total_lines % a.n == 0 && a.prof_flags == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(a.in) & 15) == 0)
+        a.tma_out = make_out_map(a) && make_in_map(a) ? 1 : 0;
     return disp_fmt(a, p.fmt.id, p.cpb, smem, dbg, st);
 }
 

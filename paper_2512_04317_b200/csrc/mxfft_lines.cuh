@@ -721,6 +721,28 @@ __device__ __forceinline__ void tma_store_4d(const void* map, unsigned smem, int
         "r"(smem), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(unsigned smem, const void* map, int c0, int c1, int c2, unsigned mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(mbar)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned addr, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n\tfence.mbarrier_init.release.cluster;" ::"r"(addr), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned addr, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(addr), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned addr, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "MBW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra MBW_%=;\n\t}" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
@@ -1219,21 +1241,27 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
     const unsigned bx = (unsigned)__cvta_generic_to_shared(smem4 + a.tw_chunks), by = bx + BUFSZ;
     char* const y_g = reinterpret_cast<char*>(smem4 + a.tw_chunks) + BUFSZ;  // generic view of Y (replay)
     if (bx & 4095u) __trap();  // swizzled addresses are formed with XOR / OR on 4 KB-aligned buffers
+    // the tile's mbarrier sits in the padding behind the twiddle tables (5 n bytes used of tw_chunks * 16)
+    const unsigned mbar = (unsigned)__cvta_generic_to_shared(twe + N);
+    if (tid == 0) mbar_init(mbar, 1);
     auto belem = [&](int j, int q) { return (j >> (5 - LT)) * (W * 32) + (j & (LPR - 1)) * N + q; };
-    // n = 256: the two line bits within a warp are swapped (conflict-free 64-bit gather, see lines_body_pipe)
-    const int lj = (LT == 3) ? (((tid >> 3) & ~3) | (((tid >> 3) & 1) << 1) | (((tid >> 4) & 1))) : (tid >> LT);
+    // this thread's line of the group.  n = 256: warp w takes lines b, b + 4, b + 1, b + 5
+    // (b = 2 (w & 1) + 8 (w >> 1)): the two lines of a half-warp differ in bit 2, which the
+    // tile's swizzle (chunk ^ line & 7) turns into disjoint bank groups for the 64-bit gather,
+    // and each warp still covers both halves of the output chunks (publish_t)
+    const int wj = (tid >> 3) & 3;
+    const int lj = (LT == 3) ? (2 * ((tid >> 5) & 1) + 8 * (tid >> 6) + 4 * (wj & 1) + (wj >> 1)) : (tid >> LT);
     const int ebase = belem(lj, 0);
-    const unsigned gaddr = caddr(bx, dsw(ebase >> 1) ^ dsw(rcol >> 1), rcol & 1);
-    const int rch = dsw(tid);
+    // X holds [segment q / 16][line][16 elements] with the 16-byte chunk index XOR (line & 7):
+    // element m T + rcol -> segment (m T) / 16, chunk ((m T mod 16) + rcol) / 2 ^ (line & 7)
+    const unsigned gaddr = bx + (unsigned)lj * 128u + ((unsigned)((rcol >> 1) ^ (lj & 7)) << 4) + 8u * (rcol & 1);
     const int64_t ngroups = a.total_lines / LPC;  // whole groups (total_lines is a multiple of n)
     LDbg dbg;
 
-    auto issue_tile = [&](int64_t grp_) {
+    auto issue_tile = [&](int64_t grp_) {  // thread 0 only
         const int64_t grp = a.reverse ? ngroups - 1 - grp_ : grp_;
-        const float4* src = reinterpret_cast<const float4*>(a.in + grp * LPC * (int64_t)N) + tid;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) cp_async16(caddr(bx, rch ^ dsw(NT * k), 0), src + NT * k, true);
-        cp_commit();
+        mbar_expect_tx(mbar, BUFSZ);
+        tma_load_3d(bx, &a.in_map, 0, (int)(grp * LPC), 0, mbar);
     };
     auto k_of = [&](int64_t grp_) {
         const int64_t nl = (a.reverse ? ngroups - 1 - grp_ : grp_) * LPC + lj;
@@ -1242,24 +1270,31 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
 
     int64_t grp_it = blockIdx.x;
     int kk_nxt = 0;
+    unsigned phase = 0;
+    __syncthreads();  // the mbarrier is initialised (and the twiddles are in place)
     if (grp_it < ngroups) {
-        issue_tile(grp_it);
+        if (tid == 0) issue_tile(grp_it);
         kk_nxt = k_of(grp_it);
     }
     for (; grp_it < ngroups; grp_it += gridDim.x) {
         const int64_t nxt = grp_it + gridDim.x;
         const int64_t grp = a.reverse ? ngroups - 1 - grp_it : grp_it;
         const int kk = kk_nxt;
-        cp_wait<0>();
-        __syncthreads();  // the tile is in X (and the twiddles are in place)
+        mbar_wait(mbar, phase);  // the tile is in X
+        phase ^= 1u;
         float2 x[32];
         bool bad = false;
 #pragma unroll
-        for (int m = 0; m < 32; ++m) x[rev_c<5>(m)] = lds64(gaddr ^ (16u * (unsigned)dsw((m * T) >> 1)));
+        for (int m = 0; m < 32; ++m) {
+            // n = 256: T = 8, two m per 128-byte segment (chunk bit 2 = m & 1); n = 512: one segment per m
+            const unsigned ad = LT == 3 ? (gaddr ^ ((unsigned)(m & 1) << 6)) + (unsigned)(m >> 1) * (LPC * 128u)
+                                        : gaddr + (unsigned)m * (LPC * 128u);
+            x[rev_c<5>(m)] = lds64(ad);
+        }
         if (nxt < ngroups) kk_nxt = k_of(nxt);
         if (tid == 0) bulk_wait_read0();  // the previous group's store has read Y
         __syncthreads();                  // X is in registers: free for the next tile; Y is free
-        if (nxt < ngroups) issue_tile(nxt);
+        if (tid == 0 && nxt < ngroups) issue_tile(nxt);
         const int kin = a.kin_const + a.kin_sign * kk, kout = a.kout_const + a.kout_sign * kk;
         if (kin) scale32<false>(x, kin, bad);
         int U, V, P, H;
@@ -1274,14 +1309,13 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
                 dst[(int64_t)(e >> (7 - LT)) * N + (e & (LPC - 1))] =
                     *reinterpret_cast<const float2*>(y_g + 16 * dsw(el >> 1) + 8 * (el & 1));
             }
-            continue;  // (the next group's first barrier orders these reads before any write to Y)
+            continue;  // (the next group's barrier orders these reads before any write to Y)
         }
         publish_t<LT>(x, by, lj, L.tl);
         fence_proxy_async();
         __syncthreads();
         if (tid == 0) tma_store_4d(&a.out_map, by, (int)(gl & (N - 1)), 0, 0, (int)(gl >> LN) * 4);
     }
-    cp_wait<0>();
     if (tid == 0) bulk_wait0();
 }
 
