@@ -40,7 +40,7 @@ static cudaError_t disp_fmt(const MxLinesArgs& a, int id, int cpb, size_t smem, 
 }
 
 #ifndef MXFFT_TMA_STORE
-#define MXFFT_TMA_STORE 1  // n = 256 / 512 transposed stores as one TMA tensor store per group
+#define MXFFT_TMA_STORE 1  // n = 128 / 256 / 512 transposed-store row passes on the TMA kernel (k_mx_lines_tma)
 #endif
 int g_tma_store = MXFFT_TMA_STORE;
 
@@ -95,14 +95,26 @@ static bool make_out_map(MxLinesArgs& a) {
     if (!enc) return false;
     const cuuint64_t n = (cuuint64_t)a.n, T = n / 32, lpc = 128 / T;
     const cuuint64_t batch = (cuuint64_t)(a.total_lines / a.n);
-    const cuuint64_t dims[4] = {n, T, 8, 4 * batch};
-    const cuuint64_t strides[3] = {8 * n * 8, n * 8, (n / 4) * n * 8};  // bytes: 8 rows, 1 row, n/4 rows
-    const cuuint32_t box[4] = {(cuuint32_t)lpc, (cuuint32_t)T, 8, 4};
-    const cuuint32_t es[4] = {1, 1, 1, 1};
-    const CUtensorMapSwizzle sw = lpc * 8 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-    const CUresult r = enc(&a.out_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, a.out, dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const cuuint64_t row = n * 8;  // bytes
+    CUresult r;
+    if (lpc <= 16) {
+        const cuuint64_t dims[4] = {n, T, 8, 4 * batch};
+        const cuuint64_t strides[3] = {8 * row, row, (n / 4) * row};  // 8 rows, 1 row, n/4 rows
+        const cuuint32_t box[4] = {(cuuint32_t)lpc, (cuuint32_t)T, 8, 4};
+        const cuuint32_t es[4] = {1, 1, 1, 1};
+        const CUtensorMapSwizzle sw = lpc * 8 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+        r = enc(&a.out_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, a.out, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        // n = 128: 32 columns per group = two 128-byte halves of a box row: [k][i][tl][half][16]
+        const cuuint64_t dims[5] = {16, n / 16, T, 8, 4 * batch};
+        const cuuint64_t strides[4] = {128, 8 * row, row, (n / 4) * row};
+        const cuuint32_t box[5] = {16, (cuuint32_t)(lpc / 16), (cuuint32_t)T, 8, 4};
+        const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+        r = enc(&a.out_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, a.out, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     return r == CUDA_SUCCESS;
 }
 
@@ -183,7 +195,7 @@ cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
     const bool dbg = lp.d_vexp != nullptr;
     a.tma_out = 0;
     if (g_tma_store && !dbg && a.tstore && !a.col_mode && !a.seg_log2 && !a.dec && p.cpb >= 8 &&
-        (a.log2T == 3 || a.log2T == 4) && a.stage_limit >= a.log2n && a.lines_per_image == a.n &&
+        a.log2T >= 2 && a.log2T <= 4 && a.stage_limit >= a.log2n && a.lines_per_image == a.n &&
         a.total_lines % a.n == 0 && a.prof_flags == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 &&
         (reinterpret_cast<uintptr_t>(a.in) & 15) == 0)
         a.tma_out = make_out_map(a) && make_in_map(a) ? 1 : 0;

@@ -701,10 +701,13 @@ __device__ __forceinline__ void publish2(const float2 (&x)[32], unsigned rb, int
 // 64-byte rows -- both depend on tl only).  T RB = 1024 for both sizes.
 template <int LT>
 __device__ __forceinline__ void publish_t(const float2 (&x)[32], unsigned buf, int lj, int tl) {
-    constexpr int T = 1 << LT, RB = 8 * (128 >> LT);
-    static_assert(T * RB == 1024, "n = 256 / 512 only");
-    const unsigned sw = RB == 128 ? (unsigned)(tl & 7) : (unsigned)((tl >> 1) & 3);
-    const unsigned base = buf + (((unsigned)(tl * RB + lj * 8)) ^ (sw << 4));
+    constexpr int T = 1 << LT, LPC = 128 >> LT;
+    constexpr int RB = LPC >= 16 ? 128 : 8 * LPC;  // bytes per box row
+    constexpr int HV = LPC > 16 ? LPC / 16 : 1;    // 128-byte halves per (k, i, tl) (n = 128: 2)
+    static_assert(T * HV * RB == 1024, "n = 128 / 256 / 512 only");
+    const int r = tl * HV + (lj >> 4) * (HV > 1);  // row within the (k, i) slab; bits above vanish mod 8 rows
+    const unsigned sw = RB == 128 ? (unsigned)(r & 7) : (unsigned)((r >> 1) & 3);
+    const unsigned base = buf + (((unsigned)(r * RB + (lj & 15) * 8)) ^ (sw << 4));
 #pragma unroll
     for (int k = 0; k < 4; ++k)
 #pragma unroll
@@ -719,6 +722,13 @@ __device__ __forceinline__ void tma_store_4d(const void* map, unsigned smem, int
         "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];\n\t"
         "cp.async.bulk.commit_group;" ::"l"(map),
         "r"(smem), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_5d(const void* map, unsigned smem, int c0, int c1, int c2, int c3, int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];\n\t"
+        "cp.async.bulk.commit_group;" ::"l"(map),
+        "r"(smem), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
         : "memory");
 }
 __device__ __forceinline__ void tma_load_3d(unsigned smem, const void* map, int c0, int c1, int c2, unsigned mbar) {
@@ -1216,7 +1226,7 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
 // ---------------------------------------------------------------------------
 template <int ID, int CPB, int LT>
 __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
-    static_assert(LT == 3 || LT == 4, "n = 256 / 512");
+    static_assert(LT >= 2 && LT <= 4, "n = 128 / 256 / 512");
     constexpr int NT = 128, GEL = NT * 32, T = 1 << LT, N = 32 * T, LN = LT + 5;
     constexpr int W = 32, LPC = NT >> LT, LPR = W >> LT;
     extern __shared__ float4 smem4[];
@@ -1245,12 +1255,16 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
     const unsigned mbar = (unsigned)__cvta_generic_to_shared(twe + N);
     if (tid == 0) mbar_init(mbar, 1);
     auto belem = [&](int j, int q) { return (j >> (5 - LT)) * (W * 32) + (j & (LPR - 1)) * N + q; };
-    // this thread's line of the group.  n = 256: warp w takes lines b, b + 4, b + 1, b + 5
-    // (b = 2 (w & 1) + 8 (w >> 1)): the two lines of a half-warp differ in bit 2, which the
-    // tile's swizzle (chunk ^ line & 7) turns into disjoint bank groups for the 64-bit gather,
-    // and each warp still covers both halves of the output chunks (publish_t)
-    const int wj = (tid >> 3) & 3;
-    const int lj = (LT == 3) ? (2 * ((tid >> 5) & 1) + 8 * (tid >> 6) + 4 * (wj & 1) + (wj >> 1)) : (tid >> LT);
+    // this thread's line of the group, chosen so that the 64-bit gather from X (chunk index XOR
+    // line & 7) and the 64-bit stores of publish_t both touch 16 distinct 8-byte bank pairs per
+    // half-warp.  n = 256: warp w takes lines b, b + 4 | b + 1, b + 5 (b = 2 (w & 1) + 8 (w >> 1)):
+    // the two lines of a half-warp differ in bit 2.  n = 128: warp w takes lines 8 w + {0, 3, 5, 6} |
+    // {1, 2, 4, 7} (even / odd parity): distinct l >> 1 for the gather, no pair (l, l ^ 4) for the
+    // publish.  n = 512: a half-warp is one line (any order works).
+    const int wj = (tid >> 3) & 3, g3 = (tid >> 2) & 3;
+    const int lj = LT == 3   ? (2 * ((tid >> 5) & 1) + 8 * (tid >> 6) + 4 * (wj & 1) + (wj >> 1))
+                   : LT == 2 ? (8 * (tid >> 5) + 2 * g3 + ((__popc(g3) & 1) ^ ((tid >> 4) & 1)))
+                             : (tid >> LT);
     const int ebase = belem(lj, 0);
     // X holds [segment q / 16][line][16 elements] with the 16-byte chunk index XOR (line & 7):
     // element m T + rcol -> segment (m T) / 16, chunk ((m T mod 16) + rcol) / 2 ^ (line & 7)
@@ -1286,9 +1300,8 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
         bool bad = false;
 #pragma unroll
         for (int m = 0; m < 32; ++m) {
-            // n = 256: T = 8, two m per 128-byte segment (chunk bit 2 = m & 1); n = 512: one segment per m
-            const unsigned ad = LT == 3 ? (gaddr ^ ((unsigned)(m & 1) << 6)) + (unsigned)(m >> 1) * (LPC * 128u)
-                                        : gaddr + (unsigned)m * (LPC * 128u);
+            constexpr int MS = 16 / T;  // values of m per 128-byte segment (chunk step T / 2)
+            const unsigned ad = (gaddr ^ ((unsigned)(m & (MS - 1)) * (T * 8u))) + (unsigned)(m / MS) * (LPC * 128u);
             x[rev_c<5>(m)] = lds64(ad);
         }
         if (nxt < ngroups) kk_nxt = k_of(nxt);
@@ -1314,7 +1327,10 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
         publish_t<LT>(x, by, lj, L.tl);
         fence_proxy_async();
         __syncthreads();
-        if (tid == 0) tma_store_4d(&a.out_map, by, (int)(gl & (N - 1)), 0, 0, (int)(gl >> LN) * 4);
+        if (tid == 0) {
+            if constexpr (LPC > 16) tma_store_5d(&a.out_map, by, 0, (int)(gl & (N - 1)) >> 4, 0, 0, (int)(gl >> LN) * 4);
+            else tma_store_4d(&a.out_map, by, (int)(gl & (N - 1)), 0, 0, (int)(gl >> LN) * 4);
+        }
     }
     if (tid == 0) bulk_wait0();
 }
@@ -1759,6 +1775,7 @@ static cudaError_t disp_lt(const MxLinesArgs& a, size_t smem, cudaStream_t st) {
     }
     if constexpr (!DBG && CPB >= 8) {
         if (a.col_mode || a.seg_log2 || a.stage_limit < a.log2n) return launch_t<ID, CPB, DBG, -1, false>(a, smem, st);
+        if (a.tma_out && a.log2T == 2) return launch_tma<ID, CPB, 2>(a, smem, st);
         if (a.tma_out && a.log2T == 3) return launch_tma<ID, CPB, 3>(a, smem, st);
         if (a.tma_out && a.log2T == 4) return launch_tma<ID, CPB, 4>(a, smem, st);
         switch (a.log2T) {

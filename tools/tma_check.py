@@ -14,7 +14,8 @@ from paper_2512_04317_b200.workloads import ellipse_kspace_batch  # noqa: E402
 
 L = _native.lib()
 ok = True
-for n, batch in ((256, 24), (512, 10)):
+L.mxfft_fused_image(0)  # n = 128: the line passes, not the fused image kernel
+for n, batch in ((128, 70), (256, 24), (512, 10)):
     x = torch.from_numpy(ellipse_kspace_batch(batch, n, seed=3)).cuda()
     kk = torch.arange(batch, dtype=torch.int32, device="cuda") % 7 - 3
     for fmt in ("e4m3", "e5m2", "e3m2", "e2m3", "e2m1"):
@@ -87,6 +88,9 @@ def time_pdl(n, batch, fmt, B, reps=30):
         print(f"pipeline n={n} batch={batch} {fmt} B={B} pdl={on}: us/step median {v[2]:.1f} min {v[0]:.1f} same={same}")
 
 
+time_case(128, 4096, "e4m3", 32, "roundtrip")
+time_pdl(128, 4096, "e4m3", 32)
+L.mxfft_fused_image(1)
 time_pdl(256, 256, "e4m3", 32)
 time_pdl(512, 64, "e3m2", 32)
 time_pdl(128, 4096, "e4m3", 32)
