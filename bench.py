@@ -428,7 +428,8 @@ def measure_batch(ctx, name, c, steps, warmup, graph=True, e2e=False, cpu_second
         ws = torch.empty(int(_native.lib().mxfft_fft2_workspace_bytes(plan.handle, c["batch"])),
                          dtype=torch.uint8, device="cuda")
         ms_pass = ctx.timed(lambda: mx.fft2_device(x, plan, "forward", out=y, workspace=ws), steps, 2, flush) / 2
-        dom = "mx_line_pass (k_mx_lines)"
+        dom = "mx_line_pass (k_mx_lines_tma: TMA tile load + butterfly stages + TMA transposed store)" if c["n"] in (
+            128, 256, 512) else "mx_line_pass (k_mx_lines)"
         kernels = {"prescale_stats": ms_stats, "mx_line_pass": ms_pass}
         ms_dom = ms_pass
         share = {"prescale_stats": ms_stats / ms, "mx_line_pass": 4 * ms_pass / ms}
@@ -469,7 +470,7 @@ def measure_batch(ctx, name, c, steps, warmup, graph=True, e2e=False, cpu_second
 
     # parity spot check of the timed output (image 0) against the oracle
     step(True, fused)
-    L.mxfft_fused_image(1)
+    L.mxfft_fused_image(-1)
     torch.cuda.synchronize()
     O = _oracle()
     oplan = O.make_plan(c["n"], O.ALL_MX[c["fmt"]], c["block"])

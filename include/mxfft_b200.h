@@ -234,10 +234,11 @@ int32_t mxfft_rss(const void* x, int32_t is_c128, int64_t groups, int32_t coils,
  * mxfft_pipeline_fused_supported(plan) != 0 (n = 128, a hardware MX format,
  * B in {16, 32, 64}). */
 int32_t mxfft_pipeline_fused_supported(mxfft_plan plan);
-/* Scheduling knob: with on != 0 (the default) mxfft_fft2 runs batches of
- * n = 128 images (plans for which mxfft_pipeline_fused_supported holds) on the
- * same one-image-per-CTA kernel, given the per-image k, instead of four line
- * passes; results are identical. */
+/* Scheduling knob for mxfft_fft2 on batches of n = 128 images (plans for which
+ * mxfft_pipeline_fused_supported holds): on > 0 the one-image-per-CTA kernel
+ * (given the per-image k), on == 0 four line passes, on < 0 (the default)
+ * automatic: the line passes when a workspace is given and batch >= 64, else
+ * the one-image-per-CTA kernel; results are identical. */
 void mxfft_fused_image(int32_t on);
 /* Scheduling knob: with on != 0 (the default) the n = 256 / 512 row passes of
  * mxfft_fft2 (rows stored transposed, fftcore.py:351-353) leave each group of

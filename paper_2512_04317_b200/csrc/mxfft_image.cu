@@ -10,7 +10,7 @@ cudaError_t run_mx_image_e2m3(const ImageArgs&, int, size_t, int, cudaStream_t);
 cudaError_t run_mx_image_e3m2(const ImageArgs&, int, size_t, int, cudaStream_t);
 cudaError_t run_mx_image_e2m1(const ImageArgs&, int, size_t, int, cudaStream_t);
 
-int g_fused_image = 1;
+int g_fused_image = -1;  // -1 automatic (mxfft_fft2), 0 line passes, 1 fused image kernel
 
 bool mx_image_ok(const Plan& p) {
     return p.n == IM_N && p.fmt.id != F_GENERIC && (p.cpb == 8 || p.cpb == 16 || p.cpb == 32);

@@ -320,10 +320,11 @@ def _fused_vs_unfused(mx, torch, x, fmt, bsz, roundtrip):
     try:
         y0, k0, r0 = mx.pipeline_device(xd, p, cfg, roundtrip, fused=False)
         torch.cuda.synchronize()
-    finally:
         _native.lib().mxfft_fused_image(1)
-    y2, k2, r2 = mx.pipeline_device(xd, p, cfg, roundtrip, fused=False)  # statistics + fused fft2
-    torch.cuda.synchronize()
+        y2, k2, r2 = mx.pipeline_device(xd, p, cfg, roundtrip, fused=False)  # statistics + fused fft2
+        torch.cuda.synchronize()
+    finally:
+        _native.lib().mxfft_fused_image(-1)  # back to the automatic choice
     assert torch.equal(k2, k0) and torch.equal(r2, r0)
     a2, b2 = y2.cpu().numpy(), y0.cpu().numpy()
     assert ((a2 == b2) | (np.isnan(a2) & np.isnan(b2))).all()
@@ -419,13 +420,16 @@ def test_fused_fft2_modes_inplace_kgroups(mx, torch, mode):
         try:
             want = mx.fft2_device(x, p, mode, k=kk, k_group=g)
             torch.cuda.synchronize()
-        finally:
             L.mxfft_fused_image(1)
-        got = mx.fft2_device(x, p, mode, k=kk, k_group=g)
-        assert torch.equal(got, want), (mode, g)
-        y = x.clone()
-        mx.fft2_device(y, p, mode, k=kk, k_group=g, out=y)
-        assert torch.equal(y, want), ("in place", mode, g)
+            got = mx.fft2_device(x, p, mode, k=kk, k_group=g)
+            assert torch.equal(got, want), (mode, g)
+            y = x.clone()
+            mx.fft2_device(y, p, mode, k=kk, k_group=g, out=y)
+            assert torch.equal(y, want), ("in place", mode, g)
+        finally:
+            L.mxfft_fused_image(-1)
+        auto = mx.fft2_device(x, p, mode, k=kk, k_group=g)  # the automatic choice
+        assert torch.equal(auto, want), ("auto", mode, g)
 
 
 def test_count_range_flush_stress_deterministic(mx, torch):
