@@ -1241,7 +1241,21 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
     L.twe = twe;
     L.tw_sh = (unsigned)__cvta_generic_to_shared(tw);
     L.lt = LT;
-    L.tl = tid & (T - 1);
+    // Thread -> (line lj of the group, thread tl of the line): a line's T threads are consecutive
+    // lanes of one warp (warp-level exchanges), ordered so that every half-warp of the 64-bit
+    // gather from X (chunk index XOR line & 7) and of the 64-bit stores of publish_t touches 16
+    // distinct 8-byte bank pairs (ncu: no excess shared-memory wavefronts).
+    //  n = 128: warp w takes lines 8 w + {0, 3, 5, 6 | 1, 2, 4, 7} (even / odd parity): a half-warp's
+    //           four lines have distinct l >> 1 (gather) and no pair (l, l ^ 4) (publish);
+    //  n = 256: warp w takes lines b + {0, 5 | 1, 4}, b = 2 (w & 1) + 8 (w >> 1): a half-warp's two
+    //           lines differ in bit 2 (gather) and in bit 0 (publish);
+    //  n = 512: warp w takes lines 2 w, 2 w + 1; a half-warp is threads 0-7 of one line and 8-15 of
+    //           the other (even / odd rcol = the two halves of a 16-byte chunk in both patterns).
+    const int lane = tid & 31, wj = (lane >> 3) & 3, g3 = (lane >> 2) & 3;
+    const int lj = LT == 2   ? (8 * (tid >> 5) + 2 * g3 + ((__popc(g3) & 1) ^ (lane >> 4)))
+                   : LT == 3 ? (2 * ((tid >> 5) & 1) + 8 * (tid >> 6) + 4 * (wj & 1) + ((wj & 1) ^ (wj >> 1)))
+                             : (2 * (tid >> 5) + (wj & 1));
+    L.tl = LT == 4 ? ((lane & 7) + 8 * ((wj & 1) ^ (lane >> 4))) : (tid & (T - 1));
     L.c = L.tl;
     L.trivial = a.trivial01;
     L.sigma = a.inverse ? -1.f : 1.f;
@@ -1255,17 +1269,10 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
     const unsigned mbar = (unsigned)__cvta_generic_to_shared(twe + N);
     if (tid == 0) mbar_init(mbar, 1);
     auto belem = [&](int j, int q) { return (j >> (5 - LT)) * (W * 32) + (j & (LPR - 1)) * N + q; };
-    // this thread's line of the group, chosen so that the 64-bit gather from X (chunk index XOR
-    // line & 7) and the 64-bit stores of publish_t both touch 16 distinct 8-byte bank pairs per
-    // half-warp.  n = 256: warp w takes lines b, b + 4 | b + 1, b + 5 (b = 2 (w & 1) + 8 (w >> 1)):
-    // the two lines of a half-warp differ in bit 2.  n = 128: warp w takes lines 8 w + {0, 3, 5, 6} |
-    // {1, 2, 4, 7} (even / odd parity): distinct l >> 1 for the gather, no pair (l, l ^ 4) for the
-    // publish.  n = 512: a half-warp is one line (any order works).
-    const int wj = (tid >> 3) & 3, g3 = (tid >> 2) & 3;
-    const int lj = LT == 3   ? (2 * ((tid >> 5) & 1) + 8 * (tid >> 6) + 4 * (wj & 1) + (wj >> 1))
-                   : LT == 2 ? (8 * (tid >> 5) + 2 * g3 + ((__popc(g3) & 1) ^ ((tid >> 4) & 1)))
-                             : (tid >> LT);
-    const int ebase = belem(lj, 0);
+    // the line's slot in Y (the exchange region): natural thread order for n <= 256, the layout
+    // the swizzled exchange patterns were derived for (two lines per quarter-warp at n = 128);
+    // n = 512: the line itself (its threads are two separate runs of 8 lanes)
+    const int ebase = belem(LT == 4 ? lj : tid >> LT, 0);
     // X holds [segment q / 16][line][16 elements] with the 16-byte chunk index XOR (line & 7):
     // element m T + rcol -> segment (m T) / 16, chunk ((m T mod 16) + rcol) / 2 ^ (line & 7)
     const unsigned gaddr = bx + (unsigned)lj * 128u + ((unsigned)((rcol >> 1) ^ (lj & 7)) << 4) + 8u * (rcol & 1);
