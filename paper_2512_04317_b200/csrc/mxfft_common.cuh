@@ -217,9 +217,9 @@ void note_launch(int n = 1);
 extern int g_pdl;
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-template <class Arg>
-inline cudaError_t launch_pdl(void (*k)(Arg), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
-                              const Arg& a) {
+template <class... Par, class... Arg>
+inline cudaError_t launch_pdl(void (*k)(Par...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                              Arg&&... a) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
@@ -230,7 +230,7 @@ inline cudaError_t launch_pdl(void (*k)(Arg), unsigned grid, unsigned block, siz
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = g_pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k, a);
+    return cudaLaunchKernelEx(&cfg, k, static_cast<Par>(a)...);
 }
 
 // Per-device launch setup (mxfft_capi.cu), thread-safe and keyed by the

@@ -355,6 +355,10 @@ __global__ void __launch_bounds__(PS_THREADS) k_prescale(const T* __restrict__ x
         ps_segment(xall, npts, cfg, out, kvec, (int)blockIdx.x, S);
         return;
     }
+    // launched with programmatic stream serialization behind the sampled kernels (its launch
+    // overlaps their tail; the list is almost always empty): wait for them before the list
+    pdl_launch_dependents();
+    pdl_wait();
     const int cnt = *list_n;
     for (int i = blockIdx.x; i < cnt; i += gridDim.x) {
         ps_segment(xall, npts, cfg, out, kvec, list[i], S);
@@ -400,10 +404,10 @@ cudaError_t launch_prescale(const void* x, int is_c128, int64_t nseg, int64_t np
                                              out, kvec, ws, &list, &list_n, st);
         if (e != cudaSuccess) return e;
         const unsigned grid = (unsigned)(nseg < 64 ? nseg : 64);
-        k_prescale<float2><<<grid, PS_THREADS, smem, st>>>(reinterpret_cast<const float2*>(x), npts, cfg,
-                                                            out, kvec, list, list_n);
+        e = launch_pdl(k_prescale<float2>, grid, PS_THREADS, smem, st, reinterpret_cast<const float2*>(x), npts, cfg,
+                       out, kvec, (const int*)list, (const int*)list_n);
         note_launch();
-        return cudaGetLastError();
+        return e != cudaSuccess ? e : cudaGetLastError();
     }
     k_prescale<float2><<<(unsigned)nseg, PS_THREADS, smem, st>>>(reinterpret_cast<const float2*>(x),
                                                                   npts, cfg, out, kvec, nullptr, nullptr);
