@@ -1695,7 +1695,7 @@ __device__ __forceinline__ void lines_body_cl2(const MxLinesArgs& a) {
 }
 
 template <int ID, int CPB, int LT>
-__global__ void __launch_bounds__(1 << LT, 2) k_mx_lines_cl2(MxLinesArgs a) {
+__global__ void __launch_bounds__(1 << LT, 2) k_mx_lines_cl2(const __grid_constant__ MxLinesArgs a) {
     lines_body_cl2<ID, CPB, LT>(a);
 }
 
@@ -1705,7 +1705,7 @@ __global__ void __launch_bounds__(128, MXFFT_LINES_MINB) k_mx_lines(const __grid
 }
 
 template <int ID, int CPB, bool DBG, int LT>
-__global__ void __launch_bounds__(512, 1) k_mx_lines_big(MxLinesArgs a) {
+__global__ void __launch_bounds__(512, 1) k_mx_lines_big(const __grid_constant__ MxLinesArgs a) {
     lines_body_direct<ID, CPB, DBG, LT>(a);
 }
 
