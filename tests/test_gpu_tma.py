@@ -100,3 +100,49 @@ def test_tma_kernel_in_place_and_many_groups(mx, torch):
         assert torch.equal(torch.view_as_real(y), torch.view_as_real(want))
     finally:
         _knobs(L)
+
+
+@pytest.mark.parametrize("n,batch", [(128, 300), (256, 80), (512, 20)])
+def test_tma_kernel_repeatable_under_buffer_reuse(mx, torch, n, batch):
+    """the same input 20 times, with one CTA per SM (every CTA walks several
+    groups: the tile / work buffers, the mbarrier phases and the split named
+    barriers are reused many times) and with the default occupancy: identical
+    bits every time (a missing wait between the TMA proxies and the threads'
+    shared-memory accesses would show up as run-to-run differences)"""
+    from paper_2512_04317_b200 import _native
+    from paper_2512_04317_b200.workloads import ellipse_kspace_batch
+
+    L = _native.lib()
+    x = torch.from_numpy(ellipse_kspace_batch(batch, n, seed=n, noise=0.02)).cuda()
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.E4M3, 32))
+    try:
+        _knobs(L, tma=0, fused=0)
+        want = mx.fft2_device(x, p, "roundtrip")
+        torch.cuda.synchronize()
+        _knobs(L, tma=1, fused=0)
+        for per_sm in (1, 0):
+            L.mxfft_lines_ctas_per_sm(per_sm)
+            for it in range(20):
+                got = mx.fft2_device(x, p, "roundtrip")
+                assert torch.equal(torch.view_as_real(got), torch.view_as_real(want)), (per_sm, it)
+    finally:
+        L.mxfft_lines_ctas_per_sm(0)
+        _knobs(L)
+
+
+def test_tma_kernel_fewer_groups_than_ctas(mx, torch):
+    """one image: fewer groups than resident CTAs (idle CTAs leave at once)"""
+    from paper_2512_04317_b200 import _native
+
+    L = _native.lib()
+    rng = np.random.default_rng(3)
+    for n in (128, 256, 512):
+        x = (rng.standard_normal((1, n, n)) + 1j * rng.standard_normal((1, n, n))).astype(np.complex64)
+        op = O.make_plan(n, O.E2M1, 16)
+        p = mx.make_plan(n, mx.ModeSpec.mx(mx.get_mx_format("e2m1"), 16))
+        try:
+            _knobs(L, tma=1, fused=0)
+            got = mx.fft2_device(torch.from_numpy(x).cuda(), p, "forward").cpu().numpy()
+        finally:
+            _knobs(L)
+        assert np.array_equal(got[0], O.fft2(x[0], op).astype(np.complex64)), n
