@@ -357,8 +357,10 @@ def measure_batch(ctx, name, c, steps, warmup, graph=True, e2e=False, cpu_second
 
     fused_ok = bool(mx.fused_pipeline_supported(plan))
 
-    def step(roundtrip=True, fused=None):
-        mx.pipeline_device(x, plan, cfg, roundtrip=roundtrip, out=y, k=kbuf, res=rbuf, fused=fused)
+    fold_ok = bool(mx.mri.folded_pipeline_supported(plan))
+
+    def step(roundtrip=True, fused=None, fold=False):
+        mx.pipeline_device(x, plan, cfg, roundtrip=roundtrip, out=y, k=kbuf, res=rbuf, fused=fused, fold=fold)
 
     def graphed(fn):
         if not graph:
@@ -378,35 +380,47 @@ def measure_batch(ctx, name, c, steps, warmup, graph=True, e2e=False, cpu_second
     # + four line passes -- and the fastest one is the measured configuration
     L = _native.lib()
     alt = None
-    fused, knob = False, 1
+    fused, knob, fold = False, 1, False
+    variants = {}
     if fused_ok:
-        variants = {"fused_all_in_one": (True, 1), "stats_then_fused_fft2": (False, 1),
-                    "stats_then_line_passes": (False, 0)}
+        variants = {"fused_all_in_one": (True, 1, False), "stats_then_fused_fft2": (False, 1, False),
+                    "stats_then_line_passes": (False, 0, False)}
+    if fold_ok:
+        # compute_prescale folded into the first line pass (mxfft_pipeline_folded)
+        variants.setdefault("stats_then_line_passes", (False, 0 if fused_ok else 1, False))
+        variants["statistics_folded_into_first_line_pass"] = (False, 0 if fused_ok else 1, True)
+    if variants:
         t = {}
-        for vname, (f, kn) in variants.items():
-            L.mxfft_fused_image(kn)
-            g_rt, _ = graphed(lambda f=f: step(True, f))
+        for vname, (f, kn, fo) in variants.items():
+            L.mxfft_fused_image(kn if fused_ok else -1)
+            g_rt, _ = graphed(lambda f=f, fo=fo: step(True, f, fo))
             t[vname] = ctx.timed(g_rt, steps, warmup, flush)
-        # the fastest variant, except that the line-pass variant (whose kernel's
+        # the fastest variant, except that a line-pass variant (whose kernel's
         # HBM roofline is the per-pass one the other configurations report)
         # wins ties within 2 %: the fused transform is compute-bound and moves
         # 16 B per point per round trip, so its HBM fraction says nothing
         best = min(t, key=t.get)
-        if t["stats_then_line_passes"] <= 1.02 * t[best]:
-            best = "stats_then_line_passes"
-        fused, knob = variants[best]
+        lp_best = min((v for v in t if v.endswith("line_passes") or v.endswith("line_pass")), key=t.get)
+        if t[lp_best] <= 1.02 * t[best]:
+            best = lp_best
+        fused, knob, fold = variants[best]
         alt = {"ms_per_step": t, "chosen": best,
                "value": {v: world * pts / (ms_ * 1e-3) / 1e9 for v, ms_ in t.items()}}
-    L.mxfft_fused_image(knob)
-    run_rt, per_step = graphed(lambda: step(True, fused))
+    L.mxfft_fused_image(knob if fused_ok else -1)
+    run_rt, per_step = graphed(lambda: step(True, fused, fold))
     for _ in range(warmup):
         run_rt()
     l0 = _native.launch_count()
     with ClockSampler(ctx.local) as clk:
         ms = ctx.timed(run_rt, steps, 0, flush)
     launches = per_step * steps if per_step is not None else _native.launch_count() - l0
-    run_fwd, _ = graphed(lambda: step(False, fused))
+    run_fwd, _ = graphed(lambda: step(False, fused, fold))
     ms_fwd = ctx.timed(run_fwd, steps, 2, flush)
+    unsettled = None
+    if fold:  # rows the folded statistics could not settle (pipeline_resolve would re-run them): none expected
+        from paper_2512_04317_b200.prescale import decode_results
+
+        unsettled = int((decode_results(rbuf)["flags"] & 4 != 0).sum())
 
     # the dominant kernel, as the pipeline runs it
     if fused:
@@ -433,6 +447,12 @@ def measure_batch(ctx, name, c, steps, warmup, graph=True, e2e=False, cpu_second
         kernels = {"prescale_stats": ms_stats, "mx_line_pass": ms_pass}
         ms_dom = ms_pass
         share = {"prescale_stats": ms_stats / ms, "mx_line_pass": 4 * ms_pass / ms}
+        if fold:
+            # the step is: accumulator memset + first pass with the statistics + resolve + 3 plain passes;
+            # the standalone statistics kernel (timed above for reference) is NOT part of it
+            kernels = {"mx_line_pass": ms_pass, "mx_first_pass_with_statistics": max(ms - 3 * ms_pass, 0.0),
+                       "prescale_stats_standalone_not_in_step": ms_stats}
+            share = {"mx_line_pass": 3 * ms_pass / ms, "mx_first_pass_with_statistics": max(ms - 3 * ms_pass, 0.0) / ms}
     peak, peak_src = measured_peak_hbm()
     achieved = BYTES_PER_POINT * pts / (ms_dom * 1e-3) / 1e9
     traffic = None
@@ -457,6 +477,7 @@ def measure_batch(ctx, name, c, steps, warmup, graph=True, e2e=False, cpu_second
         "config": describe(name, c, world),
         "l2_flushed_between_steps": flush,
         "implementations": alt,
+        "unsettled_stacks": unsettled,
     }
 
     if e2e:

@@ -59,7 +59,10 @@ typedef struct {
 /* One segment's prescale result (PrescaleResult, prescale.py:40-46).
  * flags bit 0: a non-finite value was seen (InvalidValue);
  * flags bit 1: log2 landed within a few ulps of a rounding boundary, so the
- *              host must confirm k with its own log2 (measure-zero case). */
+ *              host must confirm k with its own log2 (measure-zero case);
+ * flags bit 2: (mxfft_pipeline_folded only) the stack was not settled: re-run it
+ *              with mxfft_prescale_stats + mxfft_fft2;
+ * flags bit 3: (mxfft_pipeline_folded only) k-only row: p_tau / k2 not evaluated. */
 typedef struct {
     double a_max;
     double p_tau;
@@ -261,6 +264,32 @@ void mxfft_split_last_stage(int32_t on);
 int32_t mxfft_pipeline_fused(mxfft_plan plan, const void* x, void* y, int64_t nimg, int32_t roundtrip,
                              const mxfft_prescale_cfg* cfg, mxfft_prescale_result* d_res, int32_t* d_k,
                              uintptr_t stream);
+
+/* The pipelines with compute_prescale FOLDED INTO THE FIRST TRANSFORM PASS
+ * (forward_pipeline / roundtrip_pipeline, mri.py:84-107; n = 128 / 256 / 512,
+ * stacks of `coils` consecutive images share one prescale): no standalone
+ * statistics read of x.  The first row pass runs on the unscaled input and
+ * accumulates, per stack, the largest |x|^2, the smallest nonzero
+ * max(|re|, |im|) and the range of the MX block exponents it produced; a small
+ * kernel then settles k = clip(max(k1, k2)) (prescale.py:66-72) -- k1 from the
+ * peak, k2 <= k1 PROVEN from the smallest nonzero magnitude (p_tau is not
+ * evaluated) -- and the later passes apply 2^k on the way in and 2^-k (and
+ * 1/n^2) on the way out.  This equals the scaled transform bit for bit because
+ * the MX arithmetic commutes with powers of two while every block exponent
+ * stays inside the unclamped range, which the accumulated range proves.
+ * A stack for which any proof fails (k1 near a rounding boundary, tiny nonzero
+ * magnitudes so that k2 may exceed k1, exponents near a clamp, non-finite or
+ * out-of-range input) gets d_res[s].flags = 4 and d_k[s] = 0, and its output
+ * is unspecified: the caller re-runs those stacks with mxfft_prescale_stats +
+ * mxfft_fft2 (pipeline_resolve does).  Settled rows carry flags = 8: k and k1
+ * exact, a_max to 2^-23 relative, p_tau = NaN, k2 = INT32_MIN, nnz = -1.
+ * x, y: complex64 (nimg, n, n), out of place, 16-byte aligned; workspace: at
+ * least mxfft_pipeline_folded_workspace_bytes(plan, nimg, coils) bytes. */
+int32_t mxfft_pipeline_folded_supported(mxfft_plan plan);
+int64_t mxfft_pipeline_folded_workspace_bytes(mxfft_plan plan, int64_t nimg, int32_t coils);
+int32_t mxfft_pipeline_folded(mxfft_plan plan, const void* x, void* y, int64_t nimg, int32_t coils,
+                              int32_t roundtrip, const mxfft_prescale_cfg* cfg, mxfft_prescale_result* d_res,
+                              int32_t* d_k, void* workspace, int64_t workspace_bytes, uintptr_t stream);
 
 /* mxfft_rss with the pipelines' FP64 epilogue folded in: every coil value of
  * group g is multiplied by 2^(k_sign * d_k[g] + exp_const) in FP64 (exact)

@@ -620,6 +620,71 @@ int32_t mxfft_pipeline_fused(mxfft_plan plan, const void* x, void* y, int64_t ni
     return MXFFT_OK;
 }
 
+// ---- statistics folded into the first pass (n = 128 / 256 / 512 on the TMA line kernel) ----
+static bool fold_ok(const Plan& p) {
+    return mxfft::g_tma_store && mx_lines_ok(p) && p.cpb >= 8 && p.log2n >= 7 && p.log2n <= 9;
+}
+int32_t mxfft_pipeline_folded_supported(mxfft_plan plan) { return plan && fold_ok(plan->p) ? 1 : 0; }
+
+int64_t mxfft_pipeline_folded_workspace_bytes(mxfft_plan plan, int64_t nimg, int32_t coils) {
+    if (!plan || nimg <= 0 || coils < 1 || !fold_ok(plan->p)) return 0;
+    const int64_t nstack = nimg / coils;
+    const int64_t nn = (int64_t)plan->p.n * plan->p.n;
+    return nimg * nn * 8 + ((nstack * 32 + 255) / 256) * 256 + nimg * nn / 32 * 4;
+}
+
+int32_t mxfft_pipeline_folded(mxfft_plan plan, const void* x, void* y, int64_t nimg, int32_t coils,
+                              int32_t roundtrip, const mxfft_prescale_cfg* cfg, mxfft_prescale_result* d_res,
+                              int32_t* d_k, void* workspace, int64_t workspace_bytes, uintptr_t stream) {
+    CHECK_PLAN(plan);
+    if (!cfg) return fail(MXFFT_ERR_VALUE, "null config");
+    if (nimg < 0 || coils < 1 || nimg % coils) return fail(MXFFT_ERR_SHAPE, "the batch is not a whole number of coil stacks");
+    if (nimg == 0) return MXFFT_OK;
+    const Plan& p = plan->p;
+    if (!fold_ok(p))
+        return fail(MXFFT_ERR_UNSUPPORTED_SIZE, "the folded pipeline needs n in {128, 256, 512}, a hardware MX format and B in {16, 32, 64}");
+    if (!d_res || !d_k) return fail(MXFFT_ERR_VALUE, "null result rows / k vector");
+    if (x == y) return fail(MXFFT_ERR_VALUE, "the folded pipeline is out of place (flagged stacks are re-run from the input)");
+    if (!workspace || workspace_bytes < mxfft_pipeline_folded_workspace_bytes(plan, nimg, coils))
+        return fail(MXFFT_ERR_VALUE, "folded pipeline workspace too small");
+    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(workspace)) & 15)
+        return fail(MXFFT_ERR_VALUE, "the folded pipeline needs 16-byte aligned buffers");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nn = (int64_t)p.n * p.n, nstack = nimg / coils;
+    unsigned* acc = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(workspace) + nimg * nn * 8);
+    unsigned* minw = acc + ((nstack * 32 + 255) / 256) * 64;
+    CK(cudaMemsetAsync(acc, 0, (size_t)nstack * 32, s), "pipeline_folded (accumulators)");
+    const int npass = roundtrip ? 4 : 2;
+    for (int pass = 0; pass < npass; ++pass) {
+        LinePass lp;
+        lp.in = pass == 0 ? x : ((pass & 1) ? workspace : y);
+        lp.out = (pass & 1) ? y : workspace;
+        lp.tstore = 1;
+        lp.img_elems = nn;
+        lp.lines_per_image = p.n;
+        lp.total_lines = nimg * p.n;
+        lp.batch = nimg;
+        lp.inverse = roundtrip && pass >= 2;
+        lp.reverse = pass & 1;
+        lp.kvec = d_k;
+        lp.k_group = coils;
+        if (pass == 0) {
+            lp.kvec = nullptr;  // unscaled; the pass accumulates the statistics
+            lp.acc = acc;
+            lp.minw = minw;
+        }
+        if (pass == 1) lp.kin_sign = 1;  // x 2^k on the way in (exact: see k_fold_resolve)
+        if (pass == npass - 1) {
+            lp.kout_sign = -1;
+            if (roundtrip) lp.kout_const = -2 * p.log2n;  // x 1/n^2 (mri.py:100)
+        }
+        CK(run_mx_lines(p, lp, s), "pipeline_folded");
+        if (pass == 0)
+            CK(launch_fold_resolve(acc, minw, nstack, coils * nn, *cfg, d_res, d_k, s), "pipeline_folded (resolve)");
+    }
+    return MXFFT_OK;
+}
+
 int32_t mxfft_rss_scaled(const void* x, int32_t is_c128, int64_t groups, int32_t coils, int64_t npix,
                          const int32_t* d_k, int32_t k_sign, int32_t exp_const, double* out, uintptr_t stream) {
     if (coils < 1) return fail(MXFFT_ERR_SHAPE, "need at least one coil");

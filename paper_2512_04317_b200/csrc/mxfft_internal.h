@@ -65,6 +65,8 @@ struct LinePass {
     int seg_log2 = 0;  // rows mode, > 0: element q of line c is in[(q >> seg_log2) * seg_stride + c * 2^seg_log2 + (q & mask)]
     int64_t seg_stride = 0;
     int dec = 0;  // rows mode: line L is half (L & 1) of row L >> 1 of length 2n, decimated (x[2q + h])
+    unsigned* acc = nullptr;  // statistics-folding first pass: per-stack accumulators (8 words each, zeroed)
+    unsigned* minw = nullptr;  // ... and one word per thread and group (total points / 32 words)
     int32_t* d_vexp = nullptr;
     float* d_vcodes = nullptr;
     int32_t* d_pexp = nullptr;
@@ -105,6 +107,8 @@ struct MxLinesArgs {
     // transposed stores through TMA (n = 256 / 512 specialised kernels): one
     // cp.async.bulk.tensor store per group from a tile published in output order
     int tma_out;
+    unsigned* acc;  // statistics-folding first pass (lines_body_tma<.., ACC>), else nullptr
+    unsigned* minw;
     alignas(64) CUtensorMap out_map;
     alignas(64) CUtensorMap in_map;  // group tiles in gather order ([segment][line][16 elements], make_in_map)
 };
@@ -164,6 +168,9 @@ cudaError_t launch_prescale_sample_keys(const float2* x, int64_t npts, int64_t n
 cudaError_t launch_prescale_count_range(const float2* x, int64_t npts, float lo, float hi, float top,
                                         void* state, float2* cand, int64_t cap, float2* topb,
                                         int64_t topcap, cudaStream_t st);
+cudaError_t launch_fold_resolve(const unsigned* acc, const unsigned* minw, int64_t nstack, int64_t stack_points,
+                                const mxfft_prescale_cfg& c, mxfft_prescale_result* out, int32_t* kvec,
+                                cudaStream_t st);
 cudaError_t launch_rss(const void* x, int is_c128, int64_t groups, int coils, int64_t npix,
                        double* out, cudaStream_t st, const int32_t* kvec = nullptr, int ksign = 0,
                        int econst = 0);

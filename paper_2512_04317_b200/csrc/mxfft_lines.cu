@@ -20,6 +20,12 @@ cudaError_t run_mx_lines_e3m2_dbg(const MxLinesArgs&, int, size_t, cudaStream_t)
 cudaError_t run_mx_lines_e2m1(const MxLinesArgs&, int, size_t, cudaStream_t);
 cudaError_t run_mx_lines_e2m1_dbg(const MxLinesArgs&, int, size_t, cudaStream_t);
 
+cudaError_t run_mx_lines_acc_e4m3(const MxLinesArgs&, int, size_t, cudaStream_t);
+cudaError_t run_mx_lines_acc_e5m2(const MxLinesArgs&, int, size_t, cudaStream_t);
+cudaError_t run_mx_lines_acc_e2m3(const MxLinesArgs&, int, size_t, cudaStream_t);
+cudaError_t run_mx_lines_acc_e3m2(const MxLinesArgs&, int, size_t, cudaStream_t);
+cudaError_t run_mx_lines_acc_e2m1(const MxLinesArgs&, int, size_t, cudaStream_t);
+
 static cudaError_t disp_fmt(const MxLinesArgs& a, int id, int cpb, size_t smem, bool dbg,
                             cudaStream_t st) {
     if (dbg) switch (id) {
@@ -199,6 +205,19 @@ cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
         a.total_lines % a.n == 0 && a.prof_flags == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 &&
         (reinterpret_cast<uintptr_t>(a.in) & 15) == 0)
         a.tma_out = make_out_map(a) && make_in_map(a) ? 1 : 0;
+    a.acc = lp.acc;
+    a.minw = lp.minw;
+    if (a.acc) {  // statistics-folding first pass: the TMA kernel only (mxfft_pipeline_folded checks first)
+        if (!a.tma_out || !a.minw || a.kin_sign || a.kin_const || a.reverse) return cudaErrorInvalidValue;
+        switch (p.fmt.id) {
+            case F_E4M3: return run_mx_lines_acc_e4m3(a, p.cpb, smem, st);
+            case F_E5M2: return run_mx_lines_acc_e5m2(a, p.cpb, smem, st);
+            case F_E2M3: return run_mx_lines_acc_e2m3(a, p.cpb, smem, st);
+            case F_E3M2: return run_mx_lines_acc_e3m2(a, p.cpb, smem, st);
+            case F_E2M1: return run_mx_lines_acc_e2m1(a, p.cpb, smem, st);
+        }
+        return cudaErrorInvalidValue;
+    }
     return disp_fmt(a, p.fmt.id, p.cpb, smem, dbg, st);
 }
 

@@ -28,6 +28,7 @@
 #include "mxfft_generic.cuh"
 #include "mxfft_internal.h"
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #ifndef MXFFT_PAIR_STORE
 #define MXFFT_PAIR_STORE 1  // strided copy-out: two adjacent lines per thread, 16-byte stores
@@ -303,6 +304,24 @@ __device__ __forceinline__ float amax_2(const float (&a)[NB], const float (&b)[N
     return fmaxf(fmax3(m[0], m[1], m[2 % L]), m[3 % L]);
 }
 
+// The "replay this group" flag threaded through the stage code is either a
+// plain bool or, in the statistics-folding first pass (lines_body_tma<.., ACC>),
+// a BadTrack that also records the range of the v-block exponents it saw.
+struct BadTrack {
+    bool b = false;
+    int lo = 127, hi = -127;
+    __device__ __forceinline__ BadTrack& operator|=(bool v) {
+        b |= v;
+        return *this;
+    }
+    __device__ __forceinline__ operator bool() const { return b; }
+};
+__device__ __forceinline__ void note_ev(bool&, int) {}
+__device__ __forceinline__ void note_ev(BadTrack& t, int ev) {
+    t.lo = min(t.lo, ev);
+    t.hi = max(t.hi, ev);
+}
+
 // floor(log2 am) for the block exponent.  Non-debug kernels read the biased
 // exponent field only: a subnormal am then yields -127, which puts ev below
 // the fast range, so the group is replayed exactly (replay_lines).
@@ -314,15 +333,16 @@ __device__ __forceinline__ int flog2_hot(float am) {
 
 // SLOW: an out-of-range block takes the exact FP64-assisted path inline (as
 // the debug kernels do) instead of flagging a replay of the whole group
-template <int ID, int NB, int G, bool DBG, bool SLOW = DBG>
+template <int ID, int NB, int G, bool DBG, bool SLOW = DBG, class BT = bool>
 __device__ __forceinline__ void mxb(float2 (&u)[NB], float2 (&v)[NB], const unsigned (&w)[NB],
-                                    int ew, const LDbg* d, int bfly0, bool& bad) {
+                                    int ew, const LDbg* d, int bfly0, BT& bad) {
     using F = HwFmt<ID>;
     using Rg = DecodeRange<F>;
     constexpr bool PAIR = G == 2;
     static_assert(!((DBG || SLOW) && G > 2), "the inline exact path splits a block over at most a lane pair");
     const float am = grp_max<G>(amax_c<NB>(v));
     const int ev = am > 0.f ? flog2_hot<DBG || SLOW>(am) - F::EMAX : 0;
+    note_ev(bad, ev);
     const float inv = exp2i(-ev);
     unsigned cv[NB];
     float pr[NB], pi[NB];
@@ -383,13 +403,14 @@ __device__ __forceinline__ void mxb(float2 (&u)[NB], float2 (&v)[NB], const unsi
 // the product block equals the v block shifted by emax, so its codes are the
 // v codes (j = 0) or (ci, -cr) * sigma (j = 1) and E = ev.  Returns false when
 // the exponents leave the fast range (the caller then runs the general path).
-template <int ID, int NB, bool PAIR, int S, bool DBG>
+template <int ID, int NB, bool PAIR, int S, bool DBG, class BT>
 __device__ __forceinline__ bool trivial_block(float2 (&u)[NB], float2 (&v)[NB], int j0,
-                                              float sigma, const LDbg* d, int bfly0) {
+                                              float sigma, const LDbg* d, int bfly0, BT& bad) {
     using F = HwFmt<ID>;
     using Rg = DecodeRange<F>;
     const float am = pair_max<PAIR>(amax_c<NB>(v));
     const int ev = am > 0.f ? flog2_hot<DBG>(am) - F::EMAX : 0;
+    note_ev(bad, ev);
     const bool ok = (ev >= -127) & (ev <= 126) & (ev >= Rg::ELO) & (ev <= Rg::EHI);
     if (DBG && !ok) return false;  // non-debug kernels finish branch-free and replay
     const float inv = exp2i(-ev), sc = exp2i(ev);
@@ -420,9 +441,9 @@ __device__ __forceinline__ bool trivial_block(float2 (&u)[NB], float2 (&v)[NB], 
 // Stages 0/1 take the trivial-twiddle shortcut (plans always qualify; any
 // block outside the fast exponent range goes through the out-of-line exact
 // path).  Stages 2..4 run the general block inline.
-template <int ID, int CPB, int S, bool DBG>
+template <int ID, int CPB, int S, bool DBG, class BT>
 __device__ __forceinline__ void local_stage(float2 (&x)[32], const unsigned* tw, const signed char* twe,
-                                            int c, bool trivial, float sigma, LDbg* d, bool& bad) {
+                                            int c, bool trivial, float sigma, LDbg* d, BT& bad) {
     constexpr int half = 1 << S;
     constexpr int NB = CPB < 16 ? CPB : 16;
     constexpr bool PAIR = CPB == 32;
@@ -442,9 +463,9 @@ __device__ __forceinline__ void local_stage(float2 (&x)[32], const unsigned* tw,
             if constexpr (!DBG) {
                 // computed unconditionally (no join to merge registers at); a
                 // non-trivial plan or an out-of-range block replays the group
-                const bool done = trivial_block<ID, NB, PAIR, S, DBG>(ub, vb, j0, sigma, d, bfly0);
+                const bool done = trivial_block<ID, NB, PAIR, S, DBG>(ub, vb, j0, sigma, d, bfly0, bad);
                 bad |= !(done & trivial);
-            } else if (!(trivial && trivial_block<ID, NB, PAIR, S, DBG>(ub, vb, j0, sigma, d, bfly0))) {
+            } else if (!(trivial && trivial_block<ID, NB, PAIR, S, DBG>(ub, vb, j0, sigma, d, bfly0, bad))) {
                 // exact out-of-line path (also covers plans whose stage-0/1
                 // twiddles are not exactly 1 / -i)
                 float2 tu[NB], tv[NB];
@@ -489,8 +510,8 @@ static __device__ __noinline__ void scale32_slow(float2* x, int e) {
     for (int i = 0; i < 32; ++i) x[i] = make_float2((float)((double)x[i].x * f), (float)((double)x[i].y * f));
 }
 
-template <bool DBG>
-__device__ __forceinline__ void scale32(float2 (&x)[32], int e, bool& bad) {
+template <bool DBG, class BT>
+__device__ __forceinline__ void scale32(float2 (&x)[32], int e, BT& bad) {
     if (!DBG || (e >= -126 && e <= 127)) {
         bad |= !(e >= -126 && e <= 127);  // non-debug kernels replay the group
         const float f = exp2i(e);
@@ -607,9 +628,9 @@ __device__ __forceinline__ void lsync(bool big) {
 // address rb lives in chunk dsw(e/2), half e&1).  On return x[0..15] sit at
 // line positions U.., x[16..31] at V.. .
 // One shared-memory stage s >= 5 (thread t takes butterflies [16t, 16t+16)).
-template <int ID, int CPB, bool DBG>
+template <int ID, int CPB, bool DBG, class BT>
 __device__ __forceinline__ void smem_stage(float2 (&x)[32], int& U, int& V, const LCtx& L, unsigned rb,
-                                           int ebase, int s, bool big, LDbg* dbg, bool& bad) {
+                                           int ebase, int s, bool big, LDbg* dbg, BT& bad) {
     constexpr int NB = CPB < 16 ? CPB : 16;
     constexpr bool PAIR = CPB == 32;
     {  // publish current values at their positions
@@ -763,9 +784,9 @@ __device__ __forceinline__ void bar_sync(int id, int count) {
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-template <int ID, int CPB>
+template <int ID, int CPB, class BT>
 __device__ __forceinline__ void pair_stage(float2 (&x)[32], int& P, int& H, const LCtx& L, unsigned rb, int ebase,
-                                           int s, bool big, bool& bad) {
+                                           int s, bool big, BT& bad) {
     constexpr int G = CPB / 8;  // lanes per MX block
     const int h = 1 << s;
     const int u0 = 8 * L.tl, j0 = u0 & (h - 1);
@@ -825,9 +846,9 @@ struct NoPre {
 };
 // PRE: called once, just before the group's first write to the exchange region rb
 // (n-specialised kernels; the TMA kernel passes its "region is free" barrier)
-template <int ID, int CPB, bool DBG, int LT, class PRE = NoPre>
+template <int ID, int CPB, bool DBG, int LT, class PRE = NoPre, class BT = bool>
 __device__ __forceinline__ void run_stages(float2 (&x)[32], int& U, int& V, int& P, int& H, const LCtx& L,
-                                           unsigned rb, int ebase, LDbg* dbg, bool& bad, PRE pre = PRE()) {
+                                           unsigned rb, int ebase, LDbg* dbg, BT& bad, PRE pre = PRE()) {
     const int lt = LT >= 0 ? LT : L.lt;
     const bool big = lt > 5;  // a line spans several warps
     constexpr int LOCAL = MXFFT_LOCAL_STAGES;  // unrolled register stages (4 or 5)
@@ -1237,7 +1258,19 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
 // top of the group.  A group with a block outside the fast exponent range is
 // replayed exactly into Y and written by a plain loop.
 // ---------------------------------------------------------------------------
-template <int ID, int CPB, int LT>
+//
+// ACC (the first pass of mxfft_pipeline_folded): the pass runs on the UNSCALED
+// input and accumulates, per coil stack (a.acc, 8 words each, zeroed by the
+// caller, all combined with atomicMax): [0] the largest FP32 key re^2 + im^2
+// (bit pattern; >= 0x7f800000: non-finite or overflow), [2] 128 + the largest
+// and [3] 128 - the smallest v-block exponent of any stage, [4] 1 if a group
+// was replayed; and per thread and group one word in a.minw (group g, thread t
+// at 128 g + t): the bit pattern of the smallest nonzero max(|re|, |im|) of the
+// thread's 32 points with its low 6 bits replaced by the thread's count of
+// zero points (0xffffffc0 | 32: all zero).  k_fold_resolve
+// (mxfft_prescale_fast.cu) turns them into k or sends the stack to the
+// standard path.
+template <int ID, int CPB, int LT, bool ACC = false>
 __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
     static_assert(LT >= 2 && LT <= 4, "n = 128 / 256 / 512");
     constexpr int NT = 128, GEL = NT * 32, T = 1 << LT, N = 32 * T, LN = LT + 5;
@@ -1317,12 +1350,29 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
         mbar_wait(mbar, phase);  // the tile is in X
         phase ^= 1u;
         float2 x[32];
-        bool bad = false;
+        typename std::conditional<ACC, BadTrack, bool>::type bad{};
 #pragma unroll
         for (int m = 0; m < 32; ++m) {
             constexpr int MS = 16 / T;  // values of m per 128-byte segment (chunk step T / 2)
             const unsigned ad = (gaddr ^ ((unsigned)(m & (MS - 1)) * (T * 8u))) + (unsigned)(m / MS) * (LPC * 128u);
             x[rev_c<5>(m)] = lds64(ad);
+        }
+        if constexpr (ACC) {
+            // (the whole group belongs to one image: one lane adds the warp's largest key; every
+            // thread leaves one word about its 32 points for k_fold_resolve)
+            unsigned acc_key = 0, acc_min = 0xffffffffu, zeros = 0;
+#pragma unroll
+            for (int m = 0; m < 32; ++m) {
+                const float re = x[m].x, im = x[m].y;
+                acc_key = max(acc_key, __float_as_uint(fmaf(re, re, im * im)));  // NaN / inf compare largest
+                const unsigned ub = __float_as_uint(fmaxf(fabsf(re), fabsf(im)));
+                zeros += ub == 0u;
+                acc_min = min(acc_min, ub - 1u);  // zero -> 2^32 - 1
+            }
+            const unsigned nzb = acc_min + 1u;  // smallest nonzero max(|re|, |im|), 0: none
+            a.minw[grp * NT + tid] = (nzb ? (nzb & ~63u) : 0xffffffc0u) | zeros;
+            acc_key = __reduce_max_sync(0xffffffffu, acc_key);
+            if (lane == 0) atomicMax(a.acc + 8 * ((grp * LPC >> LN) / a.k_group), acc_key);
         }
         if (nxt < ngroups) kk_nxt = k_of(nxt);
         // n <= 256: split barriers instead of one __syncthreads.  Only warp 0 waits for every
@@ -1355,6 +1405,16 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
         run_stages<ID, CPB, false, LT>(x, U, V, P, H, L, by, ebase, &dbg, bad, y_free);
         if (kout) scale32<false>(x, kout, bad);
         const int64_t gl = grp * LPC;  // first line of the group: column gl mod n of image gl / n
+        if constexpr (ACC) {
+            const int hi_ = __reduce_max_sync(0xffffffffu, bad.hi), lo_ = __reduce_min_sync(0xffffffffu, bad.lo);
+            const unsigned b_ = __ballot_sync(0xffffffffu, bad.b);
+            if (lane == 0) {
+                unsigned* ac = a.acc + 8 * ((gl >> LN) / a.k_group);
+                atomicMax(ac + 2, (unsigned)(128 + hi_));
+                atomicMax(ac + 3, (unsigned)(128 - lo_));
+                if (b_) atomicMax(ac + 4, 1u);
+            }
+        }
         if (__syncthreads_or(bad)) {
             replay_lines(a, gl, LPC, y_g, 5 - LT, W * 32, LPR - 1);
             float2* dst = a.out + (gl >> LN) * (int64_t)N * N + (gl & (N - 1));
@@ -1376,9 +1436,9 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
     if (tid == 0) bulk_wait0();
 }
 
-template <int ID, int CPB, int LT>
+template <int ID, int CPB, int LT, bool ACC = false>
 __global__ void __launch_bounds__(128, MXFFT_LINES_MINB) k_mx_lines_tma(const __grid_constant__ MxLinesArgs a) {
-    lines_body_tma<ID, CPB, LT>(a);
+    lines_body_tma<ID, CPB, LT, ACC>(a);
 }
 
 // Lines of n = 8192/16384 (T = 256/512; one line per CTA): direct loads from
@@ -1741,9 +1801,9 @@ static cudaError_t launch_t(const MxLinesArgs& a, size_t smem, cudaStream_t st) 
     return cudaGetLastError();
 }
 
-template <int ID, int CPB, int LT>
+template <int ID, int CPB, int LT, bool ACC = false>
 static cudaError_t launch_tma(const MxLinesArgs& a, size_t smem, cudaStream_t st) {
-    void (*k)(MxLinesArgs) = k_mx_lines_tma<ID, CPB, LT>;
+    void (*k)(MxLinesArgs) = k_mx_lines_tma<ID, CPB, LT, ACC>;
     cudaError_t e = ensure_smem_attr((const void*)k, 227 * 1024);
     if (e != cudaSuccess) return e;
     const int sms = device_attr(cudaDevAttrMultiProcessorCount);
@@ -1833,6 +1893,19 @@ static cudaError_t disp_lt(const MxLinesArgs& a, size_t smem, cudaStream_t st) {
     } else {
         return launch_t<ID, CPB, DBG, -1, false>(a, smem, st);
     }
+}
+
+// statistics-folding first pass (TMA kernel only; instantiated in lines_acc_<fmt>.cu)
+template <int ID>
+static cudaError_t disp_acc(const MxLinesArgs& a, int cpb, size_t smem, cudaStream_t st) {
+    if (!a.tma_out || !a.acc) return cudaErrorInvalidValue;
+#define MXFFT_ACC_CASE(C, L) \
+    if (cpb == C && a.log2T == L) return launch_tma<ID, C, L, true>(a, smem, st);
+    MXFFT_ACC_CASE(8, 2) MXFFT_ACC_CASE(8, 3) MXFFT_ACC_CASE(8, 4)
+    MXFFT_ACC_CASE(16, 2) MXFFT_ACC_CASE(16, 3) MXFFT_ACC_CASE(16, 4)
+    MXFFT_ACC_CASE(32, 2) MXFFT_ACC_CASE(32, 3) MXFFT_ACC_CASE(32, 4)
+#undef MXFFT_ACC_CASE
+    return cudaErrorInvalidValue;
 }
 
 template <int ID, bool DBG>

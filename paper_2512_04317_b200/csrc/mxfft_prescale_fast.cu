@@ -22,6 +22,7 @@
 //            sort.  Guards: the selected magnitudes must sit clear of the
 //            window edges by more than the FP32 key rounding, else fall back.
 #include <cfloat>
+#include <climits>
 #include <cstdio>
 
 #include <cooperative_groups.h>
@@ -1339,6 +1340,111 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
     k_ps_count<<<(unsigned)(nseg * cps), CNT_THREADS, 0, st>>>(x, npts, cps, sst, cand, cap, top, TOPCAP);
     note_launch();
     k_ps_select<<<(unsigned)nseg, SEL_THREADS, 0, st>>>(sst, list, list_n, cand, cap, top, q, c, out, kvec);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Statistics folded into the first transform pass (mxfft_pipeline_folded).
+// The first row pass ran on the UNSCALED input and left, per coil stack, the
+// accumulators and per-thread words described at lines_body_tma
+// (mxfft_lines.cuh).  One CTA per stack settles k = clip(max(k1, k2))
+// (prescale.py:61-73) WITHOUT evaluating p_tau:
+//  * k1 = round(log2(target / a_max)) from the largest FP32 key (a_max to
+//    2^-23 relative, log2 to 1e-7), unless log2 lands within 1e-6 of a
+//    rounding boundary;
+//  * k2 <= k1 is PROVEN by counting: k2 = ceil(log2(tau_min / p_tau)) <= k1
+//    iff p_tau >= T = tau_min 2^-k1; every np.abs is >= max(|re|, |im|), and
+//    a thread whose smallest nonzero max(|re|, |im|) is >= T holds no
+//    magnitude below T, so at most 32 F magnitudes lie below T, F = the number
+//    of threads with a smaller word.  With nz nonzero points (exact: the
+//    words carry the zero counts) and r = floor((nz - 1) tau / 100),
+//    32 F <= r puts the order statistic v[r] -- and with it p_tau, which
+//    np.percentile interpolates upwards from v[r] -- at or above T;
+//  * the unscaled pass equals the scaled one times 2^-k exactly when every
+//    v-block exponent stays inside the fast range with and without k (the MX
+//    arithmetic is equivariant under powers of two away from its clamps) and
+//    the inputs stay FP32-normal under 2^k.
+// A stack that fails any of these gets flags = 4 and k = 0: the caller
+// (pipeline_resolve) re-runs it through the statistics kernels and the
+// standard passes.  Settled rows carry flags = 8 (a_max approximate, p_tau and
+// k2 not evaluated, nnz exact).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_fold_resolve(const unsigned* __restrict__ acc,
+                                                      const unsigned* __restrict__ minw, int64_t stack_points,
+                                                      mxfft_prescale_cfg c, mxfft_prescale_result* out,
+                                                      int32_t* kvec) {
+    const int64_t s = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const unsigned* a = acc + 8 * s;
+    const unsigned kmx = a[0];
+    const int hi = (int)a[2] - 128, lo = 128 - (int)a[3];
+    const bool replayed = a[4] != 0;
+    // k1 and the threshold T (every thread: the same scalars)
+    const double a_est = sqrt((double)__uint_as_float(kmx));
+    const double L1 = log2(c.target / fmax(a_est, 1e-30));
+    const double d1 = fabs(fabs(L1 - trunc(L1)) - 0.5);
+    const int k1 = round_half_away_d(L1);
+    const int e_key = (int)(kmx >> 23) - 127;
+    const bool k1_ok = kmx < 0x7f800000u && e_key >= -100 && d1 > 1e-6 && k1 > -200 && k1 < 200;
+    const double T = k1_ok ? ldexp(c.tau_min, -k1) * (1.0 + 0x1p-20) : 0.0;  // (margin for the reference's log2 rounding)
+    unsigned zeros = 0, small = 0, mn = 0xffffffffu;
+    const unsigned* w = minw + s * (stack_points / 32);
+    for (int64_t i = tid; i < stack_points / 32; i += 128) {
+        const unsigned v = __ldg(w + i), mb = v & ~63u;
+        zeros += v & 63u;
+        if (mb != 0xffffffc0u) {
+            mn = min(mn, mb);
+            small += (double)__uint_as_float(mb) < T;
+        }
+    }
+    __shared__ unsigned sz[4], ss[4], sm[4];
+    zeros = __reduce_add_sync(0xffffffffu, zeros);
+    small = __reduce_add_sync(0xffffffffu, small);
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    if (lane == 0) {
+        sz[tid >> 5] = zeros;
+        ss[tid >> 5] = small;
+        sm[tid >> 5] = mn;
+    }
+    __syncthreads();
+    if (tid != 0) return;
+    zeros = sz[0] + sz[1] + sz[2] + sz[3];
+    small = ss[0] + ss[1] + ss[2] + ss[3];
+    mn = min(min(sm[0], sm[1]), min(sm[2], sm[3]));
+    const unsigned long long nnz = (unsigned long long)stack_points - zeros;
+    if (kmx < 0x7f800000u && nnz == 0 && !replayed) {  // an all-zero stack: the reference's own formula
+        finish_result(c, 0.0, 0.0, 0ull, out, kvec, (int)s);
+        return;
+    }
+    mxfft_prescale_result r;
+    r.a_max = r.p_tau = __longlong_as_double(0x7ff8000000000000ll);
+    r.k1 = r.k2 = r.k = 0;
+    r.flags = 4;
+    r.nnz = (int64_t)nnz;
+    if (k1_ok && nnz > 0) {
+        const double virt = __dmul_rn((double)(nnz - 1), c.tau / 100.0);
+        const unsigned long long r_lo = virt >= (double)(nnz - 1) ? nnz - 1 : (unsigned long long)floor(virt);
+        const int k = min(max(k1, c.k_min), c.k_max);
+        const int e_mu = (int)(mn >> 23) - 127;  // (mn: a lower bound of the smallest nonzero max(|re|, |im|))
+        const bool ok = 32ull * small <= r_lo && !replayed && k >= -100 && k <= 100 && lo >= -90 && hi <= 90 &&
+                        lo + k >= -90 && hi + k <= 90 && e_mu >= -100 && e_mu + k >= -100 && e_key / 2 + k <= 100;
+        if (ok) {
+            r.a_max = a_est;
+            r.k1 = k1;
+            r.k2 = INT_MIN;
+            r.k = k;
+            r.flags = 8;
+        }
+    }
+    out[s] = r;
+    kvec[s] = r.k;
+}
+
+cudaError_t launch_fold_resolve(const unsigned* acc, const unsigned* minw, int64_t nstack, int64_t stack_points,
+                                const mxfft_prescale_cfg& c, mxfft_prescale_result* out, int32_t* kvec,
+                                cudaStream_t st) {
+    k_fold_resolve<<<(unsigned)nstack, 128, 0, st>>>(acc, minw, stack_points, c, out, kvec);
     note_launch();
     return cudaGetLastError();
 }

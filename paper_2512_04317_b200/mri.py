@@ -103,6 +103,11 @@ def rss(images) -> RssImage:
 # or, with MXFFT_FUSED=1, the fused one-image-per-CTA kernel
 # (mxfft_pipeline_fused).  Results are identical either way.
 FUSED = os.environ.get("MXFFT_FUSED", "0") == "1"
+# n = 128 / 256 / 512: compute_prescale folded into the first transform pass
+# (mxfft_pipeline_folded: no standalone statistics read of x).  Stacks the
+# in-kernel proofs cannot settle come back with flag bit 2 and are re-run by
+# pipeline_resolve through the statistics kernels.  MXFFT_FOLD=0 turns it off.
+FOLD = os.environ.get("MXFFT_FOLD", "1") == "1"
 
 
 def fused_pipeline_supported(plan: FftPlan, coils: int = 1) -> bool:
@@ -114,8 +119,16 @@ def fused_pipeline_supported(plan: FftPlan, coils: int = 1) -> bool:
     return bool(_native.load().mxfft_pipeline_fused_supported(plan.handle))
 
 
+def folded_pipeline_supported(plan: FftPlan) -> bool:
+    """True when pipeline_device can fold the prescale statistics into the first
+    transform pass (n = 128 / 256 / 512, hardware MX formats, B in {16, 32, 64})."""
+    if plan.mode.kind != "mx":
+        return False
+    return bool(_native.load().mxfft_pipeline_folded_supported(plan.handle))
+
+
 def pipeline_device(x, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, coils: int = 1,
-                    out=None, k=None, res=None, fused=None):
+                    out=None, k=None, res=None, fused=None, fold=None):
     """x: CUDA complex64 (B*coils, N, N).  Stacks of `coils` consecutive images
     share one prescale (C = 1: per image).  Returns (out complex64, k int32 (B,),
     stats uint8 (B, 40)) without synchronizing.
@@ -125,7 +138,14 @@ def pipeline_device(x, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, coil
     raises InvalidValue), bit 1 = a log2 within a few ulps of a rounding
     boundary (k must be confirmed with the host's log2).  pipeline_resolve
     turns them into the reference's behaviour after the fact; pipeline_host
-    calls it on every step."""
+    calls it on every step.
+
+    fold (default: the module's FOLD, on): for n = 128 / 256 / 512 the
+    statistics ride on the first transform pass (mxfft_pipeline_folded).  Rows
+    it settles carry flag bit 3 (k exact; a_max approximate, p_tau not
+    evaluated); a stack it cannot settle carries bit 2, its output is
+    unspecified until pipeline_resolve has re-run it.  fold=False always runs
+    the statistics kernels first (full rows)."""
     if x.dim() != 3 or coils < 1 or x.shape[0] % coils:
         raise ShapeError(f"batch of {x.shape[0]} images is not a whole number of {coils}-coil stacks")
     n = plan.n
@@ -149,6 +169,26 @@ def pipeline_device(x, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, coil
                                                          int(bool(roundtrip)), ctypes.byref(c), res.data_ptr(),
                                                          k.data_ptr(), _native.stream_handle()))
         return y, k, res
+    use_fold = FOLD if fold is None else fold
+    if (use_fold and not use_fused and x.is_cuda and nstack > 0 and folded_pipeline_supported(plan)
+            and (out is None or out.data_ptr() != x.data_ptr())):
+        import torch
+
+        if x.dtype != torch.complex64:
+            raise TypeError("expected a CUDA complex64 tensor")
+        x = x.contiguous()
+        y = out if out is not None else torch.empty_like(x)
+        res = res if res is not None else torch.empty((nstack, _native.PRESCALE_RESULT_DTYPE.itemsize),
+                                                      dtype=torch.uint8, device=x.device)
+        k = k if k is not None else torch.empty(nstack, dtype=torch.int32, device=x.device)
+        L = _native.lib()
+        need = int(L.mxfft_pipeline_folded_workspace_bytes(plan.handle, x.shape[0], coils))
+        ws = torch.empty(need, dtype=torch.uint8, device=x.device)
+        c = cfg.as_c()
+        _native.check(L.mxfft_pipeline_folded(plan.handle, x.data_ptr(), y.data_ptr(), x.shape[0], coils,
+                                              int(bool(roundtrip)), ctypes.byref(c), res.data_ptr(), k.data_ptr(),
+                                              ws.data_ptr(), need, _native.stream_handle()))
+        return y, k, res
     res, k = prescale_stats_device(x, nstack, coils * n * n, cfg, k_out=k, res_out=res)
     y = fft2_device(x, plan, "roundtrip" if roundtrip else "forward", k=k, k_group=coils, out=out)
     return y, k, res
@@ -163,10 +203,22 @@ def pipeline_resolve(x, y, k, res, plan: FftPlan, cfg: PrescaleConfig, roundtrip
     import torch
 
     r = decode_results(res)
+    redo = 0
+    unsettled = np.nonzero(r["flags"] & 4)[0]
+    if unsettled.size:
+        # the folded pipeline could not prove k for these stacks: statistics kernels + standard
+        # passes on each run of consecutive stacks, then their rows are looked at like any other
+        runs = np.split(unsettled, np.nonzero(np.diff(unsettled) != 1)[0] + 1)
+        for run in runs:
+            a, b = int(run[0]), int(run[-1]) + 1
+            sl = slice(a * coils, b * coils)
+            pipeline_device(x[sl], plan, cfg, roundtrip, coils=coils, out=y[sl], k=k[a:b], res=res[a:b],
+                            fused=False, fold=False)
+        redo += int(unsettled.size)
+        r = decode_results(res)
     bad = np.nonzero(r["flags"] & 1)[0]
     if bad.size:
         raise InvalidValue(f"non-finite input to prescale (stacks {bad[:8].tolist()})")
-    redo = 0
     for i in np.nonzero(r["flags"] & 2)[0]:
         kh, _, _ = k_from_stats(float(r["a_max"][i]), float(r["p_tau"][i]), cfg)
         if kh == int(r["k"][i]):

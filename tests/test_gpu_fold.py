@@ -1,0 +1,173 @@
+"""The prescale statistics folded into the first transform pass
+(mxfft_pipeline_folded: compute_prescale, prescale.py:61-73, riding on the
+first row pass of fft_2d, fftcore.py:344-353) against the standard path
+(statistics kernels + mxfft_fft2) and the oracle.  Settled stacks must be
+bit-identical; stacks the in-kernel proofs cannot settle must be flagged and
+come out identical after pipeline_resolve."""
+import numpy as np
+import pytest
+
+import oracle as O  # the checker (tests/conftest.py puts oracle/ on the path)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mx():
+    import paper_2512_04317_b200 as m
+
+    return m
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+
+    return t
+
+
+def _rows(mx, res):
+    from paper_2512_04317_b200.prescale import decode_results
+
+    return decode_results(res)
+
+
+def _same(torch, a, b):
+    return torch.equal(torch.view_as_real(a), torch.view_as_real(b))
+
+
+@pytest.mark.parametrize("n,batch,noise", [(128, 41, 0.05), (256, 7, 0.01), (512, 3, 0.01)])
+@pytest.mark.parametrize("fmt,bsz", [("e4m3", 32), ("e5m2", 32), ("e3m2", 16), ("e2m3", 64), ("e2m1", 32)])
+@pytest.mark.parametrize("roundtrip", [False, True])
+def test_fold_equals_standard(mx, torch, n, batch, noise, fmt, bsz, roundtrip):
+    """BASELINE-style k-space (phantom + noise): every stack is settled in the
+    first pass (flags == 8), k and every output bit equal the standard path."""
+    from paper_2512_04317_b200.workloads import ellipse_kspace_batch
+
+    x = torch.from_numpy(ellipse_kspace_batch(batch, n, seed=4000 + n + bsz, noise=noise)).cuda()
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.get_mx_format(fmt), bsz))
+    cfg = mx.PrescaleConfig()
+    assert mx.mri.folded_pipeline_supported(p)
+    y0, k0, r0 = mx.pipeline_device(x, p, cfg, roundtrip, fold=False, fused=False)
+    y1, k1, r1 = mx.pipeline_device(x, p, cfg, roundtrip, fold=True, fused=False)
+    rows = _rows(mx, r1)
+    assert (rows["flags"] == 8).all(), rows["flags"]
+    assert torch.equal(k0, k1)
+    assert _same(torch, y0, y1)
+    full = _rows(mx, r0)
+    assert (rows["k1"] == full["k1"]).all()
+    assert np.allclose(rows["a_max"], full["a_max"], rtol=1e-6, atol=0)
+    assert mx.pipeline_resolve(x, y1, k1, r1, p, cfg, roundtrip) == 0
+
+
+def test_fold_vs_oracle_and_repeatable(mx, torch):
+    """folded C4-shaped batch against the oracle, and identical on a second call
+    into the same buffers (accumulators re-zeroed)"""
+    from paper_2512_04317_b200.workloads import ellipse_kspace_batch
+
+    n, batch = 128, 6
+    xh = ellipse_kspace_batch(batch, n, seed=77, noise=0.05)
+    x = torch.from_numpy(xh).cuda()
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.E4M3, 32))
+    op = O.make_plan(n, O.E4M3, 32)
+    cfg = mx.PrescaleConfig()
+    y = torch.empty_like(x)
+    k = torch.empty(batch, dtype=torch.int32, device="cuda")
+    for _ in range(2):
+        y.zero_()
+        _, _, res = mx.pipeline_device(x, p, cfg, True, out=y, k=k, fold=True, fused=False)
+        assert (_rows(mx, res)["flags"] == 8).all()
+        for i in range(batch):
+            want, _, kw = O.pipeline(xh[i], op, True)
+            assert int(k[i]) == kw
+            assert np.array_equal(y[i].cpu().numpy().astype(np.complex128), want[0])
+
+
+def test_fold_multicoil_shares_one_k(mx, torch):
+    """stacks of 4 coils share one prescale: folded == standard"""
+    from paper_2512_04317_b200.workloads import ellipse_kspace_batch
+
+    n, coils, stacks = 128, 4, 5
+    xh = ellipse_kspace_batch(coils * stacks, n, seed=91, noise=0.02)
+    xh *= np.linspace(0.3, 7.0, coils * stacks, dtype=np.float32)[:, None, None]  # coils of unequal gain
+    x = torch.from_numpy(xh).cuda()
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.E4M3, 32))
+    cfg = mx.PrescaleConfig()
+    y0, k0, _ = mx.pipeline_device(x, p, cfg, True, coils=coils, fold=False, fused=False)
+    y1, k1, r1 = mx.pipeline_device(x, p, cfg, True, coils=coils, fold=True, fused=False)
+    assert k1.numel() == stacks and torch.equal(k0, k1)
+    assert (_rows(mx, r1)["flags"] == 8).all()
+    assert _same(torch, y0, y1)
+
+
+def test_fold_unsettled_stacks_are_flagged_and_resolved(mx, torch):
+    """Inputs on which a proof fails: many tiny nonzero magnitudes (k2 exceeds
+    k1), a peak on a log2 rounding boundary, magnitudes near the ends of FP32's
+    range (block exponents near their clamps), an all-zero image (settled by
+    the reference's own formula).  Flagged stacks equal the standard path after
+    pipeline_resolve; settled neighbours are untouched."""
+    from paper_2512_04317_b200.workloads import ellipse_kspace_batch
+
+    n = 256
+    xh = ellipse_kspace_batch(8, n, seed=5, noise=0.01)
+    xh[1, :64, :] = 1e-9 * (1 + 1j)          # a quarter of the points tiny: k2 > k1, the counting proof fails
+    xh[7, 17, 33] = 1e-9 * (1 + 1j)          # ONE tiny value does not move the 1st percentile: still settled
+    peak = np.abs(xh[2]).max()
+    xh[2] *= np.float32(np.sqrt(2.0) / peak)  # a_max ~ sqrt(2): log2(1 / a_max) ~ -0.5
+    xh[3] *= np.float32(1e-30)               # tiny magnitudes
+    xh[4] *= np.float32(1e+25)               # huge magnitudes (keys overflow FP32)
+    xh[5] = 0                                # all zeros
+    xh[6, :, :] = 0
+    xh[6, 3, 4] = 2.5 - 1j                   # a single nonzero point
+    x = torch.from_numpy(xh).cuda()
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.E4M3, 32))
+    cfg = mx.PrescaleConfig()
+    for roundtrip in (False, True):
+        y0, k0, r0 = mx.pipeline_device(x, p, cfg, roundtrip, fold=False, fused=False)
+        assert mx.pipeline_resolve(x, y0, k0, r0, p, cfg, roundtrip) == 0
+        y1, k1, r1 = mx.pipeline_device(x, p, cfg, roundtrip, fold=True, fused=False)
+        flags = _rows(mx, r1)["flags"].copy()
+        assert flags[0] == 8 and flags[7] == 8
+        assert flags[1] == 4 and flags[3] == 4 and flags[4] == 4, flags
+        assert flags[5] in (0, 2)  # all zeros: the formula itself
+        settled = [i for i in range(8) if not flags[i] & 4]
+        for i in settled:
+            assert int(k1[i]) == int(k0[i]) and _same(torch, y0[i], y1[i]), i
+        nredo = mx.pipeline_resolve(x, y1, k1, r1, p, cfg, roundtrip)
+        assert nredo == int((flags & 4 != 0).sum())
+        assert torch.equal(k0, k1)
+        assert _same(torch, y0, y1)
+        assert not (_rows(mx, r1)["flags"] & 4).any()
+
+
+def test_fold_nonfinite_raises_in_resolve(mx, torch):
+    from paper_2512_04317_b200.workloads import ellipse_kspace_batch
+
+    n = 128
+    xh = ellipse_kspace_batch(3, n, seed=9, noise=0.05)
+    xh[1, 5, 5] = np.nan
+    x = torch.from_numpy(xh).cuda()
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.E4M3, 32))
+    cfg = mx.PrescaleConfig()
+    y, k, res = mx.pipeline_device(x, p, cfg, True, fold=True, fused=False)
+    assert _rows(mx, res)["flags"][1] == 4
+    with pytest.raises(mx.InvalidValue):
+        mx.pipeline_resolve(x, y, k, res, p, cfg, True)
+
+
+def test_fold_custom_config_where_k2_wins(mx, torch):
+    """a tau_min large enough that k2 > k1: the fold must flag, never settle wrongly"""
+    from paper_2512_04317_b200.workloads import ellipse_kspace_batch
+
+    n = 128
+    xh = ellipse_kspace_batch(4, n, seed=11, noise=0.05)
+    x = torch.from_numpy(xh).cuda()
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.E5M2, 32))
+    cfg = mx.PrescaleConfig(tau_min=0.5)
+    y0, k0, r0 = mx.pipeline_device(x, p, cfg, True, fold=False, fused=False)
+    full = _rows(mx, r0)
+    assert (full["k2"] > full["k1"]).all()
+    y1, k1, r1 = mx.pipeline_device(x, p, cfg, True, fold=True, fused=False)
+    assert (_rows(mx, r1)["flags"] == 4).all()
+    assert mx.pipeline_resolve(x, y1, k1, r1, p, cfg, True) == 4
+    assert torch.equal(k0, k1) and _same(torch, y0, y1)
