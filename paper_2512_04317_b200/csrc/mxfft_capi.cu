@@ -630,7 +630,8 @@ int64_t mxfft_pipeline_folded_workspace_bytes(mxfft_plan plan, int64_t nimg, int
     if (!plan || nimg <= 0 || coils < 1 || !fold_ok(plan->p)) return 0;
     const int64_t nstack = nimg / coils;
     const int64_t nn = (int64_t)plan->p.n * plan->p.n;
-    return nimg * nn * 8 + ((nstack * 32 + 255) / 256) * 256 + nimg * nn / 32 * 4;
+    (void)nstack;
+    return nimg * nn * 8 + nimg * nn / 512 * 4 + nimg * nn / 32 * 4;  // scratch image + warp words + thread words
 }
 
 int32_t mxfft_pipeline_folded(mxfft_plan plan, const void* x, void* y, int64_t nimg, int32_t coils,
@@ -652,8 +653,7 @@ int32_t mxfft_pipeline_folded(mxfft_plan plan, const void* x, void* y, int64_t n
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t nn = (int64_t)p.n * p.n, nstack = nimg / coils;
     unsigned* acc = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(workspace) + nimg * nn * 8);
-    unsigned* minw = acc + ((nstack * 32 + 255) / 256) * 64;
-    CK(cudaMemsetAsync(acc, 0, (size_t)nstack * 32, s), "pipeline_folded (accumulators)");
+    unsigned* minw = acc + nimg * nn / 512;
     const int npass = roundtrip ? 4 : 2;
     for (int pass = 0; pass < npass; ++pass) {
         LinePass lp;

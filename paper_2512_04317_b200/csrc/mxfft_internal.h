@@ -65,7 +65,7 @@ struct LinePass {
     int seg_log2 = 0;  // rows mode, > 0: element q of line c is in[(q >> seg_log2) * seg_stride + c * 2^seg_log2 + (q & mask)]
     int64_t seg_stride = 0;
     int dec = 0;  // rows mode: line L is half (L & 1) of row L >> 1 of length 2n, decimated (x[2q + h])
-    unsigned* acc = nullptr;  // statistics-folding first pass: per-stack accumulators (8 words each, zeroed)
+    unsigned* acc = nullptr;  // statistics-folding first pass: two words per warp and group (total points / 512 words)
     unsigned* minw = nullptr;  // ... and one word per thread and group (total points / 32 words)
     int32_t* d_vexp = nullptr;
     float* d_vcodes = nullptr;

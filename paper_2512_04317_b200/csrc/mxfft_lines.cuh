@@ -1260,16 +1260,18 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
 // ---------------------------------------------------------------------------
 //
 // ACC (the first pass of mxfft_pipeline_folded): the pass runs on the UNSCALED
-// input and accumulates, per coil stack (a.acc, 8 words each, zeroed by the
-// caller, all combined with atomicMax): [0] the largest FP32 key re^2 + im^2
-// (bit pattern; >= 0x7f800000: non-finite or overflow), [2] 128 + the largest
-// and [3] 128 - the smallest v-block exponent of any stage, [4] 1 if a group
-// was replayed; and per thread and group one word in a.minw (group g, thread t
-// at 128 g + t): the bit pattern of the smallest nonzero max(|re|, |im|) of the
-// thread's 32 points with its low 6 bits replaced by the thread's count of
-// zero points (0xffffffc0 | 32: all zero).  k_fold_resolve
-// (mxfft_prescale_fast.cu) turns them into k or sends the stack to the
-// standard path.
+// input and leaves, without atomics,
+//  * per warp and group two words in a.acc (group g, warp w at 2 (4 g + w)):
+//    the largest FP32 key re^2 + im^2 of the warp's points (bit pattern;
+//    >= 0x7f800000: non-finite or overflow), and (128 + hi) << 16 |
+//    (128 - lo) << 4 | replayed, [lo, hi] the range of the v-block exponents
+//    of every stage;
+//  * per thread and group one word in a.minw (group g, thread t at 128 g + t):
+//    the bit pattern of the smallest nonzero max(|re|, |im|) of the thread's
+//    32 points with its low 6 bits replaced by the thread's count of zero
+//    points (0xffffffc0 | 32: all zero).
+// k_fold_resolve (mxfft_prescale_fast.cu) turns them into k or sends the stack
+// to the standard path.
 template <int ID, int CPB, int LT, bool ACC = false>
 __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
     static_assert(LT >= 2 && LT <= 4, "n = 128 / 256 / 512");
@@ -1358,21 +1360,27 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
             x[rev_c<5>(m)] = lds64(ad);
         }
         if constexpr (ACC) {
-            // (the whole group belongs to one image: one lane adds the warp's largest key; every
-            // thread leaves one word about its 32 points for k_fold_resolve)
-            unsigned acc_key = 0, acc_min = 0xffffffffu, zeros = 0;
+            unsigned acc_key = 0, mn_all = 0xffffffffu;
 #pragma unroll
             for (int m = 0; m < 32; ++m) {
                 const float re = x[m].x, im = x[m].y;
                 acc_key = max(acc_key, __float_as_uint(fmaf(re, re, im * im)));  // NaN / inf compare largest
-                const unsigned ub = __float_as_uint(fmaxf(fabsf(re), fabsf(im)));
-                zeros += ub == 0u;
-                acc_min = min(acc_min, ub - 1u);  // zero -> 2^32 - 1
+                mn_all = min(mn_all, __float_as_uint(fmaxf(fabsf(re), fabsf(im))));
             }
-            const unsigned nzb = acc_min + 1u;  // smallest nonzero max(|re|, |im|), 0: none
+            unsigned zeros = 0, nzb = mn_all;
+            if (__builtin_expect(mn_all == 0u, 0)) {  // the thread holds zero points: count them, skip them
+                unsigned acc_min = 0xffffffffu;
+#pragma unroll
+                for (int m = 0; m < 32; ++m) {
+                    const unsigned ub = __float_as_uint(fmaxf(fabsf(x[m].x), fabsf(x[m].y)));
+                    zeros += ub == 0u;
+                    acc_min = min(acc_min, ub - 1u);  // zero -> 2^32 - 1
+                }
+                nzb = acc_min + 1u;  // 0: every point is zero
+            }
             a.minw[grp * NT + tid] = (nzb ? (nzb & ~63u) : 0xffffffc0u) | zeros;
             acc_key = __reduce_max_sync(0xffffffffu, acc_key);
-            if (lane == 0) atomicMax(a.acc + 8 * ((grp * LPC >> LN) / a.k_group), acc_key);
+            if (lane == 0) a.acc[(grp * (NT / 32) + (tid >> 5)) * 2] = acc_key;
         }
         if (nxt < ngroups) kk_nxt = k_of(nxt);
         // n <= 256: split barriers instead of one __syncthreads.  Only warp 0 waits for every
@@ -1408,12 +1416,9 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
         if constexpr (ACC) {
             const int hi_ = __reduce_max_sync(0xffffffffu, bad.hi), lo_ = __reduce_min_sync(0xffffffffu, bad.lo);
             const unsigned b_ = __ballot_sync(0xffffffffu, bad.b);
-            if (lane == 0) {
-                unsigned* ac = a.acc + 8 * ((gl >> LN) / a.k_group);
-                atomicMax(ac + 2, (unsigned)(128 + hi_));
-                atomicMax(ac + 3, (unsigned)(128 - lo_));
-                if (b_) atomicMax(ac + 4, 1u);
-            }
+            if (lane == 0)
+                a.acc[(grp * (NT / 32) + (tid >> 5)) * 2 + 1] =
+                    ((unsigned)(128 + hi_) << 16) | ((unsigned)(128 - lo_) << 4) | (b_ ? 1u : 0u);
         }
         if (__syncthreads_or(bad)) {
             replay_lines(a, gl, LPC, y_g, 5 - LT, W * 32, LPR - 1);

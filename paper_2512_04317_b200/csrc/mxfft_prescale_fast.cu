@@ -22,6 +22,7 @@
 //            sort.  Guards: the selected magnitudes must sit clear of the
 //            window edges by more than the FP32 key rounding, else fall back.
 #include <cfloat>
+#include <cstdlib>
 #include <climits>
 #include <cstdio>
 
@@ -1347,7 +1348,7 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
 // ---------------------------------------------------------------------------
 // Statistics folded into the first transform pass (mxfft_pipeline_folded).
 // The first row pass ran on the UNSCALED input and left, per coil stack, the
-// accumulators and per-thread words described at lines_body_tma
+// per-warp and per-thread words described at lines_body_tma
 // (mxfft_lines.cuh).  One CTA per stack settles k = clip(max(k1, k2))
 // (prescale.py:61-73) WITHOUT evaluating p_tau:
 //  * k1 = round(log2(target / a_max)) from the largest FP32 key (a_max to
@@ -1370,48 +1371,108 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
 // standard passes.  Settled rows carry flags = 8 (a_max approximate, p_tau and
 // k2 not evaluated, nnz exact).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_fold_resolve(const unsigned* __restrict__ acc,
-                                                      const unsigned* __restrict__ minw, int64_t stack_points,
-                                                      mxfft_prescale_cfg c, mxfft_prescale_result* out,
-                                                      int32_t* kvec) {
+template <int FR_THREADS>
+__global__ void __launch_bounds__(FR_THREADS) k_fold_resolve(const unsigned* __restrict__ acc,
+                                                             const unsigned* __restrict__ minw, int64_t stack_points,
+                                                             mxfft_prescale_cfg c, mxfft_prescale_result* out,
+                                                             int32_t* kvec) {
+    pdl_launch_dependents();
+    pdl_wait();  // the first pass has finished
+    constexpr int NW = FR_THREADS / 32;
     const int64_t s = blockIdx.x;
-    const int tid = threadIdx.x, lane = tid & 31;
-    const unsigned* a = acc + 8 * s;
-    const unsigned kmx = a[0];
-    const int hi = (int)a[2] - 128, lo = 128 - (int)a[3];
-    const bool replayed = a[4] != 0;
-    // k1 and the threshold T (every thread: the same scalars)
-    const double a_est = sqrt((double)__uint_as_float(kmx));
-    const double L1 = log2(c.target / fmax(a_est, 1e-30));
-    const double d1 = fabs(fabs(L1 - trunc(L1)) - 0.5);
-    const int k1 = round_half_away_d(L1);
-    const int e_key = (int)(kmx >> 23) - 127;
-    const bool k1_ok = kmx < 0x7f800000u && e_key >= -100 && d1 > 1e-6 && k1 > -200 && k1 < 200;
-    const double T = k1_ok ? ldexp(c.tau_min, -k1) * (1.0 + 0x1p-20) : 0.0;  // (margin for the reference's log2 rounding)
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+    __shared__ unsigned sa[NW], sb[NW], sc[NW], sd[NW];
+    __shared__ float s_T;
+    // the thread words of the stack (stack_points / 32, a multiple of 512): first batch in flight
+    const uint4* w4 = reinterpret_cast<const uint4*>(minw + s * (stack_points / 32));
+    const int64_t n4 = stack_points / 128;
+    uint4 first = make_uint4(0xffffffc0u, 0xffffffc0u, 0xffffffc0u, 0xffffffc0u);
+    if (tid < n4) first = __ldg(w4 + tid);
+    // the warps' words: largest key, exponent range, replay flag
+    unsigned kmx = 0, hi_u = 0, lo_u = 0, rep = 0;
+    {
+        const int64_t nw = stack_points / 1024;  // warp entries of the stack
+        const uint2* w = reinterpret_cast<const uint2*>(acc) + s * nw;
+        for (int64_t i = tid; i < nw; i += FR_THREADS) {
+            const uint2 v = __ldg(w + i);
+            kmx = max(kmx, v.x);
+            hi_u = max(hi_u, v.y >> 16);
+            lo_u = max(lo_u, (v.y >> 4) & 0xfffu);
+            rep |= v.y & 1u;
+        }
+        kmx = __reduce_max_sync(0xffffffffu, kmx);
+        hi_u = __reduce_max_sync(0xffffffffu, hi_u);
+        lo_u = __reduce_max_sync(0xffffffffu, lo_u);
+        rep = __reduce_or_sync(0xffffffffu, rep);
+        if (lane == 0) {
+            sa[wp] = kmx;
+            sb[wp] = hi_u;
+            sc[wp] = lo_u;
+            sd[wp] = rep;
+        }
+        __syncthreads();
+    }
+    // k1 and the threshold T: one thread, in FP64
+    double a_est = 0.0;
+    int k1 = 0, e_key = 0;
+    bool k1_ok = false;
+    if (tid == 0) {
+        kmx = hi_u = lo_u = rep = 0;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+            kmx = max(kmx, sa[i]);
+            hi_u = max(hi_u, sb[i]);
+            lo_u = max(lo_u, sc[i]);
+            rep |= sd[i];
+        }
+        a_est = sqrt((double)__uint_as_float(kmx));
+        const double L1 = log2(c.target / fmax(a_est, 1e-30));
+        const double d1 = fabs(fabs(L1 - trunc(L1)) - 0.5);
+        k1 = round_half_away_d(L1);
+        e_key = (int)(kmx >> 23) - 127;
+        k1_ok = kmx < 0x7f800000u && e_key >= -100 && d1 > 1e-6 && k1 > -200 && k1 < 200;
+        // rounded up (and with a margin for the reference's log2 rounding): the count below can only grow
+        s_T = k1_ok ? __double2float_ru(ldexp(c.tau_min, -k1) * (1.0 + 0x1p-20)) : 0.f;
+    }
+    __syncthreads();
+    const float T = s_T;
     unsigned zeros = 0, small = 0, mn = 0xffffffffu;
-    const unsigned* w = minw + s * (stack_points / 32);
-    for (int64_t i = tid; i < stack_points / 32; i += 128) {
-        const unsigned v = __ldg(w + i), mb = v & ~63u;
+    auto take = [&](unsigned v) {
+        const unsigned mb = v & ~63u;
         zeros += v & 63u;
         if (mb != 0xffffffc0u) {
             mn = min(mn, mb);
-            small += (double)__uint_as_float(mb) < T;
+            small += __uint_as_float(mb) < T;
         }
+    };
+    for (int64_t i = tid; i < n4; i += FR_THREADS) {
+        const uint4 v = i == tid ? first : __ldg(w4 + i);
+        take(v.x);
+        take(v.y);
+        take(v.z);
+        take(v.w);
     }
-    __shared__ unsigned sz[4], ss[4], sm[4];
     zeros = __reduce_add_sync(0xffffffffu, zeros);
     small = __reduce_add_sync(0xffffffffu, small);
     mn = __reduce_min_sync(0xffffffffu, mn);
+    __syncthreads();
     if (lane == 0) {
-        sz[tid >> 5] = zeros;
-        ss[tid >> 5] = small;
-        sm[tid >> 5] = mn;
+        sa[wp] = zeros;
+        sb[wp] = small;
+        sc[wp] = mn;
     }
     __syncthreads();
     if (tid != 0) return;
-    zeros = sz[0] + sz[1] + sz[2] + sz[3];
-    small = ss[0] + ss[1] + ss[2] + ss[3];
-    mn = min(min(sm[0], sm[1]), min(sm[2], sm[3]));
+    zeros = small = 0;
+    mn = 0xffffffffu;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+        zeros += sa[i];
+        small += sb[i];
+        mn = min(mn, sc[i]);
+    }
+    const int hi = (int)hi_u - 128, lo = 128 - (int)lo_u;
+    const bool replayed = rep != 0;
     const unsigned long long nnz = (unsigned long long)stack_points - zeros;
     if (kmx < 0x7f800000u && nnz == 0 && !replayed) {  // an all-zero stack: the reference's own formula
         finish_result(c, 0.0, 0.0, 0ull, out, kvec, (int)s);
@@ -1444,9 +1505,19 @@ __global__ void __launch_bounds__(128) k_fold_resolve(const unsigned* __restrict
 cudaError_t launch_fold_resolve(const unsigned* acc, const unsigned* minw, int64_t nstack, int64_t stack_points,
                                 const mxfft_prescale_cfg& c, mxfft_prescale_result* out, int32_t* kvec,
                                 cudaStream_t st) {
-    k_fold_resolve<<<(unsigned)nstack, 128, 0, st>>>(acc, minw, stack_points, c, out, kvec);
+    static const int nt_env = getenv("MXFFT_FR_THREADS") ? atoi(getenv("MXFFT_FR_THREADS")) : 0;
+    // few large stacks: more threads per stack
+    // 128 threads: the CTAs then fit next to the first pass's (3 x 128 threads, ~150 registers) and the
+    // programmatic launch chain first pass -> resolve -> second pass keeps overlapping (256 threads: C2
+    // round trip 270 -> 302 us, C3 310 -> 354 us)
+    const int nt = nt_env ? nt_env : 128;
+    cudaError_t e = nt == 64 ? launch_pdl(k_fold_resolve<64>, (unsigned)nstack, 64u, 0, st, acc, minw, stack_points,
+                                           c, out, kvec) : nt == 256 ? launch_pdl(k_fold_resolve<256>, (unsigned)nstack, 256u, 0, st, acc, minw, stack_points,
+                                           c, out, kvec)
+                              : launch_pdl(k_fold_resolve<128>, (unsigned)nstack, 128u, 0, st, acc, minw, stack_points,
+                                           c, out, kvec);
     note_launch();
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
