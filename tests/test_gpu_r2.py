@@ -54,7 +54,14 @@ def test_baseline_shapes_match_reference_digests(mx, torch, case):
     assert mx.pipeline_resolve(xd, yr, kr, rr, p, cfg, True) == 0
     k, k1, k2 = g[key + "_k"].tolist()
     assert int(kf[0]) == int(kr[0]) == k
-    st = mx.prescale.decode_results(rr)[0]
+    # the default path folds the statistics into the first pass (k-only rows: flags 8, k1 exact,
+    # a_max to 2^-23); the statistics kernels (fold=False) give the full row
+    fr = mx.prescale.decode_results(rr)[0]
+    assert int(fr["flags"]) == 8 and int(fr["k1"]) == k1 and int(fr["k"]) == k
+    assert abs(float(fr["a_max"]) / g[key + "_stats"].tolist()[0] - 1.0) < 1e-6
+    ys, ks, rs = mx.pipeline_device(xd, p, cfg, roundtrip=True, fold=False)
+    assert int(ks[0]) == k and torch.equal(torch.view_as_real(ys), torch.view_as_real(yr))
+    st = mx.prescale.decode_results(rs)[0]
     assert (int(st["k1"]), int(st["k2"])) == (k1, k2)
     assert [float(st["a_max"]), float(st["p_tau"])] == g[key + "_stats"].tolist()
     assert digest(yf[0].cpu().numpy().astype(np.complex128)) == str(g[key + "_fwd"])
@@ -318,10 +325,10 @@ def _fused_vs_unfused(mx, torch, x, fmt, bsz, roundtrip):
     y1, k1, r1 = mx.pipeline_device(xd, p, cfg, roundtrip, fused=True)
     _native.lib().mxfft_fused_image(0)  # the reference path: statistics kernel + four line passes
     try:
-        y0, k0, r0 = mx.pipeline_device(xd, p, cfg, roundtrip, fused=False)
+        y0, k0, r0 = mx.pipeline_device(xd, p, cfg, roundtrip, fused=False, fold=False)
         torch.cuda.synchronize()
         _native.lib().mxfft_fused_image(1)
-        y2, k2, r2 = mx.pipeline_device(xd, p, cfg, roundtrip, fused=False)  # statistics + fused fft2
+        y2, k2, r2 = mx.pipeline_device(xd, p, cfg, roundtrip, fused=False, fold=False)  # statistics + fused fft2
         torch.cuda.synchronize()
     finally:
         _native.lib().mxfft_fused_image(-1)  # back to the automatic choice
