@@ -27,6 +27,9 @@
 #include "mxfft_common.cuh"
 #include "mxfft_generic.cuh"
 #include "mxfft_internal.h"
+#ifndef MXFFT_WARP_LOCAL_EXCHANGE
+#define MXFFT_WARP_LOCAL_EXCHANGE 1  // n >= 2048: warp-level sync for the exchanges that stay inside a warp
+#endif
 #include <cooperative_groups.h>
 #include <type_traits>
 
@@ -894,7 +897,9 @@ __device__ __forceinline__ void run_stages(float2 (&x)[32], int& U, int& V, int&
 #pragma unroll 1
         for (s += 2; s < LT + 5; s += 2) {
             publish4(x, rb, ebase, P, H);
-            lsync(LT > 5);
+            // the exchange before stages (s, s + 1) stays inside a 2^(s+2)-position chunk, i.e. the
+            // 2^(s-3) consecutive threads that own it after the first exchange: one warp for s <= 8
+            lsync(LT > 5 && (s > 8 || !MXFFT_WARP_LOCAL_EXCHANGE));
             pair_stage<ID, CPB>(x, P, H, L, rb, ebase, s, LT > 5, bad);
         }
         return;

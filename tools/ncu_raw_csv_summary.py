@@ -1,5 +1,5 @@
 """Summarise an exported ncu raw page (ncu -i rep --page raw --csv) into the
-metric list kept under profiles/.  usage: python tools/ncu_raw_csv_summary.py raw.csv 'header line'"""
+metric list kept under profiles/.  usage: python tools/ncu_raw_csv_summary.py raw.csv 'header line' [launch index]"""
 import csv
 import sys
 
@@ -13,7 +13,7 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
         "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
 rows = list(csv.reader(open(sys.argv[1])))
-h, u, v = rows[0], rows[1], rows[2]
+h, u, v = rows[0], rows[1], rows[2 + (int(sys.argv[3]) if len(sys.argv) > 3 else 0)]
 print("#", sys.argv[2] if len(sys.argv) > 2 else sys.argv[1])
 print("# (cold, serialised replay under ncu: use ratios and shares, not absolute times, as bench values)")
 print("Kernel Name =", v[h.index("Kernel Name")])
