@@ -318,14 +318,25 @@ def pipeline_host(x_host, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, o
 
 def _resolve_host(x_host, out_host, stats, plan, cfg, roundtrip, coils):
     """pipeline_resolve for pipeline_host: one small D2H of the statistics rows
-    of every slice; InvalidValue for non-finite stacks, and stacks whose k sat
-    on a log2 rounding boundary are redone from the host copy with the host's
-    k (never for real data)."""
+    of every slice; stacks the folded pipeline left unsettled (flag bit 2) are
+    redone from the host copy through the statistics kernels; InvalidValue for
+    non-finite stacks; stacks whose k sat on a log2 rounding boundary are
+    redone with the host's k (never for real data)."""
     import torch
 
     if not stats:
         return
-    r = decode_results(torch.cat([t for t in stats]))
+    r = decode_results(torch.cat([t for t in stats])).copy()
+    mode = "roundtrip" if roundtrip else "forward"
+    for i in np.nonzero(r["flags"] & 4)[0]:
+        # a stack the folded pipeline could not settle: statistics kernels + standard passes
+        # from the host copy; its full row then goes through the checks below
+        sl = slice(int(i) * coils, (int(i) + 1) * coils)
+        xd = x_host[sl].cuda()
+        y, _, rs = pipeline_device(xd, plan, cfg, roundtrip, coils=coils, fused=False, fold=False)
+        r[i] = decode_results(rs)[0]
+        if not int(r["flags"][i]) & 1:
+            out_host[sl].copy_(y.cpu())
     bad = np.nonzero(r["flags"] & 1)[0]
     if bad.size:
         raise InvalidValue(f"non-finite input to prescale (stacks {bad[:8].tolist()})")
@@ -336,7 +347,7 @@ def _resolve_host(x_host, out_host, stats, plan, cfg, roundtrip, coils):
         sl = slice(int(i) * coils, (int(i) + 1) * coils)
         xd = x_host[sl].cuda()
         kd = torch.tensor([kh], dtype=torch.int32, device=xd.device)
-        y = fft2_device(xd, plan, "roundtrip" if roundtrip else "forward", k=kd, k_group=coils)
+        y = fft2_device(xd, plan, mode, k=kd, k_group=coils)
         out_host[sl].copy_(y.cpu())
 
 

@@ -171,3 +171,29 @@ def test_fold_custom_config_where_k2_wins(mx, torch):
     assert (_rows(mx, r1)["flags"] == 4).all()
     assert mx.pipeline_resolve(x, y1, k1, r1, p, cfg, True) == 4
     assert torch.equal(k0, k1) and _same(torch, y0, y1)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_fold_pipeline_host_resolves_unsettled_stacks(mx, torch, graph):
+    """pipeline_host (H2D / folded pipeline / D2H slices): a stack the fold
+    flags is redone from the host copy; the result equals the statistics-kernel
+    path on every stack; non-finite input still raises"""
+    from paper_2512_04317_b200.workloads import ellipse_kspace_batch
+
+    n = 128
+    xh = ellipse_kspace_batch(20, n, seed=21, noise=0.05)
+    xh[3, :40, :] = 1e-9 * (1 + 1j)   # k2 > k1: unsettled by the fold
+    xh[11] *= np.float32(1e-30)       # exponents outside the proven range
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.E4M3, 32))
+    cfg = mx.PrescaleConfig()
+    want, kw, rw = mx.pipeline_device(torch.from_numpy(xh).cuda(), p, cfg, True, fold=False, fused=False)
+    assert mx.pipeline_resolve(torch.from_numpy(xh).cuda(), want, kw, rw, p, cfg, True) == 0
+    h = torch.from_numpy(xh).pin_memory()
+    out = torch.empty(h.shape, dtype=h.dtype).pin_memory()
+    for _ in range(2):  # (graph=True: capture, then replay)
+        out.zero_()
+        got = mx.pipeline_host(h, p, cfg, True, out_host=out, chunks=3, graph=graph)
+        assert _same(torch, got, want.cpu())
+    xh[5, 0, 0] = np.inf
+    with pytest.raises(mx.InvalidValue):
+        mx.pipeline_host(torch.from_numpy(xh).pin_memory(), p, cfg, True, chunks=3, graph=graph)
