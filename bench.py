@@ -537,6 +537,29 @@ def measure_c5(ctx, c, steps, warmup, e2e=False, cpu_seconds=0.0):
         return D.fft2_slab(xin, plan, "roundtrip" if roundtrip else "forward", comm, k=res.k, restore=False)
 
     pts = n * n
+    # 1 GPU: the global prescale can also ride on the first row pass (mxfft_pipeline_folded: no
+    # statistics pass over x, no host synchronisation); both variants are timed, the faster one
+    # is the measured configuration
+    alt, unsettled = None, None
+    step_std = step
+    if world == 1 and mx.mri.folded_pipeline_supported(plan):
+        rbuf = torch.empty((1, 40), dtype=torch.uint8, device="cuda")
+
+        def step_fold(roundtrip=True, xin=None):
+            xin = x if xin is None else xin
+            return mx.pipeline_device(xin[None], plan, cfg, roundtrip, out=y[None], k=kt, res=rbuf)[0][0]
+
+        t = {"global_statistics_then_fft2": ctx.timed(step_std, max(2, steps // 2), 2),
+             "statistics_folded_into_first_row_pass": ctx.timed(step_fold, max(2, steps // 2), 2)}
+        from paper_2512_04317_b200.prescale import decode_results
+
+        unsettled = int((decode_results(rbuf)["flags"] & 4 != 0).sum())
+        best = min(t, key=t.get)
+        if unsettled:  # (not for this workload: the fold then needs the resolve's re-run)
+            best = "global_statistics_then_fft2"
+        if best != "global_statistics_then_fft2":
+            step = step_fold
+        alt = {"ms_per_step": t, "chosen": best, "value": {v: pts / (m_ * 1e-3) / 1e9 for v, m_ in t.items()}}
     for _ in range(warmup):
         step()
     l0 = _native.launch_count()
@@ -564,6 +587,8 @@ def measure_c5(ctx, c, steps, warmup, e2e=False, cpu_seconds=0.0):
         "clocks": clk.summary(),
         "config": describe("c5", c, world),
         "exchange": None if world == 1 else "3 all-to-alls per round trip (output left as column slabs)",
+        "implementations": alt,
+        "unsettled_stacks": unsettled,
         "parity": "tests/test_gpu_r2.py::test_c5_full_size_roundtrip_vs_oracle (16384^2 forward and round "
                   "trip bit-exact vs the threaded oracle; exact global prescale)",
     }

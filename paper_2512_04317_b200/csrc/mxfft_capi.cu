@@ -620,18 +620,23 @@ int32_t mxfft_pipeline_fused(mxfft_plan plan, const void* x, void* y, int64_t ni
     return MXFFT_OK;
 }
 
-// ---- statistics folded into the first pass (n = 128 / 256 / 512 on the TMA line kernel) ----
-static bool fold_ok(const Plan& p) {
+// ---- statistics folded into the first pass (n = 128 / 256 / 512 on the TMA line kernel;
+// n = 16384 on the split passes' half-row kernel) ----
+static bool fold_ok_tma(const Plan& p) {
     return mxfft::g_tma_store && mx_lines_ok(p) && p.cpb >= 8 && p.log2n >= 7 && p.log2n <= 9;
 }
+static bool fold_ok_split(const Plan& p) {
+    return p.half && mxfft::g_split_last_stage && mx_lines_ok(p) && p.cpb >= 8 && p.log2n == 14;
+}
+static bool fold_ok(const Plan& p) { return fold_ok_tma(p) || fold_ok_split(p); }
 int32_t mxfft_pipeline_folded_supported(mxfft_plan plan) { return plan && fold_ok(plan->p) ? 1 : 0; }
 
 int64_t mxfft_pipeline_folded_workspace_bytes(mxfft_plan plan, int64_t nimg, int32_t coils) {
     if (!plan || nimg <= 0 || coils < 1 || !fold_ok(plan->p)) return 0;
-    const int64_t nstack = nimg / coils;
-    const int64_t nn = (int64_t)plan->p.n * plan->p.n;
-    (void)nstack;
-    return nimg * nn * 8 + nimg * nn / 512 * 4 + nimg * nn / 32 * 4;  // scratch image + warp words + thread words
+    const int64_t nn = (int64_t)plan->p.n * plan->p.n, nstack = nimg / coils;
+    const int64_t copies = fold_ok_split(plan->p) ? 2 : 1;
+    // scratch image(s) + warp words + thread words + the big-stack reduction scratch
+    return copies * nimg * nn * 8 + nimg * nn / 512 * 4 + nimg * nn / 32 * 4 + ((nstack * 32 + 255) / 256) * 256;
 }
 
 int32_t mxfft_pipeline_folded(mxfft_plan plan, const void* x, void* y, int64_t nimg, int32_t coils,
@@ -643,7 +648,7 @@ int32_t mxfft_pipeline_folded(mxfft_plan plan, const void* x, void* y, int64_t n
     if (nimg == 0) return MXFFT_OK;
     const Plan& p = plan->p;
     if (!fold_ok(p))
-        return fail(MXFFT_ERR_UNSUPPORTED_SIZE, "the folded pipeline needs n in {128, 256, 512}, a hardware MX format and B in {16, 32, 64}");
+        return fail(MXFFT_ERR_UNSUPPORTED_SIZE, "the folded pipeline needs n in {128, 256, 512, 16384}, a hardware MX format and B in {16, 32, 64}");
     if (!d_res || !d_k) return fail(MXFFT_ERR_VALUE, "null result rows / k vector");
     if (x == y) return fail(MXFFT_ERR_VALUE, "the folded pipeline is out of place (flagged stacks are re-run from the input)");
     if (!workspace || workspace_bytes < mxfft_pipeline_folded_workspace_bytes(plan, nimg, coils))
@@ -652,9 +657,53 @@ int32_t mxfft_pipeline_folded(mxfft_plan plan, const void* x, void* y, int64_t n
         return fail(MXFFT_ERR_VALUE, "the folded pipeline needs 16-byte aligned buffers");
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t nn = (int64_t)p.n * p.n, nstack = nimg / coils;
-    unsigned* acc = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(workspace) + nimg * nn * 8);
+    if ((int64_t)coils * nn >= (int64_t(1) << 32)) return fail(MXFFT_ERR_UNSUPPORTED_SIZE, "coil stack too large");
+    const bool split = fold_ok_split(p);
+    unsigned* acc = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(workspace) + (split ? 2 : 1) * nimg * nn * 8);
     unsigned* minw = acc + nimg * nn / 512;
+    unsigned* scratch = minw + nimg * nn / 32;
     const int npass = roundtrip ? 4 : 2;
+    if (split) {
+        // n = 16384: every pass = the 8192-point line kernel on the decimated half rows (the first
+        // one with the evidence) + the last stage fused into the transposed store (see mxfft_fft2)
+        float2* w1 = reinterpret_cast<float2*>(workspace);
+        float2* w2 = w1 + nimg * nn;
+        for (int pass = 0; pass < npass; ++pass) {
+            const bool inv = roundtrip && pass >= 2;
+            const bool last = pass == npass - 1;
+            LinePass lp;
+            lp.in = pass == 0 ? x : (const void*)w1;
+            lp.out = w2;
+            lp.dec = 1;
+            lp.lines_per_image = 2 * p.n;
+            lp.total_lines = nimg * 2 * (int64_t)p.n;
+            lp.img_elems = nn;
+            lp.inverse = inv;
+            lp.k_group = coils;
+            if (pass == 0) {
+                lp.acc = acc;
+                lp.minw = minw;
+            }
+            // (x 2^k happens at the load of the first pass's last-stage kernel, once k is known:
+            // stages 0 .. 12 of the first row pass are the unscaled, range-tracked ones)
+            CK(run_mx_lines(*p.half, lp, s), "pipeline_folded (half rows)");
+            if (pass == 0)
+                CK(launch_fold_resolve(acc, minw, nstack, coils * nn, *cfg, d_res, d_k, scratch, s),
+                   "pipeline_folded (resolve)");
+            LastStagePass ls;
+            ls.in = w2;
+            ls.out = last ? y : (void*)w1;
+            ls.batch = nimg;
+            ls.inverse = inv;
+            ls.kvec = d_k;
+            ls.k_group = coils;
+            ls.kin_sign = pass == 0 ? 1 : 0;
+            ls.kout_sign = last ? -1 : 0;
+            ls.kout_const = last && roundtrip ? -2 * p.log2n : 0;
+            CK(run_last_stage_transpose(p, ls, s), "pipeline_folded (last stage + transpose)");
+        }
+        return MXFFT_OK;
+    }
     for (int pass = 0; pass < npass; ++pass) {
         LinePass lp;
         lp.in = pass == 0 ? x : ((pass & 1) ? workspace : y);
@@ -669,7 +718,7 @@ int32_t mxfft_pipeline_folded(mxfft_plan plan, const void* x, void* y, int64_t n
         lp.kvec = d_k;
         lp.k_group = coils;
         if (pass == 0) {
-            lp.kvec = nullptr;  // unscaled; the pass accumulates the statistics
+            lp.kvec = nullptr;  // unscaled; the pass gathers the evidence
             lp.acc = acc;
             lp.minw = minw;
         }
@@ -680,7 +729,8 @@ int32_t mxfft_pipeline_folded(mxfft_plan plan, const void* x, void* y, int64_t n
         }
         CK(run_mx_lines(p, lp, s), "pipeline_folded");
         if (pass == 0)
-            CK(launch_fold_resolve(acc, minw, nstack, coils * nn, *cfg, d_res, d_k, s), "pipeline_folded (resolve)");
+            CK(launch_fold_resolve(acc, minw, nstack, coils * nn, *cfg, d_res, d_k, scratch, s),
+               "pipeline_folded (resolve)");
     }
     return MXFFT_OK;
 }

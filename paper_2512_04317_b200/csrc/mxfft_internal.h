@@ -41,6 +41,7 @@ struct LastStagePass {
     int inverse;
     const int32_t* kvec;
     int k_group, kout_sign, kout_const;
+    int kin_sign = 0;  // x 2^(kin_sign k) on load (the folded pipeline's first pass)
 };
 bool last_stage_ok(const Plan& p);
 cudaError_t run_last_stage_transpose(const Plan& p, const LastStagePass& lp, cudaStream_t st);
@@ -170,7 +171,7 @@ cudaError_t launch_prescale_count_range(const float2* x, int64_t npts, float lo,
                                         int64_t topcap, cudaStream_t st);
 cudaError_t launch_fold_resolve(const unsigned* acc, const unsigned* minw, int64_t nstack, int64_t stack_points,
                                 const mxfft_prescale_cfg& c, mxfft_prescale_result* out, int32_t* kvec,
-                                cudaStream_t st);
+                                unsigned* scratch, cudaStream_t st);
 cudaError_t launch_rss(const void* x, int is_c128, int64_t groups, int coils, int64_t npix,
                        double* out, cudaStream_t st, const int32_t* kvec = nullptr, int ksign = 0,
                        int econst = 0);

@@ -36,7 +36,7 @@ struct LastArgs {
     const unsigned* tw16;
     const signed char* twe;
     const int32_t* kvec;
-    int k_group, kout_sign, kout_const;
+    int k_group, kout_sign, kout_const, kin_sign;
 };
 
 constexpr int LS_R = 32, LS_C = 64;  // tile rows x butterflies
@@ -83,8 +83,20 @@ __global__ void __launch_bounds__(256, MXFFT_LS_MINB) k_last_stage_t(LastArgs a)
             }
             const int ew = __ldg(a.twe + hn + j);
             bool bad = false;
-            mxb<ID, 8, G, false, true>(u, v, wc, ew, nullptr, 0, bad);
             const int kk = a.kvec ? __ldg(a.kvec + b / a.k_group) : 0;
+            const int kin = a.kin_sign * kk;  // (the folded pipeline scales here: stages 0 .. L-2 ran unscaled)
+            if (kin) {
+                if (kin >= -126 && kin <= 127) {
+                    const float f = exp2i(kin);
+                    const float2 f2 = make_float2(f, f);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) u[i] = __fmul2_rn(u[i], f2), v[i] = __fmul2_rn(v[i], f2);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) u[i] = gscale(u[i], kin), v[i] = gscale(v[i], kin);
+                }
+            }
+            mxb<ID, 8, G, false, true>(u, v, wc, ew, nullptr, 0, bad);
             const int kout = a.kout_sign * kk + a.kout_const;
             if (kout) {
                 if (kout >= -126 && kout <= 127) {
@@ -152,6 +164,7 @@ cudaError_t run_last_stage_transpose(const Plan& p, const LastStagePass& lp, cud
     a.k_group = lp.k_group > 0 ? lp.k_group : 1;
     a.kout_sign = lp.kout_sign;
     a.kout_const = lp.kout_const;
+    a.kin_sign = lp.kin_sign;
     if (lp.batch <= 0) return cudaSuccess;
     switch (p.fmt.id) {
         case F_E4M3: return launch_ls<F_E4M3>(a, p.cpb, st);

@@ -208,7 +208,7 @@ cudaError_t run_mx_lines(const Plan& p, const LinePass& lp, cudaStream_t st) {
     a.acc = lp.acc;
     a.minw = lp.minw;
     if (a.acc) {  // statistics-folding first pass: the TMA kernel only (mxfft_pipeline_folded checks first)
-        if (!a.tma_out || !a.minw || a.kin_sign || a.kin_const || a.reverse) return cudaErrorInvalidValue;
+        if (!a.minw || a.kin_sign || a.kin_const || a.reverse || dbg) return cudaErrorInvalidValue;
         switch (p.fmt.id) {
             case F_E4M3: return run_mx_lines_acc_e4m3(a, p.cpb, smem, st);
             case F_E5M2: return run_mx_lines_acc_e5m2(a, p.cpb, smem, st);

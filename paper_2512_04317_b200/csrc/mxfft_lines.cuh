@@ -1252,6 +1252,46 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
 }
 
 // ---------------------------------------------------------------------------
+// Evidence for compute_prescale gathered by a first pass on the unscaled input
+// (mxfft_pipeline_folded; see lines_body_tma below for the word formats).
+// `grp` is the CTA's group (TMA kernel) or line (one-line-per-CTA kernel): its
+// threads each hold 32 points, so thread words sit at grp * blockDim + tid and
+// warp words at 2 (grp * warps + warp).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void fold_points(const float2 (&x)[32], const MxLinesArgs& a, int64_t grp) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    unsigned acc_key = 0, mn_all = 0xffffffffu;
+#pragma unroll
+    for (int m = 0; m < 32; ++m) {
+        const float re = x[m].x, im = x[m].y;
+        acc_key = max(acc_key, __float_as_uint(fmaf(re, re, im * im)));  // NaN / inf compare largest
+        mn_all = min(mn_all, __float_as_uint(fmaxf(fabsf(re), fabsf(im))));
+    }
+    unsigned zeros = 0, nzb = mn_all;
+    if (__builtin_expect(mn_all == 0u, 0)) {  // the thread holds zero points: count them, skip them
+        unsigned acc_min = 0xffffffffu;
+#pragma unroll
+        for (int m = 0; m < 32; ++m) {
+            const unsigned ub = __float_as_uint(fmaxf(fabsf(x[m].x), fabsf(x[m].y)));
+            zeros += ub == 0u;
+            acc_min = min(acc_min, ub - 1u);  // zero -> 2^32 - 1
+        }
+        nzb = acc_min + 1u;  // 0: every point is zero
+    }
+    a.minw[grp * nt + tid] = (nzb ? (nzb & ~63u) : 0xffffffc0u) | zeros;
+    acc_key = __reduce_max_sync(0xffffffffu, acc_key);
+    if ((tid & 31) == 0) a.acc[(grp * (nt >> 5) + (tid >> 5)) * 2] = acc_key;
+}
+__device__ __forceinline__ void fold_range(const BadTrack& bad, const MxLinesArgs& a, int64_t grp) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int hi_ = __reduce_max_sync(0xffffffffu, bad.hi), lo_ = __reduce_min_sync(0xffffffffu, bad.lo);
+    const unsigned b_ = __ballot_sync(0xffffffffu, bad.b);
+    if ((tid & 31) == 0)
+        a.acc[(grp * (nt >> 5) + (tid >> 5)) * 2 + 1] =
+            ((unsigned)(128 + hi_) << 16) | ((unsigned)(128 - lo_) << 4) | (b_ ? 1u : 0u);
+}
+
+// ---------------------------------------------------------------------------
 // n = 256 / 512 row passes stored transposed (the two passes of mxfft_fft2):
 // the group leaves with ONE TMA tensor store (make_out_map, mxfft_lines.cu).
 // Two 32 KB buffers with fixed roles: X receives the group tiles (cp.async,
@@ -1364,29 +1404,7 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
             const unsigned ad = (gaddr ^ ((unsigned)(m & (MS - 1)) * (T * 8u))) + (unsigned)(m / MS) * (LPC * 128u);
             x[rev_c<5>(m)] = lds64(ad);
         }
-        if constexpr (ACC) {
-            unsigned acc_key = 0, mn_all = 0xffffffffu;
-#pragma unroll
-            for (int m = 0; m < 32; ++m) {
-                const float re = x[m].x, im = x[m].y;
-                acc_key = max(acc_key, __float_as_uint(fmaf(re, re, im * im)));  // NaN / inf compare largest
-                mn_all = min(mn_all, __float_as_uint(fmaxf(fabsf(re), fabsf(im))));
-            }
-            unsigned zeros = 0, nzb = mn_all;
-            if (__builtin_expect(mn_all == 0u, 0)) {  // the thread holds zero points: count them, skip them
-                unsigned acc_min = 0xffffffffu;
-#pragma unroll
-                for (int m = 0; m < 32; ++m) {
-                    const unsigned ub = __float_as_uint(fmaxf(fabsf(x[m].x), fabsf(x[m].y)));
-                    zeros += ub == 0u;
-                    acc_min = min(acc_min, ub - 1u);  // zero -> 2^32 - 1
-                }
-                nzb = acc_min + 1u;  // 0: every point is zero
-            }
-            a.minw[grp * NT + tid] = (nzb ? (nzb & ~63u) : 0xffffffc0u) | zeros;
-            acc_key = __reduce_max_sync(0xffffffffu, acc_key);
-            if (lane == 0) a.acc[(grp * (NT / 32) + (tid >> 5)) * 2] = acc_key;
-        }
+        if constexpr (ACC) fold_points(x, a, grp);
         if (nxt < ngroups) kk_nxt = k_of(nxt);
         // n <= 256: split barriers instead of one __syncthreads.  Only warp 0 waits for every
         // warp's gather (barrier 1: X is in registers, free for the next tile) before thread 0
@@ -1418,13 +1436,7 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
         run_stages<ID, CPB, false, LT>(x, U, V, P, H, L, by, ebase, &dbg, bad, y_free);
         if (kout) scale32<false>(x, kout, bad);
         const int64_t gl = grp * LPC;  // first line of the group: column gl mod n of image gl / n
-        if constexpr (ACC) {
-            const int hi_ = __reduce_max_sync(0xffffffffu, bad.hi), lo_ = __reduce_min_sync(0xffffffffu, bad.lo);
-            const unsigned b_ = __ballot_sync(0xffffffffu, bad.b);
-            if (lane == 0)
-                a.acc[(grp * (NT / 32) + (tid >> 5)) * 2 + 1] =
-                    ((unsigned)(128 + hi_) << 16) | ((unsigned)(128 - lo_) << 4) | (b_ ? 1u : 0u);
-        }
+        if constexpr (ACC) fold_range(bad, a, grp);
         if (__syncthreads_or(bad)) {
             replay_lines(a, gl, LPC, y_g, 5 - LT, W * 32, LPR - 1);
             float2* dst = a.out + (gl >> LN) * (int64_t)N * N + (gl & (N - 1));
@@ -1454,7 +1466,7 @@ __global__ void __launch_bounds__(128, MXFFT_LINES_MINB) k_mx_lines_tma(const __
 // Lines of n = 8192/16384 (T = 256/512; one line per CTA): direct loads from
 // HBM (whole sectors per warp), no prefetch (a second 128 KB buffer would not
 // fit next to the twiddle table).
-template <int ID, int CPB, bool DBG, int LT>
+template <int ID, int CPB, bool DBG, int LT, bool ACC = false>
 __device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
     const int lt = LT >= 0 ? LT : a.log2T;
     const int T = 1 << lt, N = 32 * T;
@@ -1510,7 +1522,7 @@ __device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
         const int kout = a.kout_sign * kk + a.kout_const;
         if (DBG) dbg.row = line;
         float2 x[32];
-        bool bad = false;
+        typename std::conditional<ACC, BadTrack, bool>::type bad{};
         if (a.seg_log2 && !a.col_mode) {  // segmented rows: element m T + rcol of the line
 #pragma unroll
             for (int m = 0; m < 32; ++m) x[rev_c<5>(m)] = __ldg(a.in + seg_off(a, line, m * T + rcol));
@@ -1522,6 +1534,7 @@ __device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
             for (int m = 0; m < 32; ++m) x[rev_c<5>(m)] = __ldg(src + m * stride);
             if (kin) scale32<DBG>(x, kin, bad);
         }
+        if constexpr (ACC) fold_points(x, a, grp);  // (the folded first pass runs unscaled: kin == 0)
 #if MXFFT_BIG_PREFETCH
         // while this line computes, its successor (a contiguous row) streams into
         // L2, so the next load phase hits L2 instead of waiting on HBM
@@ -1541,6 +1554,7 @@ __device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
         int U, V, P, H;
         run_stages<ID, CPB, DBG, LT>(x, U, V, P, H, L, rb, ebase, &dbg, bad);
         if (kout) scale32<DBG>(x, kout, bad);
+        if constexpr (ACC) fold_range(bad, a, grp);
         if (!DBG && __syncthreads_or(bad)) {
             char* tile = reinterpret_cast<char*>(smem4 + a.tw_chunks);
             replay_lines(a, line, 1, tile, 0, N, 0);
@@ -1774,9 +1788,9 @@ __global__ void __launch_bounds__(128, MXFFT_LINES_MINB) k_mx_lines(const __grid
     lines_body_pipe<ID, CPB, DBG, LT>(a);
 }
 
-template <int ID, int CPB, bool DBG, int LT>
+template <int ID, int CPB, bool DBG, int LT, bool ACC = false>
 __global__ void __launch_bounds__(512, 1) k_mx_lines_big(const __grid_constant__ MxLinesArgs a) {
-    lines_body_direct<ID, CPB, DBG, LT>(a);
+    lines_body_direct<ID, CPB, DBG, LT, ACC>(a);
 }
 
 // ---------------------------------------------------------------------------
@@ -1905,10 +1919,33 @@ static cudaError_t disp_lt(const MxLinesArgs& a, size_t smem, cudaStream_t st) {
     }
 }
 
-// statistics-folding first pass (TMA kernel only; instantiated in lines_acc_<fmt>.cu)
+// the 8192-point decimated half rows of an n = 16384 split pass, with the prescale evidence
+template <int ID, int CPB>
+static cudaError_t launch_big_acc(const MxLinesArgs& a, size_t smem, cudaStream_t st) {
+    void (*k)(MxLinesArgs) = k_mx_lines_big<ID, CPB, false, 8, true>;
+    cudaError_t e = ensure_smem_attr((const void*)k, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    const int sms = device_attr(cudaDevAttrMultiProcessorCount);
+    int occ = 1;
+    e = cached_occupancy((const void*)k, 256, smem, &occ);
+    if (e != cudaSuccess) return e;
+    const int64_t cap = (int64_t)sms * occ;
+    k<<<(unsigned)(a.total_lines < cap ? a.total_lines : cap), 256, smem, st>>>(a);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// statistics-folding first pass (the TMA kernel, or the 8192-point half rows; instantiated in lines_acc_<fmt>.cu)
 template <int ID>
 static cudaError_t disp_acc(const MxLinesArgs& a, int cpb, size_t smem, cudaStream_t st) {
-    if (!a.tma_out || !a.acc) return cudaErrorInvalidValue;
+    if (!a.acc || !a.minw) return cudaErrorInvalidValue;
+    if (a.log2T == 8 && a.dec && !a.col_mode && !a.tstore && a.stage_limit >= a.log2n) {
+        if (cpb == 8) return launch_big_acc<ID, 8>(a, smem, st);
+        if (cpb == 16) return launch_big_acc<ID, 16>(a, smem, st);
+        if (cpb == 32) return launch_big_acc<ID, 32>(a, smem, st);
+        return cudaErrorInvalidValue;
+    }
+    if (!a.tma_out) return cudaErrorInvalidValue;
 #define MXFFT_ACC_CASE(C, L) \
     if (cpb == C && a.log2T == L) return launch_tma<ID, C, L, true>(a, smem, st);
     MXFFT_ACC_CASE(8, 2) MXFFT_ACC_CASE(8, 3) MXFFT_ACC_CASE(8, 4)

@@ -1371,6 +1371,54 @@ cudaError_t launch_prescale_fast(const float2* x, int64_t nseg, int64_t npts, do
 // standard passes.  Settled rows carry flags = 8 (a_max approximate, p_tau and
 // k2 not evaluated, nnz exact).
 // ---------------------------------------------------------------------------
+// the decision, from the reduced evidence (one thread)
+__device__ void fold_finish(unsigned kmx, unsigned hi_u, unsigned lo_u, unsigned rep, unsigned long long zeros,
+                            unsigned long long small, unsigned mn, double a_est, int k1, int e_key, bool k1_ok,
+                            int64_t stack_points, const mxfft_prescale_cfg& c, mxfft_prescale_result* out,
+                            int32_t* kvec, int64_t s) {
+    const int hi = (int)hi_u - 128, lo = 128 - (int)lo_u;
+    const bool replayed = rep != 0;
+    const unsigned long long nnz = (unsigned long long)stack_points - zeros;
+    if (kmx < 0x7f800000u && nnz == 0 && !replayed) {  // an all-zero stack: the reference's own formula
+        finish_result(c, 0.0, 0.0, 0ull, out, kvec, (int)s);
+        return;
+    }
+    mxfft_prescale_result r;
+    r.a_max = r.p_tau = __longlong_as_double(0x7ff8000000000000ll);
+    r.k1 = r.k2 = r.k = 0;
+    r.flags = 4;
+    r.nnz = (int64_t)nnz;
+    if (k1_ok && nnz > 0) {
+        const double virt = __dmul_rn((double)(nnz - 1), c.tau / 100.0);
+        const unsigned long long r_lo = virt >= (double)(nnz - 1) ? nnz - 1 : (unsigned long long)floor(virt);
+        const int k = min(max(k1, c.k_min), c.k_max);
+        const int e_mu = (int)(mn >> 23) - 127;  // (mn: a lower bound of the smallest nonzero max(|re|, |im|))
+        const bool ok = 32ull * small <= r_lo && !replayed && k >= -100 && k <= 100 && lo >= -90 && hi <= 90 &&
+                        lo + k >= -90 && hi + k <= 90 && e_mu >= -100 && e_mu + k >= -100 && e_key / 2 + k <= 100;
+        if (ok) {
+            r.a_max = a_est;
+            r.k1 = k1;
+            r.k2 = INT_MIN;
+            r.k = k;
+            r.flags = 8;
+        }
+    }
+    out[s] = r;
+    kvec[s] = r.k;
+}
+// k1 and the threshold T from the largest key (FP64, one thread)
+__device__ void fold_k1(unsigned kmx, const mxfft_prescale_cfg& c, double& a_est, int& k1, int& e_key, bool& k1_ok,
+                        float& T) {
+    a_est = sqrt((double)__uint_as_float(kmx));
+    const double L1 = log2(c.target / fmax(a_est, 1e-30));
+    const double d1 = fabs(fabs(L1 - trunc(L1)) - 0.5);
+    k1 = round_half_away_d(L1);
+    e_key = (int)(kmx >> 23) - 127;
+    k1_ok = kmx < 0x7f800000u && e_key >= -100 && d1 > 1e-6 && k1 > -200 && k1 < 200;
+    // rounded up (and with a margin for the reference's log2 rounding): the count below can only grow
+    T = k1_ok ? __double2float_ru(ldexp(c.tau_min, -k1) * (1.0 + 0x1p-20)) : 0.f;
+}
+
 template <int FR_THREADS>
 __global__ void __launch_bounds__(FR_THREADS) k_fold_resolve(const unsigned* __restrict__ acc,
                                                              const unsigned* __restrict__ minw, int64_t stack_points,
@@ -1425,14 +1473,9 @@ __global__ void __launch_bounds__(FR_THREADS) k_fold_resolve(const unsigned* __r
             lo_u = max(lo_u, sc[i]);
             rep |= sd[i];
         }
-        a_est = sqrt((double)__uint_as_float(kmx));
-        const double L1 = log2(c.target / fmax(a_est, 1e-30));
-        const double d1 = fabs(fabs(L1 - trunc(L1)) - 0.5);
-        k1 = round_half_away_d(L1);
-        e_key = (int)(kmx >> 23) - 127;
-        k1_ok = kmx < 0x7f800000u && e_key >= -100 && d1 > 1e-6 && k1 > -200 && k1 < 200;
-        // rounded up (and with a margin for the reference's log2 rounding): the count below can only grow
-        s_T = k1_ok ? __double2float_ru(ldexp(c.tau_min, -k1) * (1.0 + 0x1p-20)) : 0.f;
+        float Tt;
+        fold_k1(kmx, c, a_est, k1, e_key, k1_ok, Tt);
+        s_T = Tt;
     }
     __syncthreads();
     const float T = s_T;
@@ -1471,40 +1514,103 @@ __global__ void __launch_bounds__(FR_THREADS) k_fold_resolve(const unsigned* __r
         small += sb[i];
         mn = min(mn, sc[i]);
     }
-    const int hi = (int)hi_u - 128, lo = 128 - (int)lo_u;
-    const bool replayed = rep != 0;
-    const unsigned long long nnz = (unsigned long long)stack_points - zeros;
-    if (kmx < 0x7f800000u && nnz == 0 && !replayed) {  // an all-zero stack: the reference's own formula
-        finish_result(c, 0.0, 0.0, 0ull, out, kvec, (int)s);
-        return;
+    fold_finish(kmx, hi_u, lo_u, rep, zeros, small, mn, a_est, k1, e_key, k1_ok, stack_points, c, out, kvec, s);
+}
+
+// One stack too large for one CTA (C5: 2^28 points): the same decision in three grid-wide steps
+// on a per-stack scratch g (8 words, zeroed): [0] largest key, [1] 128 + hi, [2] 128 - lo,
+// [3] replay flag, [4] zeros, [5] threads below T, [6] ~(smallest word).
+__global__ void __launch_bounds__(256) k_fold_big_a(const unsigned* __restrict__ acc, int64_t stack_points,
+                                                    unsigned* g) {
+    const int64_t nw = stack_points / 1024;
+    const uint2* w = reinterpret_cast<const uint2*>(acc);
+    unsigned kmx = 0, hi_u = 0, lo_u = 0, rep = 0;
+    for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < nw; i += gridDim.x * 256ll) {
+        const uint2 v = __ldg(w + i);
+        kmx = max(kmx, v.x);
+        hi_u = max(hi_u, v.y >> 16);
+        lo_u = max(lo_u, (v.y >> 4) & 0xfffu);
+        rep |= v.y & 1u;
     }
-    mxfft_prescale_result r;
-    r.a_max = r.p_tau = __longlong_as_double(0x7ff8000000000000ll);
-    r.k1 = r.k2 = r.k = 0;
-    r.flags = 4;
-    r.nnz = (int64_t)nnz;
-    if (k1_ok && nnz > 0) {
-        const double virt = __dmul_rn((double)(nnz - 1), c.tau / 100.0);
-        const unsigned long long r_lo = virt >= (double)(nnz - 1) ? nnz - 1 : (unsigned long long)floor(virt);
-        const int k = min(max(k1, c.k_min), c.k_max);
-        const int e_mu = (int)(mn >> 23) - 127;  // (mn: a lower bound of the smallest nonzero max(|re|, |im|))
-        const bool ok = 32ull * small <= r_lo && !replayed && k >= -100 && k <= 100 && lo >= -90 && hi <= 90 &&
-                        lo + k >= -90 && hi + k <= 90 && e_mu >= -100 && e_mu + k >= -100 && e_key / 2 + k <= 100;
-        if (ok) {
-            r.a_max = a_est;
-            r.k1 = k1;
-            r.k2 = INT_MIN;
-            r.k = k;
-            r.flags = 8;
+    kmx = __reduce_max_sync(0xffffffffu, kmx);
+    hi_u = __reduce_max_sync(0xffffffffu, hi_u);
+    lo_u = __reduce_max_sync(0xffffffffu, lo_u);
+    rep = __reduce_or_sync(0xffffffffu, rep);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(g, kmx);
+        atomicMax(g + 1, hi_u);
+        atomicMax(g + 2, lo_u);
+        if (rep) atomicOr(g + 3, 1u);
+    }
+}
+__global__ void __launch_bounds__(256) k_fold_big_b(const unsigned* __restrict__ minw, int64_t stack_points,
+                                                    mxfft_prescale_cfg c, unsigned* g) {
+    __shared__ float s_T;
+    if (threadIdx.x == 0) {
+        double a_est;
+        int k1, e_key;
+        bool k1_ok;
+        float T;
+        fold_k1(g[0], c, a_est, k1, e_key, k1_ok, T);
+        s_T = T;
+    }
+    __syncthreads();
+    const float T = s_T;
+    const uint4* w4 = reinterpret_cast<const uint4*>(minw);
+    const int64_t n4 = stack_points / 128;
+    unsigned zeros = 0, small = 0, mn = 0xffffffffu;
+    auto take = [&](unsigned v) {
+        const unsigned mb = v & ~63u;
+        zeros += v & 63u;
+        if (mb != 0xffffffc0u) {
+            mn = min(mn, mb);
+            small += __uint_as_float(mb) < T;
         }
+    };
+    for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < n4; i += gridDim.x * 256ll) {
+        const uint4 v = __ldg(w4 + i);
+        take(v.x);
+        take(v.y);
+        take(v.z);
+        take(v.w);
     }
-    out[s] = r;
-    kvec[s] = r.k;
+    zeros = __reduce_add_sync(0xffffffffu, zeros);
+    small = __reduce_add_sync(0xffffffffu, small);
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(g + 4, zeros);  // (a stack has fewer than 2^32 points: mxfft_pipeline_folded checks)
+        atomicAdd(g + 5, small);
+        atomicMax(g + 6, ~mn);
+    }
+}
+__global__ void k_fold_big_c(const unsigned* g, int64_t stack_points, mxfft_prescale_cfg c,
+                             mxfft_prescale_result* out, int32_t* kvec, int64_t s) {
+    double a_est;
+    int k1, e_key;
+    bool k1_ok;
+    float T;
+    fold_k1(g[0], c, a_est, k1, e_key, k1_ok, T);
+    fold_finish(g[0], g[1], g[2], g[3], g[4], g[5], ~g[6], a_est, k1, e_key, k1_ok, stack_points, c, out, kvec, s);
 }
 
 cudaError_t launch_fold_resolve(const unsigned* acc, const unsigned* minw, int64_t nstack, int64_t stack_points,
                                 const mxfft_prescale_cfg& c, mxfft_prescale_result* out, int32_t* kvec,
-                                cudaStream_t st) {
+                                unsigned* scratch, cudaStream_t st) {
+    if (stack_points > (int64_t(1) << 22)) {  // few huge stacks: grid-wide reduction per stack
+        cudaError_t e = cudaMemsetAsync(scratch, 0, (size_t)nstack * 32, st);
+        if (e != cudaSuccess) return e;
+        const int sms = device_attr(cudaDevAttrMultiProcessorCount);
+        for (int64_t s = 0; s < nstack; ++s) {
+            unsigned* g = scratch + 8 * s;
+            k_fold_big_a<<<(unsigned)(2 * sms), 256, 0, st>>>(acc + s * (stack_points / 512), stack_points, g);
+            k_fold_big_b<<<(unsigned)(8 * sms), 256, 0, st>>>(minw + s * (stack_points / 32), stack_points, c, g);
+            k_fold_big_c<<<1, 1, 0, st>>>(g, stack_points, c, out, kvec, s);
+            note_launch();
+            note_launch();
+            note_launch();
+        }
+        return cudaGetLastError();
+    }
     static const int nt_env = getenv("MXFFT_FR_THREADS") ? atoi(getenv("MXFFT_FR_THREADS")) : 0;
     // few large stacks: more threads per stack
     // 128 threads: the CTAs then fit next to the first pass's (3 x 128 threads, ~150 registers) and the

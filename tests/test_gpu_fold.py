@@ -197,3 +197,31 @@ def test_fold_pipeline_host_resolves_unsettled_stacks(mx, torch, graph):
     xh[5, 0, 0] = np.inf
     with pytest.raises(mx.InvalidValue):
         mx.pipeline_host(torch.from_numpy(xh).pin_memory(), p, cfg, True, chunks=3, graph=graph)
+
+
+def test_fold_c5_full_size_equals_standard(mx, torch):
+    """C5: one 16384^2 image.  The folded pipeline (evidence gathered by the
+    8192-point half-row kernel of the first split pass, grid-wide resolve,
+    x 2^k at the load of that pass's last-stage kernel) equals the statistics
+    kernels + mxfft_fft2 bit for bit, forward and round trip, and equals the
+    exact global prescale's k."""
+    from paper_2512_04317_b200.workloads import ellipse_kspace_device
+
+    n = 16384
+    x = ellipse_kspace_device(n, 7, noise=0.01)[None]
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.E4M3, 32))
+    cfg = mx.PrescaleConfig()
+    assert mx.mri.folded_pipeline_supported(p)
+    kg = mx.compute_prescale_global(x[0], cfg).k
+    for roundtrip in (False, True):
+        y1, k1, r1 = mx.pipeline_device(x, p, cfg, roundtrip, fold=True)
+        row = _rows(mx, r1)[0]
+        assert int(row["flags"]) == 8 and int(k1[0]) == kg and int(row["nnz"]) == n * n
+        y0 = mx.fft2_device(x, p, "roundtrip" if roundtrip else "forward", k=k1)
+        assert _same(torch, y0, y1)
+        del y0, y1
+        torch.cuda.empty_cache()
+    # a quarter of the image tiny: k2 wins, the fold must decline
+    x[0, :4096] *= 1e-12
+    _, _, r2 = mx.pipeline_device(x, p, cfg, False, fold=True)
+    assert int(_rows(mx, r2)[0]["flags"]) == 4
