@@ -267,7 +267,8 @@ int32_t mxfft_pipeline_fused(mxfft_plan plan, const void* x, void* y, int64_t ni
 
 /* The pipelines with compute_prescale FOLDED INTO THE FIRST TRANSFORM PASS
  * (forward_pipeline / roundtrip_pipeline, mri.py:84-107; n = 128 / 256 / 512,
- * stacks of `coils` consecutive images share one prescale): no standalone
+ * and n = 16384 through the split passes; stacks of `coils` consecutive
+ * images share one prescale): no standalone
  * statistics read of x.  The first row pass runs on the unscaled input and
  * accumulates, per stack, the largest |x|^2, the smallest nonzero
  * max(|re|, |im|) and the range of the MX block exponents it produced; a small
