@@ -508,8 +508,10 @@ def measure_batch(ctx, name, c, steps, warmup, graph=True, e2e=False, cpu_second
 
 def measure_c5(ctx, c, steps, warmup, e2e=False, cpu_seconds=0.0):
     """C5: one n^2 image.  1 GPU: global prescale + fft2 (row passes and tiled
-    transposes).  N GPUs: row slabs, global prescale over all ranks,
-    all-to-all transposes (paper_2512_04317_b200/distributed.py)."""
+    transposes), or the prescale folded into the first split pass.  N GPUs:
+    row slabs, the global prescale folded into the first row pass (evidence
+    combined with two small all-reduces), all-to-all transposes
+    (paper_2512_04317_b200/distributed.py)."""
     import paper_2512_04317_b200 as mx
     from paper_2512_04317_b200 import _native, distributed as D
     from paper_2512_04317_b200.workloads import ellipse_kspace_device
@@ -529,12 +531,14 @@ def measure_c5(ctx, c, steps, warmup, e2e=False, cpu_seconds=0.0):
 
     def step(roundtrip=True, xin=None):
         xin = x if xin is None else xin
-        res = D.compute_prescale_global(xin, cfg, comm)
         if world == 1:
+            res = D.compute_prescale_global(xin, cfg, comm)
             kt.fill_(res.k)
             return mx.fft2_device(xin[None], plan, "roundtrip" if roundtrip else "forward", k=kt,
                                   out=y[None], workspace=ws)
-        return D.fft2_slab(xin, plan, "roundtrip" if roundtrip else "forward", comm, k=res.k, restore=False)
+        # N GPUs: the prescale rides on the first row pass of the slabs (two small all-reduces, one
+        # read-back of k); 3 all-to-alls per round trip, the result stays as column slabs
+        return D.pipeline_slab(xin, plan, cfg, roundtrip, comm, restore=False)[0]
 
     pts = n * n
     # 1 GPU: the global prescale can also ride on the first row pass (mxfft_pipeline_folded: no

@@ -292,6 +292,26 @@ int32_t mxfft_pipeline_folded(mxfft_plan plan, const void* x, void* y, int64_t n
                               int32_t roundtrip, const mxfft_prescale_cfg* cfg, mxfft_prescale_result* d_res,
                               int32_t* d_k, void* workspace, int64_t workspace_bytes, uintptr_t stream);
 
+/* The fold's building blocks for ONE image whose rows are split across ranks
+ * (compute_prescale over the whole image, prescale.py:61-73, SPEC.md:205;
+ * distributed.pipeline_slab combines them with two small all-reduces):
+ *  - fft_rows_evidence: the first row pass (fftcore.py:351) of this rank's
+ *    rows on the UNSCALED input (n = 16384), plus the evidence words of
+ *    mxfft_pipeline_folded in d_words (mxfft_fold_words_bytes(batch * n) bytes);
+ *  - fold_reduce, step 0: d_g (8 words) <- this rank's largest key, exponent
+ *    range and replay flag (g[0..3]; combine across ranks with MAX); step 1:
+ *    with the GLOBAL g[0] in place, g[4] += zero points, g[5] += threads below
+ *    the threshold (combine with SUM), g[6] = ~(smallest word) (MAX);
+ *  - fold_finish: k and the result row (flags 8 / 4 as mxfft_pipeline_folded)
+ *    from the combined g and the image's total point count. */
+int64_t mxfft_fold_words_bytes(int64_t npoints);
+int32_t mxfft_fft_rows_evidence(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t inverse,
+                                void* d_words, int64_t words_bytes, uintptr_t stream);
+int32_t mxfft_fold_reduce(const void* d_words, int64_t npoints, const mxfft_prescale_cfg* cfg, int32_t step,
+                          uint32_t* d_g, uintptr_t stream);
+int32_t mxfft_fold_finish(const uint32_t* d_g, int64_t total_points, const mxfft_prescale_cfg* cfg,
+                          mxfft_prescale_result* d_res, int32_t* d_k, uintptr_t stream);
+
 /* mxfft_rss with the pipelines' FP64 epilogue folded in: every coil value of
  * group g is multiplied by 2^(k_sign * d_k[g] + exp_const) in FP64 (exact)
  * before |.| -- the x 1/N^2 and undo_prescale of roundtrip_pipeline /

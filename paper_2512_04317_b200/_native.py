@@ -77,6 +77,10 @@ SIGNATURES = {
     "mxfft_pipeline_folded_workspace_bytes": ([_vp, _i64, _i32], _i64),
     "mxfft_pipeline_folded": ([_vp, _vp, _vp, _i64, _i32, _i32, ctypes.POINTER(PrescaleCfgC), _vp, _vp, _vp, _i64,
                                _u], _i32),
+    "mxfft_fold_words_bytes": ([_i64], _i64),
+    "mxfft_fft_rows_evidence": ([_vp, _vp, _vp, _i64, _i32, _vp, _i64, _u], _i32),
+    "mxfft_fold_reduce": ([_vp, _i64, ctypes.POINTER(PrescaleCfgC), _i32, _vp, _u], _i32),
+    "mxfft_fold_finish": ([_vp, _i64, ctypes.POINTER(PrescaleCfgC), _vp, _vp, _u], _i32),
     "mxfft_rss_scaled": ([_vp, _i32, _i64, _i32, _i64, _vp, _i32, _i32, _vp, _u], _i32),
     "mxfft_prescale_apply_c128": ([_vp, _vp, _i64, _i64, _vp, _u], _i32),
     "mxfft_mx_multiply_f64": ([_vp, _vp, _vp, _vp, _i64, _i32, _i32, _fp, _vp, _vp, _vp, _vp, _vp, _u], _i32),

@@ -735,6 +735,52 @@ int32_t mxfft_pipeline_folded(mxfft_plan plan, const void* x, void* y, int64_t n
     return MXFFT_OK;
 }
 
+// ---- the fold's building blocks for one image split across ranks (distributed.pipeline_slab) ----
+int64_t mxfft_fold_words_bytes(int64_t npoints) {
+    return npoints > 0 && npoints % 1024 == 0 ? npoints / 512 * 4 + npoints / 32 * 4 : 0;
+}
+
+int32_t mxfft_fft_rows_evidence(mxfft_plan plan, const void* x, void* y, int64_t batch, int32_t inverse,
+                                void* d_words, int64_t words_bytes, uintptr_t stream) {
+    CHECK_PLAN(plan);
+    const Plan& p = plan->p;
+    if (batch <= 0) return fail(MXFFT_ERR_SHAPE, "need at least one row");
+    if (!(mx_lines_ok(p) && p.cpb >= 8 && p.log2n == 14))
+        return fail(MXFFT_ERR_UNSUPPORTED_SIZE, "rows with evidence need n = 16384, a hardware MX format and B in {16, 32, 64}");
+    if (x == y) return fail(MXFFT_ERR_VALUE, "rows with evidence are out of place");
+    const int64_t npoints = batch * (int64_t)p.n;
+    if (!d_words || words_bytes < mxfft_fold_words_bytes(npoints)) return fail(MXFFT_ERR_VALUE, "evidence buffer too small");
+    LinePass lp;
+    lp.in = x;
+    lp.out = y;
+    lp.lines_per_image = 1;
+    lp.total_lines = batch;
+    lp.img_elems = p.n;
+    lp.inverse = inverse ? 1 : 0;
+    lp.acc = reinterpret_cast<unsigned*>(d_words);
+    lp.minw = lp.acc + npoints / 512;
+    CK(run_mx_lines(p, lp, (cudaStream_t)stream), "fft_rows_evidence");
+    return MXFFT_OK;
+}
+
+int32_t mxfft_fold_reduce(const void* d_words, int64_t npoints, const mxfft_prescale_cfg* cfg, int32_t step,
+                          uint32_t* d_g, uintptr_t stream) {
+    if (!cfg || !d_words || !d_g) return fail(MXFFT_ERR_VALUE, "null argument");
+    if (npoints <= 0 || npoints % 1024 || npoints >= (int64_t(1) << 32)) return fail(MXFFT_ERR_SHAPE, "bad point count");
+    if (step != 0 && step != 1) return fail(MXFFT_ERR_VALUE, "step must be 0 or 1");
+    const unsigned* acc = reinterpret_cast<const unsigned*>(d_words);
+    CK(launch_fold_reduce(acc, acc + npoints / 512, npoints, *cfg, step, d_g, (cudaStream_t)stream), "fold_reduce");
+    return MXFFT_OK;
+}
+
+int32_t mxfft_fold_finish(const uint32_t* d_g, int64_t total_points, const mxfft_prescale_cfg* cfg,
+                          mxfft_prescale_result* d_res, int32_t* d_k, uintptr_t stream) {
+    if (!cfg || !d_g || !d_res || !d_k) return fail(MXFFT_ERR_VALUE, "null argument");
+    if (total_points <= 0 || total_points >= (int64_t(1) << 32)) return fail(MXFFT_ERR_SHAPE, "bad point count");
+    CK(launch_fold_finish(d_g, total_points, *cfg, d_res, d_k, 0, (cudaStream_t)stream), "fold_finish");
+    return MXFFT_OK;
+}
+
 int32_t mxfft_rss_scaled(const void* x, int32_t is_c128, int64_t groups, int32_t coils, int64_t npix,
                          const int32_t* d_k, int32_t k_sign, int32_t exp_const, double* out, uintptr_t stream) {
     if (coils < 1) return fail(MXFFT_ERR_SHAPE, "need at least one coil");

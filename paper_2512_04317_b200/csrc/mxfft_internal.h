@@ -172,6 +172,10 @@ cudaError_t launch_prescale_count_range(const float2* x, int64_t npts, float lo,
 cudaError_t launch_fold_resolve(const unsigned* acc, const unsigned* minw, int64_t nstack, int64_t stack_points,
                                 const mxfft_prescale_cfg& c, mxfft_prescale_result* out, int32_t* kvec,
                                 unsigned* scratch, cudaStream_t st);
+cudaError_t launch_fold_reduce(const unsigned* acc, const unsigned* minw, int64_t npoints,
+                               const mxfft_prescale_cfg& c, int step, unsigned* g, cudaStream_t st);
+cudaError_t launch_fold_finish(const unsigned* g, int64_t total_points, const mxfft_prescale_cfg& c,
+                               mxfft_prescale_result* out, int32_t* kvec, int64_t s, cudaStream_t st);
 cudaError_t launch_rss(const void* x, int is_c128, int64_t groups, int coils, int64_t npix,
                        double* out, cudaStream_t st, const int32_t* kvec = nullptr, int ksign = 0,
                        int econst = 0);

@@ -1919,18 +1919,19 @@ static cudaError_t disp_lt(const MxLinesArgs& a, size_t smem, cudaStream_t st) {
     }
 }
 
-// the 8192-point decimated half rows of an n = 16384 split pass, with the prescale evidence
-template <int ID, int CPB>
+// one line per CTA with the prescale evidence: the 8192-point decimated half rows of an n = 16384
+// split pass (LT = 8) and plain n = 16384 rows (LT = 9, the slab passes of a distributed image)
+template <int ID, int CPB, int LT>
 static cudaError_t launch_big_acc(const MxLinesArgs& a, size_t smem, cudaStream_t st) {
-    void (*k)(MxLinesArgs) = k_mx_lines_big<ID, CPB, false, 8, true>;
+    void (*k)(MxLinesArgs) = k_mx_lines_big<ID, CPB, false, LT, true>;
     cudaError_t e = ensure_smem_attr((const void*)k, 227 * 1024);
     if (e != cudaSuccess) return e;
     const int sms = device_attr(cudaDevAttrMultiProcessorCount);
     int occ = 1;
-    e = cached_occupancy((const void*)k, 256, smem, &occ);
+    e = cached_occupancy((const void*)k, 1 << LT, smem, &occ);
     if (e != cudaSuccess) return e;
     const int64_t cap = (int64_t)sms * occ;
-    k<<<(unsigned)(a.total_lines < cap ? a.total_lines : cap), 256, smem, st>>>(a);
+    k<<<(unsigned)(a.total_lines < cap ? a.total_lines : cap), 1 << LT, smem, st>>>(a);
     note_launch();
     return cudaGetLastError();
 }
@@ -1940,9 +1941,15 @@ template <int ID>
 static cudaError_t disp_acc(const MxLinesArgs& a, int cpb, size_t smem, cudaStream_t st) {
     if (!a.acc || !a.minw) return cudaErrorInvalidValue;
     if (a.log2T == 8 && a.dec && !a.col_mode && !a.tstore && a.stage_limit >= a.log2n) {
-        if (cpb == 8) return launch_big_acc<ID, 8>(a, smem, st);
-        if (cpb == 16) return launch_big_acc<ID, 16>(a, smem, st);
-        if (cpb == 32) return launch_big_acc<ID, 32>(a, smem, st);
+        if (cpb == 8) return launch_big_acc<ID, 8, 8>(a, smem, st);
+        if (cpb == 16) return launch_big_acc<ID, 16, 8>(a, smem, st);
+        if (cpb == 32) return launch_big_acc<ID, 32, 8>(a, smem, st);
+        return cudaErrorInvalidValue;
+    }
+    if (a.log2T == 9 && !a.dec && !a.col_mode && !a.tstore && !a.seg_log2 && a.stage_limit >= a.log2n) {
+        if (cpb == 8) return launch_big_acc<ID, 8, 9>(a, smem, st);
+        if (cpb == 16) return launch_big_acc<ID, 16, 9>(a, smem, st);
+        if (cpb == 32) return launch_big_acc<ID, 32, 9>(a, smem, st);
         return cudaErrorInvalidValue;
     }
     if (!a.tma_out) return cudaErrorInvalidValue;

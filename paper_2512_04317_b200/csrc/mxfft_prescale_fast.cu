@@ -1593,21 +1593,42 @@ __global__ void k_fold_big_c(const unsigned* g, int64_t stack_points, mxfft_pres
     fold_finish(g[0], g[1], g[2], g[3], g[4], g[5], ~g[6], a_est, k1, e_key, k1_ok, stack_points, c, out, kvec, s);
 }
 
+// The grid-wide decision in steps (also the building blocks of a stack split across ranks: the
+// caller combines g between the steps -- MAX over g[0..3] after step 0, SUM over g[4..5] and MAX
+// over g[6] after step 1 -- mxfft_fold_reduce / mxfft_fold_finish)
+cudaError_t launch_fold_reduce(const unsigned* acc, const unsigned* minw, int64_t npoints,
+                               const mxfft_prescale_cfg& c, int step, unsigned* g, cudaStream_t st) {
+    const int sms = device_attr(cudaDevAttrMultiProcessorCount);
+    if (step == 0) {
+        cudaError_t e = cudaMemsetAsync(g, 0, 32, st);
+        if (e != cudaSuccess) return e;
+        k_fold_big_a<<<(unsigned)(2 * sms), 256, 0, st>>>(acc, npoints, g);
+    } else {
+        k_fold_big_b<<<(unsigned)(8 * sms), 256, 0, st>>>(minw, npoints, c, g);
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+cudaError_t launch_fold_finish(const unsigned* g, int64_t total_points, const mxfft_prescale_cfg& c,
+                               mxfft_prescale_result* out, int32_t* kvec, int64_t s, cudaStream_t st) {
+    k_fold_big_c<<<1, 1, 0, st>>>(g, total_points, c, out, kvec, s);
+    note_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_fold_resolve(const unsigned* acc, const unsigned* minw, int64_t nstack, int64_t stack_points,
                                 const mxfft_prescale_cfg& c, mxfft_prescale_result* out, int32_t* kvec,
                                 unsigned* scratch, cudaStream_t st) {
     if (stack_points > (int64_t(1) << 22)) {  // few huge stacks: grid-wide reduction per stack
-        cudaError_t e = cudaMemsetAsync(scratch, 0, (size_t)nstack * 32, st);
-        if (e != cudaSuccess) return e;
-        const int sms = device_attr(cudaDevAttrMultiProcessorCount);
         for (int64_t s = 0; s < nstack; ++s) {
             unsigned* g = scratch + 8 * s;
-            k_fold_big_a<<<(unsigned)(2 * sms), 256, 0, st>>>(acc + s * (stack_points / 512), stack_points, g);
-            k_fold_big_b<<<(unsigned)(8 * sms), 256, 0, st>>>(minw + s * (stack_points / 32), stack_points, c, g);
-            k_fold_big_c<<<1, 1, 0, st>>>(g, stack_points, c, out, kvec, s);
-            note_launch();
-            note_launch();
-            note_launch();
+            cudaError_t e = launch_fold_reduce(acc + s * (stack_points / 512), minw + s * (stack_points / 32),
+                                               stack_points, c, 0, g, st);
+            if (e == cudaSuccess)
+                e = launch_fold_reduce(acc + s * (stack_points / 512), minw + s * (stack_points / 32), stack_points, c,
+                                       1, g, st);
+            if (e == cudaSuccess) e = launch_fold_finish(g, stack_points, c, out, kvec, s, st);
+            if (e != cudaSuccess) return e;
         }
         return cudaGetLastError();
     }

@@ -32,7 +32,8 @@ from . import _native
 from .errors import InvalidValue, UnsupportedSize
 from .prescale import PrescaleConfig, PrescaleResult, k_from_stats
 
-__all__ = ["shard_range", "Comm", "CudaOps", "compute_prescale_global", "fft2_slab", "pipeline_slab"]
+__all__ = ["shard_range", "Comm", "CudaOps", "compute_prescale_global", "prescale_fold_slab", "fft2_slab",
+           "pipeline_slab"]
 
 
 def shard_range(n_items: int, rank: int, world: int):
@@ -115,6 +116,44 @@ class CudaOps:
         _native.check(_native.lib().mxfft_fft_rows_seg(plan.handle, recv.data_ptr(), y.data_ptr(), R, int(inverse),
                                                        int(exp_in), int(exp_out), R, _native.stream_handle()))
         return y
+
+    def rows_evidence(self, x, plan, inverse: bool = False):
+        """The first row pass on the unscaled input plus the evidence words of
+        the folded prescale (mxfft_fft_rows_evidence) -> (rows, words)."""
+        import torch
+
+        L = _native.lib()
+        y = torch.empty_like(x)
+        nb = int(L.mxfft_fold_words_bytes(x.numel()))
+        words = torch.empty(max(nb, 1), dtype=torch.uint8, device=x.device)
+        _native.check(L.mxfft_fft_rows_evidence(plan.handle, x.data_ptr(), y.data_ptr(), x.numel() // plan.n,
+                                                int(inverse), words.data_ptr(), nb, _native.stream_handle()))
+        return y, words
+
+    def fold_reduce(self, words, npoints: int, cfg: PrescaleConfig, step: int, g=None):
+        """One reduction step of the folded prescale over this rank's words;
+        g: int32 tensor of 8 words (bit patterns of uint32), created by step 0."""
+        import torch
+
+        if g is None:
+            g = torch.empty(8, dtype=torch.int32, device=words.device)
+        c = cfg.as_c()
+        _native.check(_native.lib().mxfft_fold_reduce(words.data_ptr(), npoints, ctypes.byref(c), step, g.data_ptr(),
+                                                      _native.stream_handle()))
+        return g
+
+    def fold_finish(self, g, total_points: int, cfg: PrescaleConfig):
+        """-> the result row (numpy record: k, k1, flags, a_max, ...) from the combined words."""
+        import torch
+
+        from .prescale import decode_results
+
+        res = torch.empty((1, _native.PRESCALE_RESULT_DTYPE.itemsize), dtype=torch.uint8, device=g.device)
+        k = torch.empty(1, dtype=torch.int32, device=g.device)
+        c = cfg.as_c()
+        _native.check(_native.lib().mxfft_fold_finish(g.data_ptr(), total_points, ctypes.byref(c), res.data_ptr(),
+                                                      k.data_ptr(), _native.stream_handle()))
+        return decode_results(res)[0]  # (synchronizes: the one read-back of the folded prescale)
 
     def sample_keys(self, x, nsamples: int):
         import torch
@@ -287,13 +326,16 @@ def _transpose_slabs(a, comm: Comm, ops):
 
 
 def fft2_slab(x_slab, plan, mode: str = "forward", comm: Comm = None, ops=None, k: int = 0,
-              restore: bool = True):
+              restore: bool = True, first_pass=None):
     """fft_2d (fftcore.py:344-353) of one N x N image whose rows are split across
     the ranks of `comm`; x_slab is this rank's (N/G, N) complex64 row slab.
     mode: "forward" | "inverse" | "roundtrip" (forward, inverse, x 1/N^2).
     k: prescale exponent, x 2^k on the first load and 2^-k on the last store.
     Returns this rank's rows of the result (restore=True), else its rows of
-    the transposed result (one all-to-all fewer)."""
+    the transposed result (one all-to-all fewer).
+    first_pass: the first row pass's output when it already ran on the
+    UNSCALED slab (the folded prescale, pipeline_slab): x 2^k then moves to the
+    load of the second pass, which is exact."""
     comm = comm or Comm(enabled=False)
     ops = ops or CudaOps()
     N = plan.n
@@ -306,10 +348,13 @@ def fft2_slab(x_slab, plan, mode: str = "forward", comm: Comm = None, ops=None, 
             "roundtrip": (False, False, True, True)}[mode]
     out_exp = -k - (2 * plan.stages if mode == "roundtrip" else 0)
     y = x_slab.contiguous()
+    k_at = 0 if first_pass is None else 1  # the pass whose load applies 2^k
     for i, inv in enumerate(dirs):
-        first, last = i == 0, i == len(dirs) - 1
-        e_in, e_out = (k if first else 0), (out_exp if last else 0)
-        if i == 0:
+        last = i == len(dirs) - 1
+        e_in, e_out = (k if i == k_at else 0), (out_exp if last else 0)
+        if i == 0 and first_pass is not None:
+            y = first_pass
+        elif i == 0:
             y = ops.rows(y, plan, inv, exp_in=e_in, exp_out=e_out)
         elif hasattr(ops, "rows_seg"):
             # every later pass works on the rows of the previous result's
@@ -320,10 +365,70 @@ def fft2_slab(x_slab, plan, mode: str = "forward", comm: Comm = None, ops=None, 
     return _transpose_slabs(y, comm, ops) if restore else y
 
 
-def pipeline_slab(x_slab, plan, cfg: PrescaleConfig, roundtrip: bool, comm: Comm = None, ops=None):
+def _u32(g):
+    """int32 bit patterns -> int64 values in [0, 2^32) (all-reduce MAX / SUM on unsigned words)."""
+    import torch
+
+    return g.to(torch.int64) & 0xFFFFFFFF
+
+
+def _i32(a):
+    """int64 values in [0, 2^32) -> the int32 tensor with the same bit patterns."""
+    import torch
+
+    return (((a + 2**31) % 2**32) - 2**31).to(torch.int32)
+
+
+def prescale_fold_slab(x_slab, plan, cfg: PrescaleConfig, comm: Comm, ops):
+    """compute_prescale (prescale.py:61-73) over the whole image FOLDED into the
+    first row pass of this rank's slab: the pass runs unscaled and gathers the
+    evidence (mxfft_fft_rows_evidence); two small all-reduces combine it (MAX
+    of the peak key / exponent range, then SUM of the counts under the global
+    threshold) and every rank settles the same k (mxfft_fold_finish) with one
+    read-back.  Returns (first-pass rows, result row); row["flags"] & 4: the
+    proofs declined and the caller takes the statistics path."""
+    import torch
+
+    npts = x_slab.numel()
+    y1, words = ops.rows_evidence(x_slab, plan, False)
+    g = ops.fold_reduce(words, npts, cfg, 0)
+    if comm.world > 1:
+        a = _u32(g[:4])
+        comm.max_(a)
+        g[:4] = _i32(a)
+    ops.fold_reduce(words, npts, cfg, 1, g)
+    if comm.world > 1:
+        cnt, mn = _u32(g[4:6]), _u32(g[6:7])
+        comm.sum_(cnt)
+        comm.max_(mn)
+        g[4:6] = _i32(cnt)
+        g[6:7] = _i32(mn)
+    return y1, ops.fold_finish(g, plan.n * plan.n, cfg)  # (the slabs partition one n x n image)
+
+
+def pipeline_slab(x_slab, plan, cfg: PrescaleConfig, roundtrip: bool, comm: Comm = None, ops=None,
+                  fold=None, restore: bool = True):
     """The C5 pipeline on row slabs: global prescale, then the 2-D transform
     with the scalings fused (forward_pipeline / roundtrip_pipeline,
-    mri.py:84-107, for one coil).  Returns (this rank's rows of the output, k)."""
+    mri.py:84-107, for one coil).  Returns (this rank's rows of the output, the
+    prescale result).
+
+    fold (default: on when the backend provides it and n = 16384): the
+    prescale rides on the first row pass (prescale_fold_slab) -- no statistics
+    pass over the slab, one host read-back instead of several.  If its proofs
+    decline, the statistics path below runs instead; results are identical."""
+    comm = comm or Comm(enabled=False)
+    ops = ops or CudaOps()
+    mode = "roundtrip" if roundtrip else "forward"
+    use_fold = (hasattr(ops, "rows_evidence") and plan.n == 16384) if fold is None else fold
+    if use_fold:
+        y1, row = prescale_fold_slab(x_slab, plan, cfg, comm, ops)
+        if not int(row["flags"]) & 4:
+            res = PrescaleResult(k=int(row["k"]), a_max=float(row["a_max"]), p_tau=float(row["p_tau"]),
+                                 k1=int(row["k1"]), k2=int(row["k2"]))
+            y = fft2_slab(x_slab, plan, mode, comm, ops, k=res.k, restore=restore, first_pass=y1)
+            return y, res
+        del y1
     res = compute_prescale_global(x_slab, cfg, comm, ops)
-    y = fft2_slab(x_slab, plan, "roundtrip" if roundtrip else "forward", comm, ops, k=res.k)
+    y = fft2_slab(x_slab, plan, mode, comm, ops, k=res.k, restore=restore)
     return y, res

@@ -4,6 +4,8 @@ first row pass of fft_2d, fftcore.py:344-353) against the standard path
 (statistics kernels + mxfft_fft2) and the oracle.  Settled stacks must be
 bit-identical; stacks the in-kernel proofs cannot settle must be flagged and
 come out identical after pipeline_resolve."""
+import math
+
 import numpy as np
 import pytest
 
@@ -225,3 +227,48 @@ def test_fold_c5_full_size_equals_standard(mx, torch):
     x[0, :4096] *= 1e-12
     _, _, r2 = mx.pipeline_device(x, p, cfg, False, fold=True)
     assert int(_rows(mx, r2)[0]["flags"]) == 4
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_fold_slab_pipeline_threads_c5(mx, torch, G):
+    """pipeline_slab with the folded prescale (first row pass with evidence, two
+    small all-reduces, one read-back), G ranks as threads on one GPU at the
+    C5 size: every rank's slab equals the single-GPU pipeline, k included; a
+    slab pipeline without the fold gives the same bits."""
+    import threading
+
+    from paper_2512_04317_b200 import distributed as D
+    from paper_2512_04317_b200.workloads import ellipse_kspace_device
+    from test_gpu_r2 import ThreadComm
+
+    n = 16384
+    x = ellipse_kspace_device(n, 7, noise=0.01)
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.E4M3, 32))
+    cfg = mx.PrescaleConfig()
+    want, kw, _ = mx.pipeline_device(x[None], p, cfg, False)
+    torch.cuda.synchronize()
+    shared = {"world": G, "bar": threading.Barrier(G), "box": [None] * G}
+    out = [None] * G
+    errs = []
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                r0, r1 = D.shard_range(n, r, G)
+                y, res = D.pipeline_slab(x[r0:r1], p, cfg, False, comm=ThreadComm(shared, r), fold=True)
+                assert math.isnan(res.p_tau)  # the folded path (k-only), not the statistics fallback
+                torch.cuda.current_stream().synchronize()
+                out[r] = (torch.equal(torch.view_as_real(y), torch.view_as_real(want[0, r0:r1])), res.k)
+        except BaseException as e:  # surface any rank's failure
+            errs.append(e)
+            shared["bar"].abort()
+
+    ts = [threading.Thread(target=rank_main, args=(r,)) for r in range(G)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs[0]
+    assert all(k == int(kw[0]) for _, k in out)
+    assert all(ok for ok, _ in out)
