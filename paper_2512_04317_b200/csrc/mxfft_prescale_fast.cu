@@ -1419,8 +1419,13 @@ __device__ void fold_k1(unsigned kmx, const mxfft_prescale_cfg& c, double& a_est
     T = k1_ok ? __double2float_ru(ldexp(c.tau_min, -k1) * (1.0 + 0x1p-20)) : 0.f;
 }
 
+// At most 32 registers (launch bounds; the FP64 part spills a little, which does not matter here):
+// a 128-thread CTA must fit into the registers the first pass's resident CTAs leave free -- 3 x 128
+// threads x 152 registers leave 7168, x 153 (allocated as 160) only 4096 -- or the programmatic
+// launch chain first pass -> resolve -> second pass stops overlapping (measured: C2 round trip
+// 268 -> 302 us when the resolve CTAs do not fit)
 template <int FR_THREADS>
-__global__ void __launch_bounds__(FR_THREADS) k_fold_resolve(const unsigned* __restrict__ acc,
+__global__ void __launch_bounds__(FR_THREADS, 2048 / FR_THREADS) k_fold_resolve(const unsigned* __restrict__ acc,
                                                              const unsigned* __restrict__ minw, int64_t stack_points,
                                                              mxfft_prescale_cfg c, mxfft_prescale_result* out,
                                                              int32_t* kvec) {
@@ -1434,8 +1439,13 @@ __global__ void __launch_bounds__(FR_THREADS) k_fold_resolve(const unsigned* __r
     // the thread words of the stack (stack_points / 32, a multiple of 512): first batch in flight
     const uint4* w4 = reinterpret_cast<const uint4*>(minw + s * (stack_points / 32));
     const int64_t n4 = stack_points / 128;
-    uint4 first = make_uint4(0xffffffc0u, 0xffffffc0u, 0xffffffc0u, 0xffffffc0u);
-    if (tid < n4) first = __ldg(w4 + tid);
+    constexpr int PRE = 4;  // 16-byte loads in flight per thread
+    uint4 pre[PRE];
+#pragma unroll
+    for (int j = 0; j < PRE; ++j) {
+        const int64_t i = tid + j * FR_THREADS;
+        pre[j] = i < n4 ? __ldg(w4 + i) : make_uint4(0xffffffc0u, 0xffffffc0u, 0xffffffc0u, 0xffffffc0u);
+    }
     // the warps' words: largest key, exponent range, replay flag
     unsigned kmx = 0, hi_u = 0, lo_u = 0, rep = 0;
     {
@@ -1488,12 +1498,20 @@ __global__ void __launch_bounds__(FR_THREADS) k_fold_resolve(const unsigned* __r
             small += __uint_as_float(mb) < T;
         }
     };
-    for (int64_t i = tid; i < n4; i += FR_THREADS) {
-        const uint4 v = i == tid ? first : __ldg(w4 + i);
-        take(v.x);
-        take(v.y);
-        take(v.z);
-        take(v.w);
+    for (int64_t i0 = tid;; i0 += PRE * FR_THREADS) {
+#pragma unroll
+        for (int j = 0; j < PRE; ++j) {
+            take(pre[j].x);
+            take(pre[j].y);
+            take(pre[j].z);
+            take(pre[j].w);
+        }
+        if (i0 + PRE * FR_THREADS >= n4 + tid) break;  // (n4 is a multiple of the batch or smaller than one)
+#pragma unroll
+        for (int j = 0; j < PRE; ++j) {
+            const int64_t i = i0 + (PRE + j) * FR_THREADS;
+            pre[j] = i < n4 ? __ldg(w4 + i) : make_uint4(0xffffffc0u, 0xffffffc0u, 0xffffffc0u, 0xffffffc0u);
+        }
     }
     zeros = __reduce_add_sync(0xffffffffu, zeros);
     small = __reduce_add_sync(0xffffffffu, small);
