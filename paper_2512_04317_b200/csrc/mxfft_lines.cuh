@@ -1258,8 +1258,10 @@ __device__ __forceinline__ void lines_body_pipe(const MxLinesArgs& a) {
 // threads each hold 32 points, so thread words sit at grp * blockDim + tid and
 // warp words at 2 (grp * warps + warp).
 // ---------------------------------------------------------------------------
+template <int NT>
 __device__ __forceinline__ void fold_points(const float2 (&x)[32], const MxLinesArgs& a, int64_t grp) {
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const int tid = threadIdx.x;
+    constexpr int nt = NT;
     unsigned acc_key = 0, mn_all = 0xffffffffu;
 #pragma unroll
     for (int m = 0; m < 32; ++m) {
@@ -1282,8 +1284,10 @@ __device__ __forceinline__ void fold_points(const float2 (&x)[32], const MxLines
     acc_key = __reduce_max_sync(0xffffffffu, acc_key);
     if ((tid & 31) == 0) a.acc[(grp * (nt >> 5) + (tid >> 5)) * 2] = acc_key;
 }
+template <int NT>
 __device__ __forceinline__ void fold_range(const BadTrack& bad, const MxLinesArgs& a, int64_t grp) {
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const int tid = threadIdx.x;
+    constexpr int nt = NT;
     const int hi_ = __reduce_max_sync(0xffffffffu, bad.hi), lo_ = __reduce_min_sync(0xffffffffu, bad.lo);
     const unsigned b_ = __ballot_sync(0xffffffffu, bad.b);
     if ((tid & 31) == 0)
@@ -1404,7 +1408,7 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
             const unsigned ad = (gaddr ^ ((unsigned)(m & (MS - 1)) * (T * 8u))) + (unsigned)(m / MS) * (LPC * 128u);
             x[rev_c<5>(m)] = lds64(ad);
         }
-        if constexpr (ACC) fold_points(x, a, grp);
+        if constexpr (ACC) fold_points<NT>(x, a, grp);
         if (nxt < ngroups) kk_nxt = k_of(nxt);
         // n <= 256: split barriers instead of one __syncthreads.  Only warp 0 waits for every
         // warp's gather (barrier 1: X is in registers, free for the next tile) before thread 0
@@ -1436,7 +1440,7 @@ __device__ __forceinline__ void lines_body_tma(const MxLinesArgs& a) {
         run_stages<ID, CPB, false, LT>(x, U, V, P, H, L, by, ebase, &dbg, bad, y_free);
         if (kout) scale32<false>(x, kout, bad);
         const int64_t gl = grp * LPC;  // first line of the group: column gl mod n of image gl / n
-        if constexpr (ACC) fold_range(bad, a, grp);
+        if constexpr (ACC) fold_range<NT>(bad, a, grp);
         if (__syncthreads_or(bad)) {
             replay_lines(a, gl, LPC, y_g, 5 - LT, W * 32, LPR - 1);
             float2* dst = a.out + (gl >> LN) * (int64_t)N * N + (gl & (N - 1));
@@ -1534,7 +1538,7 @@ __device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
             for (int m = 0; m < 32; ++m) x[rev_c<5>(m)] = __ldg(src + m * stride);
             if (kin) scale32<DBG>(x, kin, bad);
         }
-        if constexpr (ACC) fold_points(x, a, grp);  // (the folded first pass runs unscaled: kin == 0)
+        if constexpr (ACC) fold_points<(LT >= 0 ? (1 << (LT >= 0 ? LT : 0)) : 1)>(x, a, grp);  // (the folded first pass runs unscaled: kin == 0; ACC kernels have a compile-time LT)
 #if MXFFT_BIG_PREFETCH
         // while this line computes, its successor (a contiguous row) streams into
         // L2, so the next load phase hits L2 instead of waiting on HBM
@@ -1554,7 +1558,7 @@ __device__ __forceinline__ void lines_body_direct(const MxLinesArgs& a) {
         int U, V, P, H;
         run_stages<ID, CPB, DBG, LT>(x, U, V, P, H, L, rb, ebase, &dbg, bad);
         if (kout) scale32<DBG>(x, kout, bad);
-        if constexpr (ACC) fold_range(bad, a, grp);
+        if constexpr (ACC) fold_range<(LT >= 0 ? (1 << (LT >= 0 ? LT : 0)) : 1)>(bad, a, grp);
         if (!DBG && __syncthreads_or(bad)) {
             char* tile = reinterpret_cast<char*>(smem4 + a.tw_chunks);
             replay_lines(a, line, 1, tile, 0, N, 0);

@@ -1535,6 +1535,66 @@ __global__ void __launch_bounds__(FR_THREADS, 2048 / FR_THREADS) k_fold_resolve(
     fold_finish(kmx, hi_u, lo_u, rep, zeros, small, mn, a_est, k1, e_key, k1_ok, stack_points, c, out, kvec, s);
 }
 
+// Small stacks (<= 2^15 points, C4: one 128^2 image): one WARP per stack, four stacks per CTA --
+// no barriers, no shared memory, a quarter of the CTAs (C4: 4096 stacks)
+__global__ void __launch_bounds__(128, 16) k_fold_resolve_w(const unsigned* __restrict__ acc,
+                                                            const unsigned* __restrict__ minw, int64_t stack_points,
+                                                            int64_t nstack, mxfft_prescale_cfg c,
+                                                            mxfft_prescale_result* out, int32_t* kvec) {
+    pdl_launch_dependents();
+    pdl_wait();  // the first pass has finished
+    const int lane = threadIdx.x & 31;
+    const int64_t s = blockIdx.x * 4ll + (threadIdx.x >> 5);
+    if (s >= nstack) return;
+    const uint4* w4 = reinterpret_cast<const uint4*>(minw + s * (stack_points / 32));
+    const int n4 = (int)(stack_points / 128);  // <= 256: at most 8 per lane
+    const int nw = (int)(stack_points / 1024);  // <= 32
+    uint4 pre[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        pre[j] = lane + 32 * j < n4 ? __ldg(w4 + lane + 32 * j)
+                                    : make_uint4(0xffffffc0u, 0xffffffc0u, 0xffffffc0u, 0xffffffc0u);
+    unsigned kmx = 0, hi_u = 0, lo_u = 0, rep = 0;
+    if (lane < nw) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(acc) + s * nw + lane);
+        kmx = v.x;
+        hi_u = v.y >> 16;
+        lo_u = (v.y >> 4) & 0xfffu;
+        rep = v.y & 1u;
+    }
+    kmx = __reduce_max_sync(0xffffffffu, kmx);
+    hi_u = __reduce_max_sync(0xffffffffu, hi_u);
+    lo_u = __reduce_max_sync(0xffffffffu, lo_u);
+    rep = __reduce_or_sync(0xffffffffu, rep);
+    double a_est = 0.0;
+    int k1 = 0, e_key = 0;
+    bool k1_ok = false;
+    float T = 0.f;
+    if (lane == 0) fold_k1(kmx, c, a_est, k1, e_key, k1_ok, T);
+    T = __shfl_sync(0xffffffffu, T, 0);
+    unsigned zeros = 0, small = 0, mn = 0xffffffffu;
+    auto take = [&](unsigned v) {
+        const unsigned mb = v & ~63u;
+        zeros += v & 63u;
+        if (mb != 0xffffffc0u) {
+            mn = min(mn, mb);
+            small += __uint_as_float(mb) < T;
+        }
+    };
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        take(pre[j].x);
+        take(pre[j].y);
+        take(pre[j].z);
+        take(pre[j].w);
+    }
+    zeros = __reduce_add_sync(0xffffffffu, zeros);
+    small = __reduce_add_sync(0xffffffffu, small);
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    if (lane == 0)
+        fold_finish(kmx, hi_u, lo_u, rep, zeros, small, mn, a_est, k1, e_key, k1_ok, stack_points, c, out, kvec, s);
+}
+
 // One stack too large for one CTA (C5: 2^28 points): the same decision in three grid-wide steps
 // on a per-stack scratch g (8 words, zeroed): [0] largest key, [1] 128 + hi, [2] 128 - lo,
 // [3] replay flag, [4] zeros, [5] threads below T, [6] ~(smallest word).
@@ -1651,6 +1711,12 @@ cudaError_t launch_fold_resolve(const unsigned* acc, const unsigned* minw, int64
         return cudaGetLastError();
     }
     static const int nt_env = getenv("MXFFT_FR_THREADS") ? atoi(getenv("MXFFT_FR_THREADS")) : 0;
+    if (stack_points <= 32768 && nt_env != 128) {  // many small stacks: a warp per stack
+        cudaError_t e = launch_pdl(k_fold_resolve_w, (unsigned)((nstack + 3) / 4), 128u, 0, st, acc, minw, stack_points,
+                                   nstack, c, out, kvec);
+        note_launch();
+        return e != cudaSuccess ? e : cudaGetLastError();
+    }
     // few large stacks: more threads per stack
     // 128 threads: the CTAs then fit next to the first pass's (3 x 128 threads, ~150 registers) and the
     // programmatic launch chain first pass -> resolve -> second pass keeps overlapping (256 threads: C2

@@ -272,3 +272,56 @@ def test_fold_slab_pipeline_threads_c5(mx, torch, G):
     assert not errs, errs[0]
     assert all(k == int(kw[0]) for _, k in out)
     assert all(ok for ok, _ in out)
+
+
+@pytest.mark.parametrize("fmt,bsz,n", [("e4m3", 32, 128), ("e5m2", 16, 128), ("e2m1", 64, 256), ("e3m2", 32, 512)])
+def test_fold_randomized_against_standard(mx, torch, fmt, bsz, n):
+    """Randomized stress of the fold's proofs: images with random power-of-two
+    gains over 2^+-70, random fractions of exact zeros, sparse images, heavy
+    tails, isolated and clustered tiny values, constant images.  Whatever the
+    fold settles must equal the statistics path bit for bit (k and outputs);
+    whatever it declines must do so after pipeline_resolve; nothing else may
+    happen."""
+    from paper_2512_04317_b200.workloads import ellipse_kspace_batch
+
+    rng = np.random.default_rng(1234 + n + bsz)
+    batch = 96 if n == 128 else 24
+    xh = ellipse_kspace_batch(batch, n, seed=600 + n, noise=0.02)
+    for i in range(batch):
+        kind = i % 8
+        if kind == 1:
+            xh[i] *= np.float32(2.0 ** rng.integers(-70, 70))
+        elif kind == 2:
+            xh[i][rng.random((n, n)) < rng.uniform(0.0, 0.99)] = 0
+        elif kind == 3:
+            xh[i] = 0
+            idx = rng.integers(0, n, (rng.integers(1, 40), 2))
+            xh[i][idx[:, 0], idx[:, 1]] = (rng.standard_normal(len(idx)) + 1j * rng.standard_normal(len(idx))).astype(np.complex64)
+        elif kind == 4:
+            xh[i] = ((rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+                     * 10.0 ** rng.uniform(-6, 6, (n, n))).astype(np.complex64)
+        elif kind == 5:
+            m = rng.random((n, n)) < rng.choice([1e-4, 1e-3, 0.02, 0.3])
+            xh[i][m] *= np.float32(1e-12)
+        elif kind == 6:
+            xh[i] = np.complex64(complex(rng.uniform(-3, 3), rng.uniform(-3, 3))) * np.float32(2.0 ** rng.integers(-20, 20))
+        elif kind == 7:
+            xh[i, : n // 2] *= np.float32(2.0 ** -rng.integers(10, 40))
+    x = torch.from_numpy(xh).cuda()
+    p = mx.make_plan(n, mx.ModeSpec.mx(mx.get_mx_format(fmt), bsz))
+    cfg = mx.PrescaleConfig()
+    for roundtrip in (False, True):
+        y0, k0, r0 = mx.pipeline_device(x, p, cfg, roundtrip, fold=False, fused=False)
+        assert mx.pipeline_resolve(x, y0, k0, r0, p, cfg, roundtrip) == 0
+        y1, k1, r1 = mx.pipeline_device(x, p, cfg, roundtrip, fold=True, fused=False)
+        flags = _rows(mx, r1)["flags"].copy()
+        assert set(np.unique(flags & ~2)) <= {0, 4, 8}, np.unique(flags)
+        for i in np.nonzero((flags & 4) == 0)[0]:
+            assert int(k1[i]) == int(k0[i]), (i, i % 8)
+            a, b = y1[i].cpu().numpy(), y0[i].cpu().numpy()
+            assert ((a == b) | (np.isnan(a) & np.isnan(b))).all(), (i, i % 8)
+        assert (flags[::8] == 8).all()  # the untouched phantoms are always settled
+        mx.pipeline_resolve(x, y1, k1, r1, p, cfg, roundtrip)
+        assert torch.equal(k0, k1)
+        a, b = y1.cpu().numpy(), y0.cpu().numpy()
+        assert ((a == b) | (np.isnan(a) & np.isnan(b))).all()
