@@ -82,8 +82,14 @@ def _worker(rank, world, port, n, seed, q):
         fwd = D.fft2_slab(slab, plan, "forward", comm, ops).numpy()
         fwd_t = D.fft2_slab(slab, plan, "forward", comm, ops, restore=False).numpy()
         inv = D.fft2_slab(slab, plan, "inverse", comm, ops).numpy()
-        rt, res2 = D.pipeline_slab(slab, plan, PrescaleConfig(), True, comm, ops)
-        q.put((rank, r0, r1, res, fwd, fwd_t, inv, rt.numpy(), res2))
+        rt, res2 = D.pipeline_slab(slab, plan, PrescaleConfig(), True, comm, ops, fold=False)
+        # the folded prescale: first pass with evidence, two all-reduces, every rank the same k
+        rt_f, res_f = D.pipeline_slab(slab, plan, PrescaleConfig(), True, comm, ops, fold=True)
+        # a configuration in which k2 wins: the fold declines on every rank and the statistics path runs
+        cfg2 = PrescaleConfig(tau_min=0.5)
+        rt_d, res_d = D.pipeline_slab(slab, plan, cfg2, True, comm, ops, fold=True)
+        res_s = D.compute_prescale_global(slab, cfg2, comm, ops, nsamples=1 << 10)
+        q.put((rank, r0, r1, res, fwd, fwd_t, inv, rt.numpy(), res2, rt_f.numpy(), res_f, res_d, res_s))
     finally:
         dist.destroy_process_group()
 
@@ -108,7 +114,10 @@ def test_row_slabs_gloo_match_single_image_oracle(world):
     f = O.fft2(x, oplan, False)
     fi = O.fft2(x, oplan, True)
     out_o, _, k_o = O.pipeline(x, oplan, True)
-    for rank, r0, r1, res, fwd, fwd_t, inv, rt, res2 in outs:
+    for rank, r0, r1, res, fwd, fwd_t, inv, rt, res2, rt_f, res_f, res_d, res_s in outs:
+        assert res_f.k == k_o and np.isnan(res_f.p_tau)  # settled by the fold (k-only result)
+        np.testing.assert_array_equal(rt_f.astype(np.complex128), out_o[0][r0:r1])
+        assert res_d.k == res_s.k and res_d.p_tau == res_s.p_tau and res_s.k2 > res_s.k1  # declined -> statistics
         assert (res.k, res.a_max, res.p_tau) == (k, a_max, p_tau)
         assert res2.k == k_o
         np.testing.assert_array_equal(fwd, f[r0:r1])
