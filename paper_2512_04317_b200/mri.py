@@ -274,7 +274,7 @@ _HOST_GRAPHS_MAX = 4
 
 
 def pipeline_host(x_host, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, out_host=None,
-                  coils: int = 1, chunks: int = 12, graph: bool = True):
+                  coils: int = 1, chunks: int = 14, graph: bool = True):
     """pipeline_device for a batch in (pinned) host memory -- see
     _pipeline_host_eager for the slicing and stream overlap.
 
