@@ -284,9 +284,12 @@ def test_fold_randomized_against_standard(mx, torch, fmt, bsz, n):
     happen."""
     from paper_2512_04317_b200.workloads import ellipse_kspace_batch
 
-    rng = np.random.default_rng(1234 + n + bsz)
+    import os
+
+    soak = int(os.environ.get("MXFFT_FOLD_SOAK", "0"))  # other seeds for soak runs (tools/fold_soak.sh)
+    rng = np.random.default_rng(1234 + n + bsz + 1000 * soak)
     batch = 96 if n == 128 else 24
-    xh = ellipse_kspace_batch(batch, n, seed=600 + n, noise=0.02)
+    xh = ellipse_kspace_batch(batch, n, seed=600 + n + 7919 * soak, noise=0.02)
     for i in range(batch):
         kind = i % 8
         if kind == 1:
