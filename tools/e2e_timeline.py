@@ -11,7 +11,7 @@ import paper_2512_04317_b200 as mx  # noqa: E402
 from paper_2512_04317_b200.mri import pipeline_device  # noqa: E402
 from paper_2512_04317_b200.workloads import ellipse_kspace_batch  # noqa: E402
 
-B, n = 256, 256
+B, n = int(os.environ.get("TL_B", "256")), int(os.environ.get("TL_N", "256"))
 chunks = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 x = ellipse_kspace_batch(B, n, seed=0)
 hx = torch.from_numpy(x).pin_memory()
