@@ -108,6 +108,10 @@ FUSED = os.environ.get("MXFFT_FUSED", "0") == "1"
 # in-kernel proofs cannot settle come back with flag bit 2 and are re-run by
 # pipeline_resolve through the statistics kernels.  MXFFT_FOLD=0 turns it off.
 FOLD = os.environ.get("MXFFT_FOLD", "1") == "1"
+# (plan, config) pairs for which pipeline_resolve found the fold unproductive (more than a
+# quarter of a call's stacks unsettled, e.g. a configuration in which k2 wins): later default calls
+# run the statistics kernels directly instead of transforming twice.  fold=True still forces it.
+_FOLD_UNPRODUCTIVE = set()
 
 
 def fused_pipeline_supported(plan: FftPlan, coils: int = 1) -> bool:
@@ -169,7 +173,7 @@ def pipeline_device(x, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, coil
                                                          int(bool(roundtrip)), ctypes.byref(c), res.data_ptr(),
                                                          k.data_ptr(), _native.stream_handle()))
         return y, k, res
-    use_fold = FOLD if fold is None else fold
+    use_fold = (FOLD and (id(plan), repr(cfg)) not in _FOLD_UNPRODUCTIVE) if fold is None else fold
     if (use_fold and not use_fused and x.is_cuda and nstack > 0 and folded_pipeline_supported(plan)
             and (out is None or out.data_ptr() != x.data_ptr())):
         import torch
@@ -215,6 +219,8 @@ def pipeline_resolve(x, y, k, res, plan: FftPlan, cfg: PrescaleConfig, roundtrip
             pipeline_device(x[sl], plan, cfg, roundtrip, coils=coils, out=y[sl], k=k[a:b], res=res[a:b],
                             fused=False, fold=False)
         redo += int(unsettled.size)
+        if 4 * unsettled.size > r.size:
+            _FOLD_UNPRODUCTIVE.add((id(plan), repr(cfg)))
         r = decode_results(res)
     bad = np.nonzero(r["flags"] & 1)[0]
     if bad.size:
@@ -328,6 +334,8 @@ def _resolve_host(x_host, out_host, stats, plan, cfg, roundtrip, coils):
         return
     r = decode_results(torch.cat([t for t in stats])).copy()
     mode = "roundtrip" if roundtrip else "forward"
+    if 4 * int((r["flags"] & 4 != 0).sum()) > r.size:
+        _FOLD_UNPRODUCTIVE.add((id(plan), repr(cfg)))  # (a captured graph keeps its fold; eager calls drop it)
     for i in np.nonzero(r["flags"] & 4)[0]:
         # a stack the folded pipeline could not settle: statistics kernels + standard passes
         # from the host copy; its full row then goes through the checks below

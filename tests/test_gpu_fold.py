@@ -173,6 +173,11 @@ def test_fold_custom_config_where_k2_wins(mx, torch):
     assert (_rows(mx, r1)["flags"] == 4).all()
     assert mx.pipeline_resolve(x, y1, k1, r1, p, cfg, True) == 4
     assert torch.equal(k0, k1) and _same(torch, y0, y1)
+    # the resolve has noted that the fold does not pay for this plan and configuration: the next
+    # default call goes straight to the statistics kernels (full rows, nothing to resolve)
+    y2, k2, r2 = mx.pipeline_device(x, p, cfg, True, fused=False)
+    assert not (_rows(mx, r2)["flags"] & (4 | 8)).any()
+    assert torch.equal(k0, k2) and _same(torch, y0, y2)
 
 
 @pytest.mark.parametrize("graph", [False, True])
