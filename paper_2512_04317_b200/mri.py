@@ -301,7 +301,7 @@ def pipeline_host(x_host, plan: FftPlan, cfg: PrescaleConfig, roundtrip: bool, o
         return _pipeline_host_eager(x_host, plan, cfg, roundtrip, out_host, coils, chunks)
     dev = torch.cuda.current_device()
     key = (dev, x_host.data_ptr(), out_host.data_ptr(), tuple(x_host.shape), id(plan), plan.n,
-           repr(cfg), bool(roundtrip), int(coils), int(chunks))
+           repr(cfg), bool(roundtrip), int(coils), int(chunks), (id(plan), repr(cfg)) in _FOLD_UNPRODUCTIVE)
     ent = _HOST_GRAPHS.get(key)
     if ent is None or ent[1] is not plan:
         _pipeline_host_eager(x_host, plan, cfg, roundtrip, out_host, coils, chunks)  # warm-up
@@ -335,7 +335,7 @@ def _resolve_host(x_host, out_host, stats, plan, cfg, roundtrip, coils):
     r = decode_results(torch.cat([t for t in stats])).copy()
     mode = "roundtrip" if roundtrip else "forward"
     if 4 * int((r["flags"] & 4 != 0).sum()) > r.size:
-        _FOLD_UNPRODUCTIVE.add((id(plan), repr(cfg)))  # (a captured graph keeps its fold; eager calls drop it)
+        _FOLD_UNPRODUCTIVE.add((id(plan), repr(cfg)))  # (pipeline_host then captures a new graph without the fold)
     for i in np.nonzero(r["flags"] & 4)[0]:
         # a stack the folded pipeline could not settle: statistics kernels + standard passes
         # from the host copy; its full row then goes through the checks below
