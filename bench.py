@@ -462,6 +462,21 @@ def measure_batch(ctx, name, c, steps, warmup, graph=True, e2e=False, cpu_second
     except Exception:
         pass
 
+    # the pass's second roofline: instruction issue.  Executed warp
+    # instructions per launch from the committed ncu captures; issue rate = SMs x 4 x SM clock
+    issue = None
+    try:
+        winst = (json.load(open(os.path.join(ROOT, "profiles", "instructions.json"))).get(name) or {}).get(
+            "mx_line_pass")
+        if winst and not (fused or (fused_ok and knob)):
+            props = torch.cuda.get_device_properties(ctx.local)
+            rate = props.multi_processor_count * 4 * (clk.summary().get("sm_mhz") or 1965) * 1e6
+            issue = {"warp_instructions_per_launch": winst, "issue_floor_ms": winst / rate * 1e3,
+                     "frac_of_issue_rate": winst / rate * 1e3 / ms_dom,
+                     "hbm_floor_ms": BYTES_PER_POINT * pts / (peak * 1e9) * 1e3}
+    except Exception:
+        pass
+
     rec = {
         "value": world * pts / (ms * 1e-3) / 1e9, "unit": "Gpoints/s", "ms_per_step": ms,
         "hbm_fraction": pts / (ms * 1e-3) / 1e9 * BYTES_PER_POINT / peak,
@@ -470,7 +485,7 @@ def measure_batch(ctx, name, c, steps, warmup, graph=True, e2e=False, cpu_second
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "peak_source": peak_src,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": BYTES_PER_POINT * pts, "kernel_ms": kernels,
-                     "share_of_step": share},
+                     "share_of_step": share, "issue": issue},
         "gpu_launches": int(launches),
         "launch": "eager" if not graph else "CUDA graph replay of the captured step",
         "clocks": clk.summary(),
